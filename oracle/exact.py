@@ -1,0 +1,121 @@
+"""Exact references and the DoS reconstruction, numpy/scipy (O4-O7).
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).  Each function cites the
+passage it writes out.
+"""
+from __future__ import annotations
+
+from fractions import Fraction
+
+import numpy as np
+
+
+def exact_moments_from_eigs(lam, a: float, b: float, N: int, chunk: int = 1 << 16) -> np.ndarray:
+    """Eq (13): mu_n = (1/D) sum_k T_n(E~_k), E~_k = (E_k - b)/a (Eq 8),
+    with T_n(x) = cos(n arccos x) (Eq 3).  x is clipped to [-1, 1] against rounding."""
+    lam = np.asarray(lam, dtype=np.float64).ravel()
+    x = np.clip((lam - b) / a, -1.0, 1.0)
+    th = np.arccos(x)
+    n = np.arange(N, dtype=np.float64)
+    acc = np.zeros(N, dtype=np.float64)
+    for s in range(0, len(th), chunk):
+        acc += np.cos(np.outer(n, th[s:s + chunk])).sum(axis=1)
+    return acc / len(lam)
+
+
+def exact_moments_dense(H, a: float, b: float, N: int) -> np.ndarray:
+    """O4: exact trace of T_n(H~) from dense diagonalisation of a tiny H (CSR or array)."""
+    Hd = H.dense() if hasattr(H, "dense") else np.asarray(H)
+    return exact_moments_from_eigs(np.linalg.eigvalsh(Hd), a, b, N)
+
+
+def lattice_spectrum(ndim: int, L, t: float) -> np.ndarray:
+    """O5: spectrum of the clean periodic nearest-neighbour lattice:
+    plane waves give E(k) = 2 t sum_d cos(2 pi k_d / L_d), k_d = 0..L_d-1."""
+    E = np.zeros(1)
+    for d in range(ndim):
+        e = 2.0 * t * np.cos(2.0 * np.pi * np.arange(L[d]) / L[d])
+        E = (E[:, None] + e[None, :]).ravel()
+    return E
+
+
+def harper_spectrum(L0: int, L1: int, t: float, flux: float) -> np.ndarray:
+    """O5 (Peierls): exact spectrum of the 2D lattice whose y-bond (x,y)->(x,y+1)
+    carries t e^{i 2 pi flux x} (reading X15).  With flux = p/q and plane waves
+    e^{i k_y y} e^{i k_x q X} (x = q X + s) H splits into L1 * L0/q Hermitian q x q
+    blocks: M_ss = 2t cos(2 pi flux s - k_y), M_{s,s+-1} = t, corner terms
+    t e^{+-i k_x q}.  k_y = 2 pi m / L1, k_x = 2 pi j / L0, j < L0/q."""
+    fr = Fraction(flux).limit_denominator(1 << 20)
+    q = fr.denominator
+    assert L0 % q == 0, "flux * L0 must be an integer"
+    out = []
+    s = np.arange(q)
+    for m in range(L1):
+        ky = 2.0 * np.pi * m / L1
+        for j in range(L0 // q):
+            kx = 2.0 * np.pi * j / L0
+            M = np.zeros((q, q), dtype=np.complex128)
+            M[s, s] += 2.0 * t * np.cos(2.0 * np.pi * float(fr) * s - ky)
+            for u in range(q):
+                v = u + 1
+                if v < q:
+                    M[u, v] += t
+                    M[v, u] += t
+                else:  # bond from cell X to X+1: psi(x + q) = e^{i kx q} psi(x)
+                    M[u, 0] += t * np.exp(1j * kx * q)
+                    M[0, u] += t * np.exp(-1j * kx * q)
+            out.append(np.linalg.eigvalsh(M))
+    return np.concatenate(out)
+
+
+def jackson(N: int) -> np.ndarray:
+    """Jackson kernel g_n, n = 0..N-1 (named at PAPER.md:25, formula from the paper's
+    ref [10], Weisse et al. RMP 78, 275; reading X8):
+    g_n = [(N-n+1) cos(pi n/(N+1)) + sin(pi n/(N+1)) cot(pi/(N+1))] / (N+1)."""
+    n = np.arange(N, dtype=np.float64)
+    q = np.pi / (N + 1)
+    return ((N - n + 1) * np.cos(q * n) + np.sin(q * n) / np.tan(q)) / (N + 1)
+
+
+def chebyshev_nodes(K: int) -> np.ndarray:
+    """x_k = cos(pi (k + 1/2) / K), k = 0..K-1 (reading X7)."""
+    return np.cos(np.pi * (np.arange(K) + 0.5) / K)
+
+
+def dos(mu, a: float, b: float, omega, kernel: str = "jackson") -> np.ndarray:
+    """Eq (6), mapped back to omega (Eq 11-12; reading X9):
+    rho(omega) = [g_0 mu_0 + 2 sum_{n=1}^{N-1} g_n mu_n T_n(x)] / (pi sqrt(1-x^2)) / a,
+    x = (omega - b)/a; rho = 0 for |x| >= 1 (reading X7)."""
+    mu = np.asarray(mu, dtype=np.float64)
+    N = len(mu)
+    g = jackson(N) if kernel == "jackson" else np.ones(N)
+    x = (np.asarray(omega, dtype=np.float64) - b) / a
+    out = np.zeros_like(x)
+    inside = np.abs(x) < 1.0
+    xi = x[inside]
+    c = g * mu
+    c[1:] *= 2.0
+    T = np.cos(np.outer(np.arccos(xi), np.arange(N)))  # T_n(x) = cos(n arccos x), Eq (3)
+    out[inside] = (T @ c) / (np.pi * np.sqrt(1.0 - xi * xi)) / a
+    return out
+
+
+def dos_closed_1d(E, t: float = -1.0) -> np.ndarray:
+    """O7: DoS of the infinite 1D chain, rho(E) = 1/(pi sqrt(4t^2 - E^2)), |E| < 2|t|."""
+    E = np.asarray(E, dtype=np.float64)
+    out = np.zeros_like(E)
+    m = np.abs(E) < 2 * abs(t)
+    out[m] = 1.0 / (np.pi * np.sqrt(4 * t * t - E[m] ** 2))
+    return out
+
+
+def dos_closed_2d(E, t: float = -1.0) -> np.ndarray:
+    """O7: DoS of the infinite square lattice, rho(E) = K(1 - E^2/16t^2) / (2 pi^2 |t|),
+    |E| < 4|t| (K the complete elliptic integral of the first kind, parameter m = k^2)."""
+    from scipy.special import ellipk
+    E = np.asarray(E, dtype=np.float64)
+    out = np.zeros_like(E)
+    m = (np.abs(E) < 4 * abs(t)) & (E != 0)
+    out[m] = ellipk(1.0 - E[m] ** 2 / (16 * t * t)) / (2 * np.pi ** 2 * abs(t))
+    out[E == 0] = np.inf
+    return out
