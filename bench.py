@@ -1,0 +1,291 @@
+#!/usr/bin/env python
+"""Benchmark of the KPM moment engine (BASELINE.json metric: D*N*R vector-element
+updates/s and HBM GB/s).
+
+One "step" = one whole kpm_moments call = the full hot path on one batch: generate
+R random vectors, first step, floor(N/2)-1 fused recursion steps, fixed-order
+finish, doubling assembly (and, for N > 1 ranks, the one all-reduce of the sums).
+Default workload: BASELINE.json configs[1] (2D square lattice 512x512, N=1024,
+R=64, fp64), whose vector block (2 x 134 MB) exceeds the 126 MB L2.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+Under torchrun each rank owns R vectors of its own (random-vector partition,
+weak scaling); rank 0 prints one JSON line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import kpm_inputs as ki  # noqa: E402
+
+METRIC = "KPM vector-element updates/s (D*N*R/s)"
+UNIT = "updates/s"
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [p.strip() for p in l.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def oracle_sample(cfg, lat, a, b, seconds_target=15.0):
+    """The oracle as it stands, on a bounded sample of the workload: full D and N,
+    R' = #threads vectors (more if that is quick).  Returns value in D*N*R/s."""
+    import oracle
+    H = oracle.lattice_csr(lat)
+    threads = oracle.num_threads()
+    Rs = threads
+    r = ki.rademacher(cfg["seed"], Rs, lat["D"])
+    t0 = time.perf_counter()
+    oracle.moments_doubling(H, a, b, r, cfg["N"])
+    dt = time.perf_counter() - t0
+    value = lat["D"] * cfg["N"] * Rs / dt
+    sample = (f"{Rs} of {cfg['R']} vectors (global vectors 0..{Rs - 1}) at full D={lat['D']} and N={cfg['N']}; "
+              f"{dt:.2f} s of CPU time on {threads} OpenMP threads; CSR build excluded")
+    return value, threads, sample, dt
+
+
+def run_reference(args, cfg, lat, a, b, rank, world):
+    if rank != 0:
+        return
+    steps = []
+    for i in range(args.warmup + args.steps):
+        v, threads, sample, dt = oracle_sample(cfg, lat, a, b)
+        if i >= args.warmup:
+            steps.append((v, dt))
+    value = statistics.median(v for v, _ in steps)
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * statistics.median(d for _, d in steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": config_obj(args, cfg, lat, world),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def config_obj(args, cfg, lat, world):
+    return {"workload": f"BASELINE.json configs[{int(args.config[1]) - 1}]: {cfg['name']}", "config": args.config,
+            "D": lat["D"], "N": cfg["N"], "R_per_gpu": cfg["R"], "R_total": cfg["R"] * world, "ndim": lat["ndim"],
+            "L": list(lat["L"]), "t": lat["t"], "anderson_W": cfg["W"], "flux": lat["flux"],
+            "vector_seed": cfg["seed"], "disorder_seed": cfg["disorder_seed"],
+            "parallelism": f"vectors{world}", "l2": "inputs larger than L2 (2 x D*R*s vector blocks)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(ki.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = ki.CONFIGS[args.config]
+    lat = ki.lattice(cfg)
+
+    if args.impl == "reference":
+        import oracle
+        a, b = oracle.gershgorin(oracle.lattice_csr(lat))
+        run_reference(args, cfg, lat, a, b, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_1105_5481_b200 import kpm
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    dev = torch.device("cuda", local_rank)
+
+    a, b = kpm.kpm_gershgorin_stencil(lat["ndim"], lat["L"], lat["t"], onsite=lat["onsite"], flux=lat["flux"])
+    N, R_loc = cfg["N"], cfg["R"]
+    R = R_loc * world
+    part = (kpm.KPM_PART_VECTORS, rank, world)
+    h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
+                               device=local_rank, dist=part)
+    stream = torch.cuda.Stream(device=dev)
+    h.set_stream(stream.cuda_stream)
+    ws_bytes = h.workspace_size(N, R)
+    ws = torch.empty(ws_bytes + 256, dtype=torch.uint8, device=dev)
+    base = (ws.data_ptr() + 255) // 256 * 256
+    h.set_workspace(base, ws_bytes)
+    S = torch.empty(N, dtype=torch.float64, device=dev)
+    mu = torch.empty(N, dtype=torch.float64, device=dev)
+
+    def step():
+        h.moments_ex(N, R, cfg["seed"], flags=kpm.KPM_RAW_SUMS | kpm.KPM_DEVICE_OUT, out=S.data_ptr())
+        if world > 1:
+            with torch.cuda.stream(stream):
+                dist.all_reduce(S)
+        h.assemble(S.data_ptr(), N, R, out=mu.data_ptr())
+
+    for _ in range(args.warmup):
+        step()
+    stream.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    steps_ms, step_launches, launches = 0.0, 0, 0
+    with ClockSampler(local_rank) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+            ms, sl, tl = h.last_timing()   # events the library records on its stream
+            steps_ms += ms
+            step_launches += sl
+            launches += tl + 1             # + the assemble kernel
+        ev1.record(stream)
+        stream.synchronize()
+    torch.cuda.synchronize(dev)
+    ms_total = ev0.elapsed_time(ev1)
+    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    ms_per_step = float(t.item()) / args.steps
+    D = lat["D"]
+    value = D * N * R / (ms_per_step / 1000.0)
+
+    # roofline of the dominant kernel: the fused recursion step
+    peak, peak_kind = peak_hbm()
+    step_bytes = h.step_bytes(R)
+    avg_step_ms = steps_ms / max(step_launches, 1)
+    achieved = step_bytes / (avg_step_ms / 1000.0) / 1e9
+    mu_host = mu.cpu().numpy()
+
+    # end-to-end through the public API with host buffers: create (H2D of H~'s data),
+    # moments (random vectors drawn on the GPU, as the paper does), D2H of mu.
+    e2e = None
+    if not args.no_e2e:
+        onsite_bytes = 0 if lat["onsite"] is None else lat["onsite"].nbytes
+        phase_bytes = 16 * lat["L"][0] if lat["flux"] else 0
+        pinned_onsite = None
+        if lat["onsite"] is not None:
+            pinned_onsite = torch.from_numpy(lat["onsite"]).pin_memory().numpy()
+
+        def e2e_step():
+            h2 = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=pinned_onsite,
+                                        flux=lat["flux"], device=local_rank, dist=part)
+            if world > 1:
+                out = kpm.moments_distributed(h2, N, R, cfg["seed"])
+            else:
+                out = h2.moments(N, R, cfg["seed"])
+            h2.close()
+            return out
+        e2e_step()
+        if world > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(max(1, min(args.steps, 5))):
+            e2e_out = e2e_step()
+        k = max(1, min(args.steps, 5))
+        e2e_ms = (time.perf_counter() - t0) * 1000 / k
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_ms = float(te.item())
+        assert np.array_equal(e2e_out, mu_host), "e2e result differs from the device-resident run"
+        e2e = {"value": D * N * R / (e2e_ms / 1000.0), "unit": UNIT, "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": int(onsite_bytes + phase_bytes + 64), "d2h_bytes_per_step": 8 * N,
+               "path": "kpm_create_stencil + kpm_moments (host mu) + kpm_destroy per step"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, threads, sample, _ = oracle_sample(cfg, lat, a, b)
+        cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Rademacher vectors, lattice H)",
+                "config": config_obj(args, cfg, lat, world),
+                "hbm_gbs_alg": step_bytes * (N // 2) / (ms_per_step / 1000.0) / 1e9 * world,
+                "roofline": {"bound": "hbm", "kernel": "kpm_step_kernel (fused SpMM + recursion + reductions)",
+                             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                             "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": step_bytes,
+                             "avg_launch_ms": avg_step_ms},
+                "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
+                                                        "max_abs_mu": float(np.abs(mu_host).max())}}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

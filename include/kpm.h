@@ -1,0 +1,186 @@
+/*
+ * kpm.h -- C ABI of the B200-native KPM moment engine (libkpm.so).
+ *
+ * The Kernel Polynomial Method (Zhang, Yamagiwa, Okumura, Yunoki, arxiv
+ * 1105.5481; PAPER.md = /root/reference/PAPER.md): estimate the Chebyshev
+ * moments of the density of states
+ *     mu_n = (1/D) Tr T_n(H~)                               (Eq 13)
+ * stochastically with R random vectors |r> (Eq 14-16) through
+ * the vector recursion |a_0> = |r>, |a_1> = H~|a_0>,
+ * |a_{n+1}> = 2 H~|a_n> - |a_{n-1}> (Eq 17-18), on the
+ * rescaled Hamiltonian H~ = (H - b)/a (Eq 8-9; a = alpha_-,
+ * b = alpha_+), using the doubling identities
+ *     mu_{2n} = 2<a_n|a_n> - mu_0,   mu_{2n+1} = 2<a_{n+1}|a_n> - mu_1,
+ * so that N moments cost floor(N/2) sparse-matrix x vector-block products.
+ * The DoS is rebuilt from Jackson-damped moments by Eq (6).
+ *
+ * Conventions (all entry points):
+ *  - Every call returns a kpm_status; nothing throws across the ABI.  On a
+ *    non-OK status kpm_last_error() returns a thread-local message.  After
+ *    KPM_ERR_CUDA the handle is unusable except for kpm_destroy.
+ *  - Input arrays are caller-owned HOST arrays, copied during the call, unless
+ *    a flag says "device".  Outputs are caller-allocated.  Device memory of a
+ *    handle is owned by the handle (cudaMalloc), or by the caller through
+ *    kpm_set_workspace (e.g. a torch tensor).
+ *  - Work is ordered on the handle's CUDA stream (kpm_set_stream; default: a
+ *    stream the handle creates).  Calls with host outputs synchronise it.
+ *  - Determinism: for a given handle, (N, R, seed) and GPU model, repeated
+ *    calls return bitwise-identical results (fixed-order reductions, no
+ *    floating-point atomics).
+ *  - Vectors are real Rademacher +-1 (Eq 14 asks only for real iid mean 0,
+ *    variance 1; reading X1): xi_{r,i} = 1 - 2*(mix64(key ^ ctr) >> 63),
+ *    key = mix64(seed + 0x9E3779B97F4A7C15), ctr = r * D + i over GLOBAL r and
+ *    i, mix64 = the splitmix64 finaliser.  They are generated on the fly on the
+ *    GPU; the set does not depend on the number of ranks.
+ *  - Normalisation: mu_n = (1/(D R)) sum_r <r|T_n(H~)|r> (Eq 16, 19).
+ *  - Layout on the device: the vector block is interleaved [site][vector]
+ *    (vector index fastest) so one matrix/stencil entry serves all R vectors.
+ */
+#ifndef KPM_H_
+#define KPM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct kpm_handle_s* kpm_handle;
+typedef int32_t kpm_status;
+
+enum {
+    KPM_OK = 0,
+    KPM_ERR_INVALID_ARG = 1, /* bad size, a <= 0, non-finite a/b, flux*L0 not integer, ... */
+    KPM_ERR_OOM = 2,         /* device allocation failed or workspace too small */
+    KPM_ERR_CUDA = 3,        /* CUDA runtime error (sticky) */
+    KPM_ERR_UNSUPPORTED = 4, /* valid request this build does not implement */
+    KPM_ERR_SPECTRUM = 5     /* |mu_n| > mu_0 (1 + 1e-8) or non-finite: [b-a, b+a] does not
+                                enclose the spectrum (Eq 8 requires it).  Output still written. */
+};
+
+/* Element type of H and of the vector block. */
+enum { KPM_REAL64 = 0, KPM_COMPLEX128 = 1 };
+
+/* Damping kernel g_n of Eq (6). */
+enum {
+    KPM_KERNEL_JACKSON = 0, /* g_n = [(N-n+1)cos(pi n/(N+1)) + sin(pi n/(N+1))cot(pi/(N+1))]/(N+1)
+                               (formula from its ref [10]; X8) */
+    KPM_KERNEL_NONE = 1     /* g_n = 1 (truncated series, Eq 1) */
+};
+
+/* kpm_moments_ex flags. */
+enum {
+    KPM_PER_VECTOR = 1u, /* out = [R_local][N] per-vector moments (1/D)<r|T_n(H~)|r> instead of mu[N] */
+    KPM_DIRECT = 2u,     /* the paper's own scheme, Eq (19): mu_n = <r|a_n>, N-1 products (validation) */
+    KPM_DEVICE_OUT = 4u, /* out is a device pointer */
+    KPM_RAW_SUMS = 8u,   /* out = raw sums S[N] over this rank's vectors, before normalisation and
+                            the doubling transform (for a cross-rank all-reduce; see kpm_assemble) */
+    KPM_DEVICE_IN = 16u  /* r0 is a device pointer */
+};
+
+/* Nearest-neighbour lattice Hamiltonian (the paper's model, PAPER.md:229:
+ * 3D cubic, 7 entries per row, zero diagonal, off-diagonal -1; periodic).
+ * Sites are numbered i = x + L[0]*(y + L[1]*z).  Unused dims must have L = 1. */
+typedef struct {
+    int32_t ndim;          /* 1, 2 or 3 */
+    int64_t L[3];          /* extents (each >= 2 for used dims) */
+    double t;              /* hopping on every bond (paper: -1) */
+    const double* onsite;  /* host [D] on-site energies eps_i (Anderson), or NULL (all 0) */
+    double flux;           /* ndim == 2 only: Peierls flux per plaquette phi; the bond
+                              (x,y)->(x,y+1) carries H[(x,y+1)][(x,y)] = t e^{+i 2 pi phi x}
+                              (Landau gauge, X15).  phi*L[0] must be an integer.
+                              phi != 0 makes H complex (KPM_COMPLEX128). */
+} kpm_stencil_desc;
+
+/* Partition of the work across ranks (one process per GPU).  NULL = one GPU. */
+enum { KPM_PART_NONE = 0, KPM_PART_VECTORS = 1 };
+typedef struct {
+    int32_t partition; /* KPM_PART_VECTORS: rank owns global vectors
+                          [R*rank/world, R*(rank+1)/world) (Eq 16 is a sum over independent r) */
+    int32_t rank;
+    int32_t world;
+} kpm_dist;
+
+/* ---- creation (host -> device upload of H~; "the CPU copies the data to
+ *      the VRAM") ------------------------------------------------------------------- */
+
+/* H given as a lattice stencil.  a > 0 and b are the rescaling of Eq (8):
+ * H~ = (H - b)/a.  device: CUDA ordinal.  dist may be NULL. */
+kpm_status kpm_create_stencil(const kpm_stencil_desc* desc, double a, double b, int32_t device,
+                              const kpm_dist* dist, kpm_handle* out);
+
+/* H given in CSR ("CRS"): rowptr int64[D+1], col int32[nnz] (0 <= col < D),
+ * val: double[nnz] (KPM_REAL64) or interleaved (re, im) double[2*nnz] (KPM_COMPLEX128).
+ * H must be Hermitian (not checked).  Converted to ELL on the host. */
+kpm_status kpm_create_csr(int64_t D, const int64_t* rowptr, const int32_t* col, const void* val,
+                          int32_t dtype, double a, double b, int32_t device, const kpm_dist* dist,
+                          kpm_handle* out);
+
+/* H given in ELL: K entries per row, col int32[K][D] (-1 = padding), val [K][D] of dtype. */
+kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* val, int32_t dtype,
+                          double a, double b, int32_t device, const kpm_dist* dist,
+                          kpm_handle* out);
+
+/* Gerschgorin bounds: E_upper = max_i (Re H_ii + sum_{j!=i} |H_ij|),
+ * E_lower = min_i (...); eps pads both (0 = none); returns a = (Eu-El)/2, b = (Eu+El)/2. */
+kpm_status kpm_gershgorin_stencil(const kpm_stencil_desc* desc, double eps, double* a, double* b);
+kpm_status kpm_gershgorin_csr(int64_t D, const int64_t* rowptr, const int32_t* col,
+                              const void* val, int32_t dtype, double eps, double* a, double* b);
+
+/* ---- execution ------------------------------------------------------------------- */
+
+/* Use this CUDA stream (a cudaStream_t; NULL = legacy default stream). */
+kpm_status kpm_set_stream(kpm_handle h, void* stream);
+
+/* Device bytes kpm_moments_ex needs for (N, R global, flags). */
+kpm_status kpm_workspace_size(kpm_handle h, int32_t N, int64_t R, uint32_t flags, size_t* bytes);
+
+/* Give the handle caller-owned device memory (>= kpm_workspace_size bytes, 256-B aligned).
+ * The caller keeps it alive until kpm_destroy or the next kpm_set_workspace. NULL = own. */
+kpm_status kpm_set_workspace(kpm_handle h, void* dev_ptr, size_t bytes);
+
+/* mu[0..N-1] (host) from R random vectors drawn from `seed`.  One GPU only
+ * (with KPM_PART_VECTORS and world > 1 use kpm_moments_ex + KPM_RAW_SUMS). */
+kpm_status kpm_moments(kpm_handle h, int32_t N, int64_t R, uint64_t seed, double* mu);
+
+/* General form.  R is the GLOBAL number of vectors; this rank runs its share R_local.
+ * r0: NULL = generate (see conventions); else this rank's start vectors, vector-major
+ *     [R_local][D] of real doubles (host, or device with KPM_DEVICE_IN).
+ * out: mu[N]; or [R_local][N] with KPM_PER_VECTOR; or S[N] with KPM_RAW_SUMS
+ *      (host, or device with KPM_DEVICE_OUT). */
+kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, const void* r0,
+                          uint32_t flags, void* out);
+
+/* Raw sums S[N] (summed over all ranks) -> mu[N]: mu_0 = S_0/(D R), mu_1 = S_1/(D R),
+ * mu_{2n} = 2 S_{2n}/(D R) - mu_0, mu_{2n+1} = 2 S_{2n+1}/(D R) - mu_1; with KPM_DIRECT
+ * mu_n = S_n/(D R).  KPM_DEVICE_OUT: S and mu are device pointers (handle's stream). */
+kpm_status kpm_assemble(kpm_handle h, const double* S, int32_t N, int64_t R, uint32_t flags,
+                        double* mu);
+
+/* Eq (6) mapped back to omega (Eq 11-12; X9):
+ *   rho(omega_k) = [g_0 mu_0 + 2 sum_{n=1}^{N-1} g_n mu_n T_n(x_k)] / (pi a sqrt(1 - x_k^2)),
+ *   x_k = (omega_k - b)/a; rho = 0 for |x_k| >= 1.
+ * Host mu[N], omega[K] -> host rho[K]; computed on `device`. */
+kpm_status kpm_dos(const double* mu, int32_t N, int32_t kernel, double a, double b,
+                   const double* omega, int64_t K, double* rho, int32_t device);
+
+/* ---- introspection ---------------------------------------------------------------- */
+
+/* Device time (ms, CUDA events on the handle's stream) of the last kpm_moments_ex's
+ * recursion-step launches (all steps after the first), their count, and the kernel
+ * launches the call made in total. */
+kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launches,
+                           int32_t* total_launches);
+
+/* Algorithmic HBM bytes of one recursion-step launch. */
+kpm_status kpm_step_bytes(kpm_handle h, int64_t R, double* bytes);
+
+void kpm_destroy(kpm_handle h); /* NULL-safe */
+const char* kpm_last_error(void);
+const char* kpm_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KPM_H_ */

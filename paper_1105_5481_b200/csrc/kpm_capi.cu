@@ -1,0 +1,682 @@
+// kpm_capi.cu -- host side of the C ABI declared in include/kpm.h.
+//
+// Owns: validation, the upload of H~ (Eq 8), the device workspace plan, the
+// launch sequence of one kpm_moments call (first step, M-1 fused steps, finish,
+// assembly) and error reporting.  All arithmetic of the method runs in the
+// kernels of kpm_kernels.cuh; this file only marshals.
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/kpm.h"
+#include "kpm_kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+kpm_status fail(kpm_status st, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    g_err = buf;
+    return st;
+}
+
+#define KPM_CUDA(call)                                                                        \
+    do {                                                                                      \
+        cudaError_t e_ = (call);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return fail(KPM_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #call,              \
+                        cudaGetErrorString(e_));                                              \
+    } while (0)
+
+#define KPM_TRY(expr)                        \
+    do {                                     \
+        kpm_status s_ = (expr);              \
+        if (s_ != KPM_OK) return s_;         \
+    } while (0)
+
+enum Kind { KIND_STENCIL = 0, KIND_ELL = 1 };
+constexpr int kThreads = 512;     // threads per CTA of the step kernels
+constexpr size_t kAlign = 256;
+
+size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+}  // namespace
+
+struct kpm_handle_s {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    int kind = KIND_STENCIL;
+    int dtype = KPM_REAL64;
+    double a = 1.0, b = 0.0;
+    int64_t D = 0;
+    // stencil
+    int ndim = 1;
+    int64_t L[3] = {1, 1, 1};
+    double t_scaled = 0.0;
+    double* d_eps = nullptr;      // (eps_i - b)/a
+    double2* d_phase = nullptr;   // e^{i 2 pi phi x}
+    // ELL
+    int K = 0;
+    int32_t* d_col = nullptr;
+    double* d_val = nullptr;
+    // partition
+    kpm_dist dist{KPM_PART_NONE, 0, 1};
+    // workspace
+    char* ws = nullptr;
+    size_t ws_bytes = 0;
+    bool ws_own = true;
+    // device facts
+    int num_sms = 148;
+    // timing of the last call
+    cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    int step_launches = 0, total_launches = 0;
+};
+
+namespace {
+
+struct Plan {
+    int N = 0, M = 0;
+    long long R_loc = 0, r_off = 0;
+    int RG = 0, RP = 0;
+    int TR = 0, TS = 0, gx = 0, gy = 0;
+    int nslots = 0;      // moment slots = N
+    size_t lane_bytes = 0;
+    size_t off_P = 0, off_C = 0, off_R = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0, total = 0;
+};
+
+bool is_cplx(const kpm_handle_s* h) { return h->dtype == KPM_COMPLEX128; }
+
+kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p) {
+    if (N < 1) return fail(KPM_ERR_INVALID_ARG, "N must be >= 1 (got %d)", N);
+    if (R < 1) return fail(KPM_ERR_INVALID_ARG, "R must be >= 1 (got %lld)", (long long)R);
+    const int world = h->dist.partition == KPM_PART_VECTORS ? h->dist.world : 1;
+    const int rank = h->dist.partition == KPM_PART_VECTORS ? h->dist.rank : 0;
+    p->N = N;
+    p->M = N / 2;
+    p->r_off = (long long)(R * rank / world);
+    p->R_loc = (long long)(R * (rank + 1) / world) - p->r_off;
+    if (p->R_loc < 1) return fail(KPM_ERR_INVALID_ARG, "rank %d of %d owns no vectors (R=%lld)", rank, world, (long long)R);
+    p->RG = is_cplx(h) ? (int)p->R_loc : (int)((p->R_loc + 1) / 2);
+    p->RP = is_cplx(h) ? p->RG : 2 * p->RG;
+    int tr = 1;
+    while (tr < p->RG && tr < 32) tr <<= 1;
+    p->TR = tr;
+    p->TS = kThreads / tr;
+    p->gy = (p->RG + tr - 1) / tr;
+    const long long site_ctas = (h->D + p->TS - 1) / p->TS;
+    p->gx = (int)std::min<long long>(site_ctas, 2LL * h->num_sms);
+    p->nslots = N;
+    p->lane_bytes = (size_t)h->D * p->RG * sizeof(double2);
+    size_t off = 0;
+    p->off_P = off; off = align_up(off + p->lane_bytes);
+    p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
+    p->off_R = off;
+    if ((flags & KPM_DIRECT) && with_r0) off = align_up(off + p->lane_bytes);
+    p->off_part = off; off = align_up(off + (size_t)N * p->gx * p->RP * sizeof(double));
+    p->off_Sv = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
+    p->off_S = off; off = align_up(off + (size_t)N * sizeof(double));
+    p->off_out = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
+    p->total = off;
+    if (h->D * (long long)p->RG > (1LL << 40)) return fail(KPM_ERR_INVALID_ARG, "problem too large");
+    return KPM_OK;
+}
+
+kpm_status ensure_workspace(kpm_handle_s* h, size_t bytes) {
+    if (h->ws_bytes >= bytes) return KPM_OK;
+    if (!h->ws_own) return fail(KPM_ERR_OOM, "caller workspace has %zu bytes, need %zu", h->ws_bytes, bytes);
+    if (h->ws) cudaFree(h->ws);
+    h->ws = nullptr;
+    h->ws_bytes = 0;
+    cudaError_t e = cudaMalloc(&h->ws, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(KPM_ERR_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    }
+    h->ws_bytes = bytes;
+    return KPM_OK;
+}
+
+// Launch one fused kernel of `mode` with operator op.
+template <int MODE, bool CPLX, class OP>
+kpm_status launch_step(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int tail) {
+    dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
+    const size_t smem = 3 * (size_t)kThreads * sizeof(double2);
+    kpm::kpm_step_kernel<OP, MODE, CPLX><<<grid, block, smem, h->stream>>>(op, v, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
+template <bool CPLX, class OP>
+kpm_status launch_mode(kpm_handle_s* h, const Plan& p, const OP& op, int mode, const kpm::VecArgs& v, int tail) {
+    switch (mode) {
+        case kpm::FIRST_GEN: return launch_step<kpm::FIRST_GEN, CPLX>(h, p, op, v, tail);
+        case kpm::FIRST_BUF: return launch_step<kpm::FIRST_BUF, CPLX>(h, p, op, v, tail);
+        case kpm::STEP: return launch_step<kpm::STEP, CPLX>(h, p, op, v, tail);
+        case kpm::DIRECT_GEN: return launch_step<kpm::DIRECT_GEN, CPLX>(h, p, op, v, tail);
+        default: return launch_step<kpm::DIRECT_BUF, CPLX>(h, p, op, v, tail);
+    }
+}
+
+kpm::StencilGeom stencil_geom(const kpm_handle_s* h) {
+    kpm::StencilGeom g;
+    g.L0 = (int)h->L[0];
+    g.L1 = (int)h->L[1];
+    g.L2 = (int)h->L[2];
+    g.plane = (int)(h->L[0] * h->L[1]);
+    g.t = h->t_scaled;
+    g.shift = -h->b / h->a;
+    g.eps = h->d_eps;
+    g.phase = h->d_phase;
+    return g;
+}
+
+// Dispatch on the operator type of the handle.
+kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& v, int tail) {
+    using namespace kpm;
+    if (h->kind == KIND_ELL) {
+        if (is_cplx(h)) return launch_mode<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, mode, v, tail);
+        return launch_mode<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, mode, v, tail);
+    }
+    const StencilGeom g = stencil_geom(h);
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_mode<true>(h, p, StencilOp<2, true, true>{g}, mode, v, tail);
+        return launch_mode<true>(h, p, StencilOp<2, false, true>{g}, mode, v, tail);
+    }
+    switch (h->ndim * 2 + (on ? 1 : 0)) {
+        case 2: return launch_mode<false>(h, p, StencilOp<1, false, false>{g}, mode, v, tail);
+        case 3: return launch_mode<false>(h, p, StencilOp<1, true, false>{g}, mode, v, tail);
+        case 4: return launch_mode<false>(h, p, StencilOp<2, false, false>{g}, mode, v, tail);
+        case 5: return launch_mode<false>(h, p, StencilOp<2, true, false>{g}, mode, v, tail);
+        case 6: return launch_mode<false>(h, p, StencilOp<3, false, false>{g}, mode, v, tail);
+        default: return launch_mode<false>(h, p, StencilOp<3, true, false>{g}, mode, v, tail);
+    }
+}
+
+kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) {
+    if (!out) return fail(KPM_ERR_INVALID_ARG, "out handle pointer is NULL");
+    *out = nullptr;
+    if (dist) {
+        if (dist->partition != KPM_PART_NONE && dist->partition != KPM_PART_VECTORS)
+            return fail(KPM_ERR_UNSUPPORTED, "partition %d not supported", dist->partition);
+        if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
+            return fail(KPM_ERR_INVALID_ARG, "bad rank %d / world %d", dist->rank, dist->world);
+    }
+    int ndev = 0;
+    KPM_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(KPM_ERR_INVALID_ARG, "device %d not present (%d devices)", device, ndev);
+    KPM_CUDA(cudaSetDevice(device));
+    auto* h = new kpm_handle_s();
+    h->device = device;
+    if (dist) h->dist = *dist;
+    cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev_begin);
+    if (e == cudaSuccess) e = cudaEventCreate(&h->ev_end);
+    if (e != cudaSuccess) {
+        kpm_destroy(h);
+        return fail(KPM_ERR_CUDA, "stream/event creation failed: %s", cudaGetErrorString(e));
+    }
+    h->own_stream = true;
+    *out = h;
+    return KPM_OK;
+}
+
+kpm_status check_ab(double a, double b) {
+    if (!(a > 0.0) || !std::isfinite(a) || !std::isfinite(b))
+        return fail(KPM_ERR_INVALID_ARG, "scale a must be finite and > 0, shift b finite (a=%g b=%g)", a, b);
+    return KPM_OK;
+}
+
+kpm_status check_stencil(const kpm_stencil_desc* d) {
+    if (!d) return fail(KPM_ERR_INVALID_ARG, "stencil descriptor is NULL");
+    if (d->ndim < 1 || d->ndim > 3) return fail(KPM_ERR_INVALID_ARG, "ndim must be 1..3 (got %d)", d->ndim);
+    for (int k = 0; k < 3; ++k) {
+        if (k < d->ndim && d->L[k] < 2) return fail(KPM_ERR_INVALID_ARG, "L[%d] must be >= 2", k);
+        if (k >= d->ndim && d->L[k] != 1) return fail(KPM_ERR_INVALID_ARG, "unused L[%d] must be 1", k);
+    }
+    const long long D = d->L[0] * d->L[1] * d->L[2];
+    if (D >= (1LL << 31)) return fail(KPM_ERR_INVALID_ARG, "D = %lld sites exceeds 2^31 per GPU", D);
+    if (!std::isfinite(d->t)) return fail(KPM_ERR_INVALID_ARG, "hopping t not finite");
+    if (d->flux != 0.0) {
+        if (d->ndim != 2) return fail(KPM_ERR_INVALID_ARG, "Peierls flux needs ndim == 2");
+        const double q = d->flux * (double)d->L[0];
+        if (!std::isfinite(q) || std::fabs(q - std::nearbyint(q)) > 1e-9)
+            return fail(KPM_ERR_INVALID_ARG, "flux * L[0] must be an integer (got %.17g)", q);
+    }
+    return KPM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* kpm_last_error(void) { return g_err.c_str(); }
+const char* kpm_version(void) { return "kpm-b200 0.1 (sm_100a)"; }
+
+void kpm_destroy(kpm_handle h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->ws_own && h->ws) cudaFree(h->ws);
+    cudaFree(h->d_eps);
+    cudaFree(h->d_phase);
+    cudaFree(h->d_col);
+    cudaFree(h->d_val);
+    if (h->ev_begin) cudaEventDestroy(h->ev_begin);
+    if (h->ev_end) cudaEventDestroy(h->ev_end);
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+    delete h;
+}
+
+kpm_status kpm_gershgorin_stencil(const kpm_stencil_desc* d, double eps, double* a, double* b) {
+    KPM_TRY(check_stencil(d));
+    if (!a || !b) return fail(KPM_ERR_INVALID_ARG, "a/b output pointers are NULL");
+    // Every row: diagonal eps_i, off-diagonal moduli |t| on 2 ndim bonds.
+    const long long D = d->L[0] * d->L[1] * d->L[2];
+    double lo = 0.0, hi = 0.0;
+    if (d->onsite) {
+        lo = hi = d->onsite[0];
+        for (long long i = 1; i < D; ++i) {
+            lo = std::min(lo, d->onsite[i]);
+            hi = std::max(hi, d->onsite[i]);
+        }
+    }
+    const double radius = 2.0 * d->ndim * std::fabs(d->t);
+    const double Eu = hi + radius + eps, El = lo - radius - eps;
+    *a = (Eu - El) / 2.0;
+    *b = (Eu + El) / 2.0;
+    return KPM_OK;
+}
+
+kpm_status kpm_gershgorin_csr(int64_t D, const int64_t* rowptr, const int32_t* col, const void* val, int32_t dtype,
+                              double eps, double* a, double* b) {
+    if (D < 1 || !rowptr || !col || !val || !a || !b) return fail(KPM_ERR_INVALID_ARG, "bad CSR arguments");
+    if (dtype != KPM_REAL64 && dtype != KPM_COMPLEX128) return fail(KPM_ERR_INVALID_ARG, "bad dtype %d", dtype);
+    const double* v = static_cast<const double*>(val);
+    double Eu = -INFINITY, El = INFINITY;
+    for (int64_t i = 0; i < D; ++i) {
+        double diag = 0.0, rad = 0.0;
+        for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+            const double re = dtype == KPM_REAL64 ? v[k] : v[2 * k];
+            const double im = dtype == KPM_REAL64 ? 0.0 : v[2 * k + 1];
+            if (col[k] == i) diag += re;
+            else rad += std::hypot(re, im);
+        }
+        Eu = std::max(Eu, diag + rad);
+        El = std::min(El, diag - rad);
+    }
+    Eu += eps;
+    El -= eps;
+    *a = (Eu - El) / 2.0;
+    *b = (Eu + El) / 2.0;
+    return KPM_OK;
+}
+
+kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int32_t device, const kpm_dist* dist,
+                              kpm_handle* out) {
+    KPM_TRY(check_stencil(d));
+    KPM_TRY(check_ab(a, b));
+    kpm_handle_s* h = nullptr;
+    KPM_TRY(new_handle(device, dist, &h));
+    h->kind = KIND_STENCIL;
+    h->dtype = d->flux != 0.0 ? KPM_COMPLEX128 : KPM_REAL64;
+    h->a = a;
+    h->b = b;
+    h->ndim = d->ndim;
+    for (int k = 0; k < 3; ++k) h->L[k] = d->L[k];
+    h->D = d->L[0] * d->L[1] * d->L[2];
+    h->t_scaled = d->t / a;
+    kpm_status st = KPM_OK;
+    if (d->onsite) {
+        std::vector<double> e(h->D);
+        for (int64_t i = 0; i < h->D; ++i) e[i] = (d->onsite[i] - b) / a;  // Eq (8) on the diagonal
+        cudaError_t ce = cudaMalloc(&h->d_eps, h->D * sizeof(double));
+        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_eps, e.data(), h->D * sizeof(double), cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site upload: %s", cudaGetErrorString(ce));
+    }
+    if (st == KPM_OK && d->flux != 0.0) {
+        std::vector<double2> ph(h->L[0]);
+        for (int64_t x = 0; x < h->L[0]; ++x) {
+            // theta = 2 pi phi x, reduced to 2 pi frac(phi x) before the cos/sin
+            const double f = std::fmod(d->flux * (double)x, 1.0);
+            ph[x] = make_double2(std::cos(2.0 * CUDART_PI * f), std::sin(2.0 * CUDART_PI * f));
+        }
+        cudaError_t ce = cudaMalloc(&h->d_phase, h->L[0] * sizeof(double2));
+        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_phase, ph.data(), h->L[0] * sizeof(double2), cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "phase upload: %s", cudaGetErrorString(ce));
+    }
+    if (st != KPM_OK) {
+        kpm_destroy(h);
+        return st;
+    }
+    *out = h;
+    return KPM_OK;
+}
+
+kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* val, int32_t dtype, double a,
+                          double b, int32_t device, const kpm_dist* dist, kpm_handle* out) {
+    if (D < 1 || D >= (1LL << 31) || K < 0 || (K > 0 && (!col || !val)))
+        return fail(KPM_ERR_INVALID_ARG, "bad ELL arguments (D=%lld K=%d)", (long long)D, K);
+    if (dtype != KPM_REAL64 && dtype != KPM_COMPLEX128) return fail(KPM_ERR_INVALID_ARG, "bad dtype %d", dtype);
+    KPM_TRY(check_ab(a, b));
+    const int w = dtype == KPM_COMPLEX128 ? 2 : 1;
+    std::vector<int32_t> c((size_t)K * D);
+    std::vector<double> v((size_t)K * D * w);
+    const double* vin = static_cast<const double*>(val);
+    for (int64_t e = 0; e < (int64_t)K * D; ++e) {
+        const int64_t i = e % D;
+        const int32_t j = col[e];
+        if (j < -1 || j >= D) return fail(KPM_ERR_INVALID_ARG, "ELL column %d out of range at entry %lld", j, (long long)e);
+        c[e] = j < 0 ? (int32_t)i : j;  // padding -> (row, 0)
+        for (int q = 0; q < w; ++q) v[e * w + q] = j < 0 ? 0.0 : vin[e * w + q] / a;
+    }
+    kpm_handle_s* h = nullptr;
+    KPM_TRY(new_handle(device, dist, &h));
+    h->kind = KIND_ELL;
+    h->dtype = dtype;
+    h->a = a;
+    h->b = b;
+    h->D = D;
+    h->K = K;
+    kpm_status st = KPM_OK;
+    if (K > 0) {
+        cudaError_t ce = cudaMalloc(&h->d_col, c.size() * sizeof(int32_t));
+        if (ce == cudaSuccess) ce = cudaMalloc(&h->d_val, v.size() * sizeof(double));
+        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_col, c.data(), c.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_val, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice);
+        if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "ELL upload: %s", cudaGetErrorString(ce));
+    }
+    if (st != KPM_OK) {
+        kpm_destroy(h);
+        return st;
+    }
+    *out = h;
+    return KPM_OK;
+}
+
+kpm_status kpm_create_csr(int64_t D, const int64_t* rowptr, const int32_t* col, const void* val, int32_t dtype,
+                          double a, double b, int32_t device, const kpm_dist* dist, kpm_handle* out) {
+    if (D < 1 || D >= (1LL << 31) || !rowptr || !col || !val) return fail(KPM_ERR_INVALID_ARG, "bad CSR arguments");
+    if (dtype != KPM_REAL64 && dtype != KPM_COMPLEX128) return fail(KPM_ERR_INVALID_ARG, "bad dtype %d", dtype);
+    if (rowptr[0] != 0) return fail(KPM_ERR_INVALID_ARG, "rowptr[0] must be 0");
+    int32_t K = 0;
+    for (int64_t i = 0; i < D; ++i) {
+        const int64_t len = rowptr[i + 1] - rowptr[i];
+        if (len < 0) return fail(KPM_ERR_INVALID_ARG, "rowptr not monotone at row %lld", (long long)i);
+        K = std::max<int32_t>(K, (int32_t)len);
+    }
+    const int w = dtype == KPM_COMPLEX128 ? 2 : 1;
+    const double* vin = static_cast<const double*>(val);
+    std::vector<int32_t> c((size_t)K * D, -1);
+    std::vector<double> v((size_t)K * D * w, 0.0);
+    for (int64_t i = 0; i < D; ++i) {
+        for (int64_t k = rowptr[i]; k < rowptr[i + 1]; ++k) {
+            const int64_t slot = k - rowptr[i];
+            if (col[k] < 0 || col[k] >= D) return fail(KPM_ERR_INVALID_ARG, "CSR column %d out of range in row %lld", col[k], (long long)i);
+            c[slot * D + i] = col[k];
+            for (int q = 0; q < w; ++q) v[(slot * D + i) * w + q] = vin[k * w + q];
+        }
+    }
+    return kpm_create_ell(D, K, c.data(), v.data(), dtype, a, b, device, dist, out);
+}
+
+kpm_status kpm_set_stream(kpm_handle h, void* stream) {
+    if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
+    KPM_CUDA(cudaSetDevice(h->device));
+    if (h->own_stream && h->stream) {
+        cudaStreamSynchronize(h->stream);
+        cudaStreamDestroy(h->stream);
+    }
+    h->stream = static_cast<cudaStream_t>(stream);
+    h->own_stream = false;
+    return KPM_OK;
+}
+
+kpm_status kpm_workspace_size(kpm_handle h, int32_t N, int64_t R, uint32_t flags, size_t* bytes) {
+    if (!h || !bytes) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
+    Plan p;
+    KPM_TRY(make_plan(h, N, R, flags, true, &p));
+    *bytes = p.total;
+    return KPM_OK;
+}
+
+kpm_status kpm_set_workspace(kpm_handle h, void* dev_ptr, size_t bytes) {
+    if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
+    if (dev_ptr && (reinterpret_cast<uintptr_t>(dev_ptr) % kAlign) != 0)
+        return fail(KPM_ERR_INVALID_ARG, "workspace must be %zu-byte aligned", kAlign);
+    KPM_CUDA(cudaSetDevice(h->device));
+    cudaStreamSynchronize(h->stream);
+    if (h->ws_own && h->ws) cudaFree(h->ws);
+    h->ws = static_cast<char*>(dev_ptr);
+    h->ws_bytes = dev_ptr ? bytes : 0;
+    h->ws_own = dev_ptr == nullptr;
+    return KPM_OK;
+}
+
+kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, const void* r0, uint32_t flags,
+                          void* out) {
+    if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
+    if (!out) return fail(KPM_ERR_INVALID_ARG, "NULL output");
+    if ((flags & KPM_PER_VECTOR) && (flags & KPM_RAW_SUMS))
+        return fail(KPM_ERR_INVALID_ARG, "KPM_PER_VECTOR and KPM_RAW_SUMS are exclusive");
+    KPM_CUDA(cudaSetDevice(h->device));
+    Plan p;
+    KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p));
+    KPM_TRY(ensure_workspace(h, p.total));
+    const bool cplx = is_cplx(h);
+    const bool direct = (flags & KPM_DIRECT) != 0;
+    double2* P = reinterpret_cast<double2*>(h->ws + p.off_P);
+    double2* C = reinterpret_cast<double2*>(h->ws + p.off_C);
+    double2* Rb = reinterpret_cast<double2*>(h->ws + p.off_R);
+    double* part = reinterpret_cast<double*>(h->ws + p.off_part);
+    double* Sv = reinterpret_cast<double*>(h->ws + p.off_Sv);
+    double* S = reinterpret_cast<double*>(h->ws + p.off_S);
+    double* dout = reinterpret_cast<double*>(h->ws + p.off_out);
+    const size_t slot = (size_t)p.gx * p.RP;  // doubles per moment slot of partials
+    h->total_launches = 0;
+    h->step_launches = 0;
+
+    kpm::VecArgs v{};
+    v.P = P;
+    v.C = C;
+    v.Rbuf = Rb;
+    v.D = (int)h->D;
+    v.RG = p.RG;
+    v.RP = p.RP;
+    v.R_loc = p.R_loc;
+    v.key = kpm::vector_key(seed);
+    v.r_off = p.r_off;
+    v.D_total = h->D;
+    v.i_off = 0;
+
+    // a_0: generated in the first-step kernel, or the caller's block staged through C.
+    int first_mode = kpm::FIRST_GEN;
+    if (r0) {
+        const size_t rbytes = (size_t)p.R_loc * h->D * sizeof(double);
+        KPM_CUDA(cudaMemcpyAsync(C, r0, rbytes, (flags & KPM_DEVICE_IN) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
+                                 h->stream));
+        const long long n = h->D * (long long)p.RG;
+        const int blocks = (int)std::min<long long>((n + 255) / 256, 8LL * h->num_sms);
+        if (cplx) kpm::load_r0_kernel<true><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double*>(C), P, (int)h->D, p.RG, p.R_loc);
+        else kpm::load_r0_kernel<false><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double*>(C), P, (int)h->D, p.RG, p.R_loc);
+        KPM_CUDA(cudaGetLastError());
+        h->total_launches++;
+        if (direct) KPM_CUDA(cudaMemcpyAsync(Rb, P, p.lane_bytes, cudaMemcpyDeviceToDevice, h->stream));
+        first_mode = kpm::FIRST_BUF;
+    }
+    // First step: a_0, a_1 = H~ a_0; S_0 = <a_0|a_0>, S_1 = <a_0|a_1> (Eq 17, 19).
+    v.red0 = part;
+    v.red1 = N > 1 ? part + slot : nullptr;
+    v.red2 = (!direct && N == 3) ? part + 2 * slot : nullptr;
+    KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
+
+    // Recursion steps (Eq 18), a_{n+1} over a_{n-1}; swap roles after each step.
+    const int nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
+    KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
+    double2* cur = C;   // a_n
+    double2* prev = P;  // a_{n-1}
+    for (int n = 1; n <= nsteps; ++n) {
+        v.C = cur;
+        v.P = prev;
+        if (direct) {
+            v.red0 = part + (size_t)(n + 1) * slot;  // <r|a_{n+1}> -> mu_{n+1}
+            v.red1 = v.red2 = nullptr;
+            KPM_TRY(launch(h, p, r0 ? kpm::DIRECT_BUF : kpm::DIRECT_GEN, v, 0));
+        } else {
+            v.red0 = part + (size_t)(2 * n) * slot;      // <a_n|a_n>     -> mu_{2n}
+            v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
+            const bool tail = (N & 1) && n == nsteps;    // odd N: <a_M|a_M> -> mu_{N-1}
+            v.red2 = tail ? part + (size_t)(2 * n + 2) * slot : nullptr;
+            KPM_TRY(launch(h, p, kpm::STEP, v, tail));
+        }
+        h->step_launches++;
+        std::swap(cur, prev);
+    }
+    KPM_CUDA(cudaEventRecord(h->ev_end, h->stream));
+
+    // Fixed-order finish of the CTA partials, then the output form.
+    kpm::finish_kernel<<<N, 256, 0, h->stream>>>(part, p.gx, p.RP, p.R_loc, Sv, S);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    const bool dev_out = (flags & KPM_DEVICE_OUT) != 0;
+    size_t out_bytes = 0;
+    const double* src = nullptr;
+    if (flags & KPM_RAW_SUMS) {
+        src = S;
+        out_bytes = (size_t)N * sizeof(double);
+    } else if (flags & KPM_PER_VECTOR) {
+        const long long n = (long long)N * p.R_loc;
+        kpm::assemble_pervec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(Sv, N, p.R_loc, 1.0 / (double)h->D,
+                                                                                          direct, dout);
+        KPM_CUDA(cudaGetLastError());
+        h->total_launches++;
+        src = dout;
+        out_bytes = (size_t)n * sizeof(double);
+    } else {
+        if (h->dist.partition == KPM_PART_VECTORS && h->dist.world > 1)
+            return fail(KPM_ERR_INVALID_ARG, "multi-rank: use KPM_RAW_SUMS, all-reduce, then kpm_assemble");
+        kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, 1.0 / ((double)h->D * (double)p.R_loc), direct,
+                                                                     dout);
+        KPM_CUDA(cudaGetLastError());
+        h->total_launches++;
+        src = dout;
+        out_bytes = (size_t)N * sizeof(double);
+    }
+    KPM_CUDA(cudaMemcpyAsync(out, src, out_bytes, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+    if (dev_out) return KPM_OK;
+    KPM_CUDA(cudaStreamSynchronize(h->stream));
+    // Spectrum guard: |T_n| <= 1 on [-1, 1] (Eq 3) => |mu_n| <= mu_0 when [b-a, b+a] encloses spec(H).
+    if (!(flags & KPM_RAW_SUMS)) {
+        const double* o = static_cast<const double*>(out);
+        const long long rows = (flags & KPM_PER_VECTOR) ? p.R_loc : 1;
+        for (long long r = 0; r < rows; ++r) {
+            const double* m = o + r * N;
+            for (int n = 0; n < N; ++n)
+                if (!std::isfinite(m[n]) || std::fabs(m[n]) > std::fabs(m[0]) * (1.0 + 1e-8) + 1e-300)
+                    return fail(KPM_ERR_SPECTRUM, "|mu_%d| = %g exceeds mu_0 = %g: [b-a, b+a] does not enclose the spectrum", n,
+                                m[n], m[0]);
+        }
+    }
+    return KPM_OK;
+}
+
+kpm_status kpm_moments(kpm_handle h, int32_t N, int64_t R, uint64_t seed, double* mu) {
+    return kpm_moments_ex(h, N, R, seed, nullptr, 0u, mu);
+}
+
+kpm_status kpm_assemble(kpm_handle h, const double* S, int32_t N, int64_t R, uint32_t flags, double* mu) {
+    if (!h || !S || !mu || N < 1 || R < 1) return fail(KPM_ERR_INVALID_ARG, "bad kpm_assemble arguments");
+    KPM_CUDA(cudaSetDevice(h->device));
+    const int direct = (flags & KPM_DIRECT) ? 1 : 0;
+    const double c = 1.0 / ((double)h->D * (double)R);
+    double* dS = nullptr;
+    double* dmu = nullptr;
+    const bool dev = (flags & KPM_DEVICE_OUT) != 0;
+    if (dev) {
+        dS = const_cast<double*>(S);
+        dmu = mu;
+    } else {
+        KPM_CUDA(cudaMallocAsync(&dS, 2 * (size_t)N * sizeof(double), h->stream));
+        dmu = dS + N;
+        KPM_CUDA(cudaMemcpyAsync(dS, S, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    }
+    kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(dS, N, c, direct, dmu);
+    KPM_CUDA(cudaGetLastError());
+    if (!dev) {
+        KPM_CUDA(cudaMemcpyAsync(mu, dmu, (size_t)N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+        KPM_CUDA(cudaFreeAsync(dS, h->stream));
+        KPM_CUDA(cudaStreamSynchronize(h->stream));
+    }
+    return KPM_OK;
+}
+
+kpm_status kpm_dos(const double* mu, int32_t N, int32_t kernel, double a, double b, const double* omega, int64_t K,
+                   double* rho, int32_t device) {
+    if (!mu || !omega || !rho || N < 1 || K < 0) return fail(KPM_ERR_INVALID_ARG, "bad kpm_dos arguments");
+    if (kernel != KPM_KERNEL_JACKSON && kernel != KPM_KERNEL_NONE) return fail(KPM_ERR_INVALID_ARG, "bad kernel %d", kernel);
+    KPM_TRY(check_ab(a, b));
+    if (K == 0) return KPM_OK;
+    KPM_CUDA(cudaSetDevice(device));
+    double* buf = nullptr;
+    const size_t bytes = (2 * (size_t)N + 2 * (size_t)K) * sizeof(double);
+    KPM_CUDA(cudaMalloc(&buf, bytes));
+    double *dmu = buf, *dc = buf + N, *dom = buf + 2 * N, *drho = buf + 2 * N + K;
+    cudaError_t e = cudaMemcpy(dmu, mu, N * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(dom, omega, K * sizeof(double), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        kpm::dos_coeff_kernel<<<(N + 255) / 256, 256>>>(dmu, N, kernel == KPM_KERNEL_JACKSON, dc);
+        kpm::dos_kernel<<<(unsigned)((K + 255) / 256), 256>>>(dc, N, a, b, dom, K, drho);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(rho, drho, K * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(buf);
+    if (e != cudaSuccess) return fail(KPM_ERR_CUDA, "kpm_dos: %s", cudaGetErrorString(e));
+    return KPM_OK;
+}
+
+kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launches, int32_t* total_launches) {
+    if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
+    KPM_CUDA(cudaSetDevice(h->device));
+    float ms = 0.f;
+    if (steps_ms) {
+        KPM_CUDA(cudaEventSynchronize(h->ev_end));
+        KPM_CUDA(cudaEventElapsedTime(&ms, h->ev_begin, h->ev_end));
+        *steps_ms = ms;
+    }
+    if (step_launches) *step_launches = h->step_launches;
+    if (total_launches) *total_launches = h->total_launches;
+    return KPM_OK;
+}
+
+kpm_status kpm_step_bytes(kpm_handle h, int64_t R, double* bytes) {
+    if (!h || !bytes) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
+    Plan p;
+    KPM_TRY(make_plan(h, 2, R, 0u, false, &p));
+    const double s = is_cplx(h) ? 16.0 : 8.0;
+    // read a_n, read a_{n-1}, write a_{n+1} (3 V) + the matrix / on-site data per step.
+    double b = 3.0 * (double)h->D * (double)p.R_loc * s;
+    if (h->kind == KIND_STENCIL) {
+        if (h->d_eps) b += 8.0 * (double)h->D;
+    } else {
+        b += (double)h->K * (double)h->D * (4.0 + s);
+    }
+    *bytes = b;
+    return KPM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,334 @@
+// kpm_kernels.cuh -- sm_100a kernels of the KPM moment recursion.
+//
+// Hot path: one fused kernel per recursion step
+//     a_{n+1} = 2 H~ a_n - a_{n-1}          (Eq 18)
+// written over a_{n-1} in place, with the two inner products the doubling
+// identities need, <a_n|a_n> and <a_n|a_{n+1}>, reduced from the values already
+// in registers (per vector, per CTA; fixed order, no atomics).  The first-step
+// kernel regenerates the Rademacher start block on the fly (Eq 14-15, 17).
+//
+// Data layout: the vector block is interleaved [site][vector] with the vector
+// index fastest, handled as 16-byte lanes (double2): a real lane holds two
+// vectors, a complex128 lane one vector.  One stencil/ELL entry is applied to all
+// R vectors of a site by the threads of one warp, so a warp reads a contiguous
+// run of 16-byte lanes (coalesced, 128-bit).  The matrix is never stored for
+// lattices (StencilOp): hopping t~ = t/a and the rescaled on-site energies
+// eps~_i = (eps_i - b)/a (Eq 8) are applied arithmetically.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include <cstdint>
+
+#include "kpm_rng.cuh"
+
+namespace kpm {
+
+// ------------------------------------------------------------ lane arithmetic
+__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 scale2(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 fma2(double s, double2 a, double2 c) {
+    return make_double2(fma(s, a.x, c.x), fma(s, a.y, c.y));
+}
+// complex p * z
+__device__ __forceinline__ double2 cmul(double2 p, double2 z) {
+    return make_double2(fma(p.x, z.x, -p.y * z.y), fma(p.x, z.y, p.y * z.x));
+}
+// complex conj(p) * z
+__device__ __forceinline__ double2 cmulc(double2 p, double2 z) {
+    return make_double2(fma(p.x, z.x, p.y * z.y), fma(p.x, z.y, -p.y * z.x));
+}
+// acc += Re <a|b> per vector: real lane = two vectors, complex lane = one vector
+template <bool CPLX>
+__device__ __forceinline__ void dot_acc(double2& acc, double2 a, double2 b) {
+    if (CPLX) {
+        acc.x = fma(a.x, b.x, fma(a.y, b.y, acc.x));
+    } else {
+        acc.x = fma(a.x, b.x, acc.x);
+        acc.y = fma(a.y, b.y, acc.y);
+    }
+}
+
+// ------------------------------------------------------------ operators H~
+struct StencilGeom {
+    int L0, L1, L2;          // extents (sites = L0*L1*L2)
+    int plane;               // L0*L1
+    double t;                // t / a
+    double shift;            // -b / a   (used when there is no on-site array)
+    const double* eps;       // (eps_i - b)/a per site, or nullptr
+    const double2* phase;    // Peierls: e^{i 2 pi phi x}, x = 0..L0-1
+};
+
+// Nearest-neighbour periodic lattice in NDIM dims (readings X12-X15).
+template <int NDIM, bool ONSITE, bool PEIERLS>
+struct StencilOp {
+    StencilGeom g;
+    template <class XF>
+    __device__ __forceinline__ double2 apply(int s, const XF& X, double2 xs) const {
+        const int x = s % g.L0;
+        const int xm = (x == 0) ? s + g.L0 - 1 : s - 1;
+        const int xp = (x == g.L0 - 1) ? s - g.L0 + 1 : s + 1;
+        double2 nb = add2(X(xm), X(xp));
+        if (NDIM >= 2) {
+            const int q = s / g.L0;
+            const int y = (NDIM == 2) ? q : q % g.L1;
+            const int ym = (y == 0) ? s + g.plane - g.L0 : s - g.L0;
+            const int yp = (y == g.L1 - 1) ? s - g.plane + g.L0 : s + g.L0;
+            if (PEIERLS) {
+                // H[s][s+e_y] = t e^{-i theta_x}, H[s][s-e_y] = t e^{+i theta_x}
+                const double2 ph = __ldg(g.phase + x);
+                nb = add2(nb, add2(cmulc(ph, X(yp)), cmul(ph, X(ym))));
+            } else {
+                nb = add2(nb, add2(X(ym), X(yp)));
+            }
+            if (NDIM == 3) {
+                const int z = q / g.L1;
+                const int vol = g.plane * g.L2;
+                const int zm = (z == 0) ? s + vol - g.plane : s - g.plane;
+                const int zp = (z == g.L2 - 1) ? s - vol + g.plane : s + g.plane;
+                nb = add2(nb, add2(X(zm), X(zp)));
+            }
+        }
+        const double e = ONSITE ? __ldg(g.eps + s) : g.shift;
+        return fma2(e, xs, scale2(g.t, nb));
+    }
+};
+
+// General sparse H~ in ELL form: K entries per row, [K][D] arrays, values
+// pre-scaled by 1/a, the -b/a shift applied separately.  Padding: col = row, val = 0.
+template <bool CPLX>
+struct EllOp {
+    int D, K;
+    const int* col;       // [K][D]
+    const double* val;    // real: double[K][D]; complex: double2[K][D]
+    double shift;         // -b / a
+    template <class XF>
+    __device__ __forceinline__ double2 apply(int s, const XF& X, double2 xs) const {
+        double2 h = scale2(shift, xs);
+        for (int k = 0; k < K; ++k) {
+            const size_t e = (size_t)k * D + s;
+            const int j = __ldg(col + e);
+            if (CPLX) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(val) + e);
+                h = add2(h, cmul(v, X(j)));
+            } else {
+                h = fma2(__ldg(val + e), X(j), h);
+            }
+        }
+        return h;
+    }
+};
+
+// ------------------------------------------------------------ the fused step
+enum Mode { FIRST_GEN = 0, FIRST_BUF = 1, STEP = 2, DIRECT_GEN = 3, DIRECT_BUF = 4 };
+
+struct VecArgs {
+    double2* P;            // STEP: a_{n-1} in, a_{n+1} out; FIRST: a_0 (out for GEN, in for BUF)
+    double2* C;            // STEP: a_n in; FIRST: a_1 out
+    const double2* Rbuf;   // DIRECT_BUF: start block r in lane layout
+    int D;                 // sites on this GPU
+    int RG;                // lanes per site
+    int RP;                // padded vectors per site (real: 2*RG, complex: RG)
+    long long R_loc;       // real vectors on this GPU (<= RP)
+    unsigned long long key;// vector_key(seed)
+    long long r_off;       // global index of this GPU's first vector
+    long long D_total;     // global number of sites (RNG counter stride)
+    long long i_off;       // global index of this GPU's site 0
+    double* red0;          // partial sums of moment slot 0: [gridDim.x][RP] (nullable)
+    double* red1;          // slot 1
+    double* red2;          // slot 2 (odd-N tail <a_{n+1}|a_{n+1}>)
+};
+
+template <bool CPLX>
+__device__ __forceinline__ double2 gen_lane(const VecArgs& v, int j, int rg) {
+    const uint64_t i = (uint64_t)(v.i_off + j);
+    if (CPLX) {
+        const long long r = rg;
+        return make_double2(r < v.R_loc ? rademacher(v.key, (uint64_t)(v.r_off + r) * v.D_total + i) : 0.0, 0.0);
+    } else {
+        const long long r = 2LL * rg;
+        const double x0 = r < v.R_loc ? rademacher(v.key, (uint64_t)(v.r_off + r) * v.D_total + i) : 0.0;
+        const double x1 = r + 1 < v.R_loc ? rademacher(v.key, (uint64_t)(v.r_off + r + 1) * v.D_total + i) : 0.0;
+        return make_double2(x0, x1);
+    }
+}
+
+// Block = (TR lanes) x (TS sites); grid = (site CTAs) x (lane groups).
+// Sites are visited grid-stride so that, at any moment, all CTAs sweep one compact
+// window of the lattice and the neighbour planes they re-read stay in L2; the
+// a_{n-1} read and a_{n+1} write are cache-streaming (evict-first) so they do not
+// displace those planes.
+template <class OP, int MODE, bool CPLX>
+__global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArgs v, const int tail) {
+    const int TR = blockDim.x, TS = blockDim.y;
+    const int rg = blockIdx.y * TR + threadIdx.x;
+    const bool active = rg < v.RG;
+    double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0;
+    if (active) {
+        for (int s = blockIdx.x * TS + threadIdx.y; s < v.D; s += gridDim.x * TS) {
+            const size_t idx = (size_t)s * v.RG + rg;
+            if (MODE == FIRST_GEN) {
+                auto X = [&](int j) { return gen_lane<CPLX>(v, j, rg); };
+                const double2 x = X(s);
+                const double2 y = op.apply(s, X, x);   // a_1 = H~ a_0   (Eq 17)
+                v.P[idx] = x;
+                v.C[idx] = y;
+                dot_acc<CPLX>(acc0, x, x);
+                dot_acc<CPLX>(acc1, x, y);
+                if (tail) dot_acc<CPLX>(acc2, y, y);
+            } else if (MODE == FIRST_BUF) {
+                auto X = [&](int j) { return __ldg(v.P + (size_t)j * v.RG + rg); };
+                const double2 x = X(s);
+                const double2 y = op.apply(s, X, x);
+                v.C[idx] = y;
+                dot_acc<CPLX>(acc0, x, x);
+                dot_acc<CPLX>(acc1, x, y);
+                if (tail) dot_acc<CPLX>(acc2, y, y);
+            } else {
+                auto X = [&](int j) { return __ldg(v.C + (size_t)j * v.RG + rg); };
+                const double2 x = X(s);
+                const double2 h = op.apply(s, X, x);
+                const double2 p = __ldcs(v.P + idx);
+                const double2 y = make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));  // Eq 18
+                __stcs(v.P + idx, y);
+                if (MODE == STEP) {
+                    dot_acc<CPLX>(acc0, x, x);
+                    dot_acc<CPLX>(acc1, x, y);
+                    if (tail) dot_acc<CPLX>(acc2, y, y);
+                } else if (MODE == DIRECT_GEN) {
+                    dot_acc<CPLX>(acc0, gen_lane<CPLX>(v, s, rg), y);   // <r|a_{n+1}>  (Eq 19)
+                } else {
+                    dot_acc<CPLX>(acc0, __ldcs(v.Rbuf + idx), y);
+                }
+            }
+        }
+    }
+    // CTA-level finish of the per-vector partial sums, fixed order over the TS site rows.
+    extern __shared__ double2 sred[];
+    const int tid = threadIdx.y * TR + threadIdx.x;
+    const int nthr = TR * TS;
+    sred[tid] = acc0;
+    sred[nthr + tid] = acc1;
+    sred[2 * nthr + tid] = acc2;
+    __syncthreads();
+    if (threadIdx.y == 0 && active) {
+        double* rows[3] = {v.red0, v.red1, tail ? v.red2 : nullptr};
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            if (rows[k] == nullptr) continue;
+            double2 s = make_double2(0.0, 0.0);
+            for (int ty = 0; ty < TS; ++ty) s = add2(s, sred[k * nthr + ty * TR + threadIdx.x]);
+            double* row = rows[k] + (size_t)blockIdx.x * v.RP;
+            if (CPLX) {
+                row[rg] = s.x;
+            } else {
+                row[2 * rg] = s.x;
+                row[2 * rg + 1] = s.y;
+            }
+        }
+    }
+}
+
+// ------------------------------------------------------------ helpers
+// Caller start vectors, vector-major [R_loc][D] real -> lane layout [D][RG].
+template <bool CPLX>
+__global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restrict__ out, int D, int RG,
+                               long long R_loc) {
+    const long long n = (long long)D * RG;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+        const int s = (int)(e / RG), rg = (int)(e % RG);
+        double2 val;
+        if (CPLX) {
+            val = make_double2(rg < R_loc ? r0[(size_t)rg * D + s] : 0.0, 0.0);
+        } else {
+            const long long r = 2LL * rg;
+            val = make_double2(r < R_loc ? r0[(size_t)r * D + s] : 0.0, r + 1 < R_loc ? r0[(size_t)(r + 1) * D + s] : 0.0);
+        }
+        out[e] = val;
+    }
+}
+
+// Sum the CTA partials of every moment slot in a fixed order:
+// Sv[m][v] = sum_c partial[m][c][v] (per vector), S[m] = sum_v Sv[m][v].
+__global__ void finish_kernel(const double* __restrict__ partial, int nCTA, int RP, long long R_loc,
+                              double* __restrict__ Sv, double* __restrict__ S) {
+    const int m = blockIdx.x;
+    const double* base = partial + (size_t)m * nCTA * RP;
+    double local = 0.0;
+    for (long long v = threadIdx.x; v < R_loc; v += blockDim.x) {
+        double s = 0.0;
+        for (int c = 0; c < nCTA; ++c) s += base[(size_t)c * RP + v];
+        Sv[(size_t)m * R_loc + v] = s;
+        local += s;
+    }
+    __shared__ double red[1024];
+    red[threadIdx.x] = local;
+    __syncthreads();
+    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) S[m] = red[0];
+}
+
+// Doubling transform + normalisation (north_star; Eq 19 for direct):
+// mu_0 = S_0 c, mu_1 = S_1 c, mu_{2n} = 2 S_{2n} c - mu_0, mu_{2n+1} = 2 S_{2n+1} c - mu_1.
+__device__ __forceinline__ double assemble_one(const double* S, long long stride, int n, double c, int direct) {
+    const double x = S[(size_t)n * stride] * c;
+    if (direct || n < 2) return x;
+    return 2.0 * x - ((n & 1) ? S[stride] * c : S[0] * c);
+}
+
+__global__ void assemble_kernel(const double* __restrict__ S, int N, double c, int direct, double* __restrict__ mu) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n < N) mu[n] = assemble_one(S, 1, n, c, direct);
+}
+
+// Per-vector moments: pv[v][n] from Sv[n][v].
+__global__ void assemble_pervec_kernel(const double* __restrict__ Sv, int N, long long R_loc, double c, int direct,
+                                       double* __restrict__ pv) {
+    const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (e >= (long long)N * R_loc) return;
+    const long long v = e / N;
+    const int n = (int)(e % N);
+    pv[e] = assemble_one(Sv + v, R_loc, n, c, direct);
+}
+
+// ------------------------------------------------------------ DoS (Eq 6)
+// c_n = g_n mu_n (n = 0), 2 g_n mu_n (n >= 1); Jackson g_n (X8).
+__global__ void dos_coeff_kernel(const double* __restrict__ mu, int N, int jackson, double* __restrict__ c) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    double g = 1.0;
+    if (jackson) {
+        const double q = CUDART_PI / (N + 1);
+        double sn, cn;
+        sincospi((double)n / (N + 1), &sn, &cn);
+        g = ((N - n + 1) * cn + sn * (cos(q) / sin(q))) / (N + 1);
+    }
+    c[n] = (n == 0 ? 1.0 : 2.0) * g * mu[n];
+}
+
+// rho(omega) = sum_n c_n T_n(x) / (pi a sqrt(1 - x^2)), x = (omega - b)/a; T_n by Eq (4)-(5).
+__global__ void dos_kernel(const double* __restrict__ c, int N, double a, double b, const double* __restrict__ omega,
+                           long long K, double* __restrict__ rho) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const double x = (omega[k] - b) / a;
+    if (!(fabs(x) < 1.0)) {
+        rho[k] = 0.0;
+        return;
+    }
+    double t0 = 1.0, t1 = x;
+    double s = c[0];
+    if (N > 1) s = fma(c[1], t1, s);
+    for (int n = 2; n < N; ++n) {
+        const double t2 = fma(2.0 * x, t1, -t0);
+        s = fma(c[n], t2, s);
+        t0 = t1;
+        t1 = t2;
+    }
+    rho[k] = s / (CUDART_PI * a * sqrt(1.0 - x * x));
+}
+
+}  // namespace kpm

@@ -1,0 +1,292 @@
+"""Thin ctypes binding of libkpm.so (include/kpm.h): argument marshalling only.
+
+Every step of the method runs in the CUDA kernels behind the C ABI; nothing
+here computes moments.  If libkpm.so is missing this module raises on import
+(there is no CPU fallback).  Names follow the C ABI: kpm_create_stencil,
+kpm_create_csr, kpm_create_ell, kpm_gershgorin_stencil, kpm_gershgorin_csr,
+kpm_moments, kpm_moments_ex, kpm_assemble, kpm_dos, kpm_workspace_size,
+kpm_set_workspace, kpm_set_stream, kpm_last_timing, kpm_step_bytes,
+kpm_destroy, kpm_last_error, kpm_version.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkpm.so")
+if not os.path.exists(LIB_PATH):
+    raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+                      "g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+_lib = ctypes.CDLL(LIB_PATH)
+
+KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM_ERR_SPECTRUM = range(6)
+KPM_REAL64, KPM_COMPLEX128 = 0, 1
+KPM_KERNEL_JACKSON, KPM_KERNEL_NONE = 0, 1
+KPM_PER_VECTOR, KPM_DIRECT, KPM_DEVICE_OUT, KPM_RAW_SUMS, KPM_DEVICE_IN = 1, 2, 4, 8, 16
+KPM_PART_NONE, KPM_PART_VECTORS = 0, 1
+
+EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershgorin_stencil",
+           "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
+           "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
+           "kpm_step_bytes", "kpm_destroy", "kpm_last_error", "kpm_version"]
+
+
+class kpm_stencil_desc(ctypes.Structure):
+    _fields_ = [("ndim", ctypes.c_int32), ("L", ctypes.c_int64 * 3), ("t", ctypes.c_double),
+                ("onsite", ctypes.c_void_p), ("flux", ctypes.c_double)]
+
+
+class kpm_dist(ctypes.Structure):
+    _fields_ = [("partition", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32)]
+
+
+_P, _i32, _i64, _u32, _u64, _f64, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
+                                         ctypes.c_uint64, ctypes.c_double, ctypes.c_size_t)
+_SIG = {
+    "kpm_create_stencil": [ctypes.POINTER(kpm_stencil_desc), _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
+    "kpm_create_csr": [_i64, _P, _P, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
+    "kpm_create_ell": [_i64, _i32, _P, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
+    "kpm_gershgorin_stencil": [ctypes.POINTER(kpm_stencil_desc), _f64, _P, _P],
+    "kpm_gershgorin_csr": [_i64, _P, _P, _P, _i32, _f64, _P, _P],
+    "kpm_set_stream": [_P, _P],
+    "kpm_workspace_size": [_P, _i32, _i64, _u32, _P],
+    "kpm_set_workspace": [_P, _P, _sz],
+    "kpm_moments": [_P, _i32, _i64, _u64, _P],
+    "kpm_moments_ex": [_P, _i32, _i64, _u64, _P, _u32, _P],
+    "kpm_assemble": [_P, _P, _i32, _i64, _u32, _P],
+    "kpm_dos": [_P, _i32, _i32, _f64, _f64, _P, _i64, _P, _i32],
+    "kpm_last_timing": [_P, _P, _P, _P],
+    "kpm_step_bytes": [_P, _i64, _P],
+}
+for _name, _args in _SIG.items():
+    _fn = getattr(_lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = ctypes.c_int32
+_lib.kpm_destroy.argtypes = [_P]
+_lib.kpm_destroy.restype = None
+_lib.kpm_last_error.restype = ctypes.c_char_p
+_lib.kpm_version.restype = ctypes.c_char_p
+
+
+class KPMError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"kpm status {status}: {msg}")
+        self.status = status
+
+
+def _check(st):
+    if st != KPM_OK:
+        raise KPMError(st, _lib.kpm_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def kpm_last_error() -> str:
+    return _lib.kpm_last_error().decode()
+
+
+def kpm_version() -> str:
+    return _lib.kpm_version().decode()
+
+
+def _desc(ndim, L, t, onsite, flux):
+    L = tuple(int(v) for v in L) + (1,) * (3 - len(L))
+    on = None if onsite is None else np.ascontiguousarray(onsite, dtype=np.float64)
+    d = kpm_stencil_desc(int(ndim), (ctypes.c_int64 * 3)(*L), float(t),
+                         None if on is None else on.ctypes.data, float(flux))
+    return d, on
+
+
+def _dist(dist):
+    if dist is None:
+        return None
+    part, rank, world = dist
+    return ctypes.byref(kpm_dist(int(part), int(rank), int(world)))
+
+
+def kpm_gershgorin_stencil(ndim, L, t, onsite=None, flux=0.0, eps=0.0):
+    d, _keep = _desc(ndim, L, t, onsite, flux)
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.kpm_gershgorin_stencil(ctypes.byref(d), float(eps), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+def _csr_arrays(rowptr, col, val):
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    val = np.asarray(val)
+    if np.iscomplexobj(val):
+        v = np.ascontiguousarray(val, dtype=np.complex128).view(np.float64)
+        return rowptr, col, v, KPM_COMPLEX128
+    return rowptr, col, np.ascontiguousarray(val, dtype=np.float64), KPM_REAL64
+
+
+def kpm_gershgorin_csr(D, rowptr, col, val, eps=0.0):
+    rowptr, col, v, dt = _csr_arrays(rowptr, col, val)
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.kpm_gershgorin_csr(int(D), _ptr(rowptr), _ptr(col), _ptr(v), dt, float(eps),
+                                   ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
+
+
+class Handle:
+    """Owns one kpm_handle (one GPU, one process)."""
+
+    def __init__(self, raw, D, R_of=None, dist=None):
+        self._h = raw
+        self.D = int(D)
+        self.dist = dist
+
+    def __del__(self):
+        self.close()
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib.kpm_destroy(self._h)
+            self._h = None
+
+    @property
+    def raw(self):
+        return self._h
+
+    def set_stream(self, stream_ptr: int):
+        _check(_lib.kpm_set_stream(self._h, ctypes.c_void_p(int(stream_ptr))))
+
+    def workspace_size(self, N, R, flags=0):
+        n = ctypes.c_size_t()
+        _check(_lib.kpm_workspace_size(self._h, int(N), int(R), int(flags), ctypes.byref(n)))
+        return n.value
+
+    def set_workspace(self, dev_ptr: int, nbytes: int):
+        _check(_lib.kpm_set_workspace(self._h, ctypes.c_void_p(int(dev_ptr)) if dev_ptr else None, int(nbytes)))
+
+    def r_local(self, R):
+        if self.dist is None or self.dist[0] != KPM_PART_VECTORS:
+            return 0, int(R)
+        _, rank, world = self.dist
+        lo, hi = R * rank // world, R * (rank + 1) // world
+        return lo, hi - lo
+
+    def moments(self, N, R, seed):
+        mu = np.zeros(int(N), dtype=np.float64)
+        _check(_lib.kpm_moments(self._h, int(N), int(R), int(seed), _ptr(mu)))
+        return mu
+
+    def moments_ex(self, N, R, seed, r0=None, flags=0, out=None):
+        """out: None -> a new host array of the right shape; an int -> device pointer
+        (pass KPM_DEVICE_OUT).  r0: host array (R_local, D) or an int device pointer
+        (pass KPM_DEVICE_IN)."""
+        _, R_loc = self.r_local(R)
+        keep = None
+        if r0 is None:
+            r0p = None
+        elif isinstance(r0, (int, np.integer)):
+            r0p = ctypes.c_void_p(int(r0))
+        else:
+            keep = np.ascontiguousarray(r0, dtype=np.float64)
+            assert keep.shape == (R_loc, self.D), (keep.shape, (R_loc, self.D))
+            r0p = _ptr(keep)
+        if isinstance(out, (int, np.integer)):
+            _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags),
+                                       ctypes.c_void_p(int(out))))
+            return None
+        shape = (R_loc, int(N)) if flags & KPM_PER_VECTOR else (int(N),)
+        res = np.zeros(shape, dtype=np.float64)
+        _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags), _ptr(res)))
+        return res
+
+    def assemble(self, S, N, R, flags=0, out=None):
+        if isinstance(S, (int, np.integer)):
+            _check(_lib.kpm_assemble(self._h, ctypes.c_void_p(int(S)), int(N), int(R),
+                                     int(flags) | KPM_DEVICE_OUT, ctypes.c_void_p(int(out))))
+            return None
+        S = np.ascontiguousarray(S, dtype=np.float64)
+        mu = np.zeros(int(N), dtype=np.float64)
+        _check(_lib.kpm_assemble(self._h, _ptr(S), int(N), int(R), int(flags) & ~KPM_DEVICE_OUT, _ptr(mu)))
+        return mu
+
+    def last_timing(self):
+        ms, sl, tl = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
+        _check(_lib.kpm_last_timing(self._h, ctypes.byref(ms), ctypes.byref(sl), ctypes.byref(tl)))
+        return ms.value, sl.value, tl.value
+
+    def step_bytes(self, R):
+        b = ctypes.c_double()
+        _check(_lib.kpm_step_bytes(self._h, int(R), ctypes.byref(b)))
+        return b.value
+
+
+def kpm_create_stencil(ndim, L, t, a, b, onsite=None, flux=0.0, device=0, dist=None) -> Handle:
+    d, _keep = _desc(ndim, L, t, onsite, flux)
+    h = ctypes.c_void_p()
+    _check(_lib.kpm_create_stencil(ctypes.byref(d), float(a), float(b), int(device), _dist(dist), ctypes.byref(h)))
+    Ls = tuple(L) + (1,) * (3 - len(L))
+    return Handle(h.value, Ls[0] * Ls[1] * Ls[2], dist=dist)
+
+
+def kpm_create_csr(D, rowptr, col, val, a, b, device=0, dist=None) -> Handle:
+    rowptr, col, v, dt = _csr_arrays(rowptr, col, val)
+    h = ctypes.c_void_p()
+    _check(_lib.kpm_create_csr(int(D), _ptr(rowptr), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
+                               _dist(dist), ctypes.byref(h)))
+    return Handle(h.value, D, dist=dist)
+
+
+def kpm_create_ell(D, K, col, val, a, b, device=0, dist=None) -> Handle:
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    val = np.asarray(val)
+    if np.iscomplexobj(val):
+        v, dt = np.ascontiguousarray(val, dtype=np.complex128).view(np.float64), KPM_COMPLEX128
+    else:
+        v, dt = np.ascontiguousarray(val, dtype=np.float64), KPM_REAL64
+    h = ctypes.c_void_p()
+    _check(_lib.kpm_create_ell(int(D), int(K), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
+                               _dist(dist), ctypes.byref(h)))
+    return Handle(h.value, D, dist=dist)
+
+
+def kpm_moments(h: Handle, N, R, seed):
+    return h.moments(N, R, seed)
+
+
+def kpm_moments_ex(h: Handle, N, R, seed, r0=None, flags=0, out=None):
+    return h.moments_ex(N, R, seed, r0=r0, flags=flags, out=out)
+
+
+def kpm_assemble(h: Handle, S, N, R, flags=0, out=None):
+    return h.assemble(S, N, R, flags=flags, out=out)
+
+
+def kpm_dos(mu, a, b, omega, kernel=KPM_KERNEL_JACKSON, device=0):
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    om = np.ascontiguousarray(omega, dtype=np.float64)
+    rho = np.zeros(len(om), dtype=np.float64)
+    _check(_lib.kpm_dos(_ptr(mu), len(mu), int(kernel), float(a), float(b), _ptr(om), len(om), _ptr(rho),
+                        int(device)))
+    return rho
+
+
+def kpm_destroy(h: Handle):
+    h.close()
+
+
+def moments_distributed(h: Handle, N, R, seed, group=None, flags=0):
+    """Vector partition across ranks (one process per GPU): each rank runs its share of
+    the R vectors, the raw sums S[N] are summed over ranks with ONE all-reduce
+    (torch.distributed over NCCL), then assembled into mu on the device."""
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device())
+    S = torch.empty(int(N), dtype=torch.float64, device=dev)
+    h.moments_ex(N, R, seed, flags=flags | KPM_RAW_SUMS | KPM_DEVICE_OUT, out=S.data_ptr())
+    torch.cuda.synchronize(dev)
+    dist.all_reduce(S, op=dist.ReduceOp.SUM, group=group)
+    mu = torch.empty_like(S)
+    h.assemble(S.data_ptr(), N, R, flags=flags & KPM_DIRECT, out=mu.data_ptr())
+    torch.cuda.synchronize(dev)
+    return mu.cpu().numpy()

@@ -1,0 +1,164 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same
+seeded inputs.  Bar (X17): normwise max_n |mu_gpu - mu_orc| <= 1e-10 *
+max_n |mu_orc|; bitwise for config c1 (every a_n is integer-valued, Q4) and for the
+Rademacher generator (integer work)."""
+import numpy as np
+import pytest
+
+import kpm_inputs as ki
+import oracle
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-10
+
+
+@pytest.fixture(scope="module")
+def kpm():
+    import torch
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    from paper_1105_5481_b200 import kpm as k
+    return k
+
+
+def normwise(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
+
+
+def make(kpm, lat, a, b, form="stencil"):
+    if form == "stencil":
+        return kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"],
+                                      flux=lat["flux"])
+    H = oracle.lattice_csr(lat)
+    val = H.val_re + 1j * H.val_im if H.is_complex else H.val_re
+    return kpm.kpm_create_csr(H.D, H.rowptr, H.col, val, a, b)
+
+
+def lat_of(ndim, L, t=-1.0, W=0.0, flux=0.0, dseed=5):
+    L = tuple(L) + (1,) * (3 - len(L))
+    D = L[0] * L[1] * L[2]
+    return dict(ndim=ndim, L=L, D=D, t=t, onsite=ki.anderson_onsite(dseed, D, W) if W else None, flux=flux)
+
+
+CASES = {
+    # name: (lattice, N, R)  -- sizes span several CTAs/lane groups with ragged tails
+    "1d_ragged": (lat_of(1, (1000,)), 37, 5),
+    "2d": (lat_of(2, (37, 29)), 64, 7),
+    "2d_wide": (lat_of(2, (64, 48)), 33, 70),          # R > 64: two lane groups, odd N
+    "3d_clean": (lat_of(3, (13, 11, 9)), 50, 13),
+    "3d_anderson": (lat_of(3, (12, 10, 16), W=2.0), 64, 16),
+    "3d_L2": (lat_of(3, (2, 7, 5), W=1.0), 20, 3),    # L = 2: both neighbours coincide
+    "peierls": (lat_of(2, (32, 20), flux=1 / 8), 60, 9),
+    "peierls_anderson": (lat_of(2, (24, 24), flux=1 / 4, W=1.0), 41, 4),
+}
+
+
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+@pytest.mark.parametrize("case", sorted(CASES))
+def test_moments_match_oracle(kpm, case, form):
+    lat, N, R = CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b += 0.05 * a  # exercise the shift term (still encloses the spectrum after widening a)
+    a *= 1.06
+    r = ki.rademacher(11, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b, form)
+    mu = h.moments(N, R, 11)
+    assert normwise(mu, ref) < TOL
+    mu_r0 = h.moments_ex(N, R, 11, r0=r)
+    assert np.array_equal(mu, mu_r0), "on-the-fly generator differs from kpm_inputs.rademacher"
+    pv = h.moments_ex(N, R, 11, flags=kpm.KPM_PER_VECTOR)
+    assert pv.shape == (R, N) and normwise(pv, ref_pv) < TOL
+    assert np.array_equal(h.moments(N, R, 11), mu), "not deterministic"
+
+
+@pytest.mark.parametrize("case", ["2d", "3d_anderson", "peierls"])
+def test_direct_mode_matches_oracle_direct(kpm, case):
+    """KPM_DIRECT: the paper's own estimator, Eq (19): mu_n = <r|a_n>, N-1 products."""
+    lat, N, R = CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    r = ki.rademacher(3, R, lat["D"])
+    ref = oracle.moments_direct(H, a, b, r, N)
+    h = make(kpm, lat, a, b)
+    assert normwise(h.moments_ex(N, R, 3, flags=kpm.KPM_DIRECT), ref) < TOL
+    assert normwise(h.moments_ex(N, R, 3, r0=r, flags=kpm.KPM_DIRECT), ref) < TOL
+
+
+def test_c1_bitwise(kpm):
+    """Q4: config c1 is exact in fp64, so the GPU equals the oracle bit for bit."""
+    c = ki.CONFIGS["c1"]
+    lat = ki.lattice(c)
+    H = oracle.lattice_csr(lat)
+    ref = oracle.moments_doubling(H, 2.0, 0.0, ki.rademacher(c["seed"], c["R"], lat["D"]), c["N"])
+    mu = make(kpm, lat, 2.0, 0.0).moments(c["N"], c["R"], c["seed"])
+    assert np.array_equal(mu, ref)
+    assert mu[0] == 1.0
+
+
+@pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8, 9])
+@pytest.mark.parametrize("R", [1, 2, 3])
+def test_small_N_and_R_edges(kpm, N, R):
+    lat = lat_of(2, (9, 7), W=1.0)
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(9, R, lat["D"]), N)
+    mu = make(kpm, lat, a, b).moments(N, R, 9)
+    assert mu.shape == (N,) and normwise(mu, ref) < TOL
+
+
+def test_unit_vectors_give_exact_trace_on_gpu(kpm):
+    """Q2 through the GPU: R = D unit vectors sqrt(D) e_i (caller start block) give
+    (1/D) Tr T_n(H~) of the paper's 10x10x10 lattice."""
+    lat = lat_of(3, (10, 10, 10))
+    H = oracle.lattice_csr(lat)
+    ex = oracle.exact_moments_dense(H, 6.0, 0.0, 128)
+    r = np.sqrt(1000.0) * np.eye(1000)
+    mu = make(kpm, lat, 6.0, 0.0).moments_ex(128, 1000, 0, r0=r)
+    assert np.abs(mu - ex).max() < 1e-12
+
+
+def test_spectrum_guard(kpm):
+    lat = lat_of(2, (16, 16))
+    h = make(kpm, lat, 2.0, 0.0)  # a = 2 < spectral radius 4: recursion diverges
+    with pytest.raises(kpm.KPMError) as e:
+        h.moments(64, 4, 1)
+    assert e.value.status == kpm.KPM_ERR_SPECTRUM
+
+
+def test_raw_sums_and_assemble(kpm):
+    lat, N, R = CASES["3d_anderson"]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    h = make(kpm, lat, a, b)
+    S = h.moments_ex(N, R, 5, flags=kpm.KPM_RAW_SUMS)
+    mu = h.assemble(S, N, R)
+    assert np.array_equal(mu, h.moments(N, R, 5))
+
+
+def test_vector_partition_ranks_sum_to_whole(kpm):
+    """P1 host logic on one GPU: per-rank raw sums of a 3-way vector partition add up to the
+    1-rank sums (same global vectors), and assemble to the same moments."""
+    lat, N, R = CASES["2d_wide"]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    whole = make(kpm, lat, a, b).moments_ex(N, R, 2, flags=kpm.KPM_RAW_SUMS)
+    parts = []
+    for rank in range(3):
+        h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, dist=(kpm.KPM_PART_VECTORS, rank, 3))
+        parts.append(h.moments_ex(N, R, 2, flags=kpm.KPM_RAW_SUMS))
+    S = parts[0] + parts[1] + parts[2]
+    assert normwise(S, whole) < 1e-13
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(2, R, lat["D"]), N)
+    assert normwise(h.assemble(S, N, R), ref) < TOL
+
+
+def test_dos_matches_oracle(kpm):
+    lat = lat_of(2, (32, 32), flux=1 / 8)
+    H = oracle.lattice_csr(lat)
+    mu = oracle.moments_doubling(H, 4.0, 0.0, ki.rademacher(1, 4, 1024), 256)
+    om = np.linspace(-4.5, 4.5, 1001)
+    for kern, name in [(kpm.KPM_KERNEL_JACKSON, "jackson"), (kpm.KPM_KERNEL_NONE, "none")]:
+        rho = kpm.kpm_dos(mu, 4.0, 0.0, om, kernel=kern)
+        ref = oracle.dos(mu, 4.0, 0.0, om, kernel=name)
+        assert np.abs(rho - ref).max() < 1e-10 * np.abs(ref).max()
