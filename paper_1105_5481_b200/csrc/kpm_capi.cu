@@ -4,6 +4,8 @@
 // launch sequence of one kpm_moments call (first step, M-1 fused steps, finish,
 // assembly) and error reporting.  All arithmetic of the method runs in the
 // kernels of kpm_kernels.cuh; this file only marshals.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -11,12 +13,14 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "../../include/kpm.h"
 #include "kpm_kernels.cuh"
+#include "kpm_tma.cuh"
 
 namespace {
 
@@ -93,11 +97,60 @@ struct Plan {
     int RG = 0, RP = 0;
     int TR = 0, TS = 0, gx = 0, gy = 0;
     int nslots = 0;      // moment slots = N
+    // TMA-pipelined step kernel (2D/3D stencils), see kpm_tma.cuh
+    bool use_tma = false;
+    int TL = 0, TX = 0, TY = 0, tma_grid = 0;
+    size_t tma_smem = 0;
     size_t lane_bytes = 0;
     size_t off_P = 0, off_C = 0, off_R = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0, total = 0;
 };
 
 bool is_cplx(const kpm_handle_s* h) { return h->dtype == KPM_COMPLEX128; }
+
+bool tma_disabled() {
+    const char* e = getenv("KPM_NO_TMA");
+    return e && e[0] && e[0] != '0';
+}
+
+// Tile choice for the TMA march: ~16 KB main tiles (TX*TY*TL = 1024 lanes), full passes
+// of the 256 consumer threads, tiles dividing the lattice, lane groups dividing RG.
+void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
+    p->use_tma = false;
+    if (h->kind != KIND_STENCIL || h->ndim < 2 || (flags & KPM_DIRECT) || tma_disabled()) return;
+    const int RG = p->RG;
+    int TL = 0;
+    const int cands2[3] = {32, 16, 8}, cands3[3] = {8, 16, 32};
+    for (int c : (h->ndim == 2 ? cands2 : cands3))
+        if (RG % c == 0) { TL = c; break; }
+    if (!TL) return;
+    int TX, TY;
+    if (h->ndim == 2) {
+        TY = 1;
+        TX = 1024 / TL;
+        while (TX * TL > 256 && h->L[0] % TX) TX /= 2;
+        if (h->L[0] % TX) return;
+    } else {
+        TY = 8;
+        TX = std::max(1, 1024 / (TL * TY));
+        while (TX * TY * TL > 256 && h->L[0] % TX) TX /= 2;
+        while (TX * TY * TL > 256 && h->L[1] % TY) TY /= 2;
+        if (h->L[0] % TX || h->L[1] % TY) return;
+    }
+    if ((TX * TY * TL) % (kpm::kTmaConsumerWarps * 32) != 0) return;
+    if ((TX * 8) % 16 != 0) return;  // eps box inner dimension
+    const kpm::SlotLayout SL(h->ndim, TX, TY, TL, h->d_eps != nullptr);
+    const size_t tile = (size_t)TX * TY * TL * 16;
+    p->tma_smem = kpm::kSA * (size_t)SL.bytes + kpm::kSP * tile + 3 * (size_t)p->RP * 8 +
+                  3 * (size_t)kpm::kTmaConsumerWarps * 32 * 16 + (2 * kpm::kSA + 2 * kpm::kSP) * 8;
+    if (p->tma_smem > 227 * 1024) return;
+    const long long Lm = h->ndim == 2 ? h->L[1] : h->L[2];
+    const long long W = (long long)(RG / TL) * (h->L[0] / TX) * (h->ndim == 3 ? h->L[1] / TY : 1) * Lm;
+    p->TL = TL;
+    p->TX = TX;
+    p->TY = TY;
+    p->tma_grid = (int)std::min<long long>(W, h->num_sms);
+    p->use_tma = true;
+}
 
 kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p) {
     if (N < 1) return fail(KPM_ERR_INVALID_ARG, "N must be >= 1 (got %d)", N);
@@ -118,6 +171,8 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->gy = (p->RG + tr - 1) / tr;
     const long long site_ctas = (h->D + p->TS - 1) / p->TS;
     p->gx = (int)std::min<long long>(site_ctas, 2LL * h->num_sms);
+    plan_tma(h, flags, p);
+    if (p->use_tma) p->gx = p->tma_grid;
     p->nslots = N;
     p->lane_bytes = (size_t)h->D * p->RG * sizeof(double2);
     size_t off = 0;
@@ -205,6 +260,94 @@ kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& 
         case 6: return launch_mode<false>(h, p, StencilOp<3, false, false>{g}, mode, v, tail);
         default: return launch_mode<false>(h, p, StencilOp<3, true, false>{g}, mode, v, tail);
     }
+}
+
+using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
+
+EncodeFn get_encode() {
+    static EncodeFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(ptr);
+    }
+    return fn;
+}
+
+// Tensor map over the lane-layout vector block viewed as doubles [L2][L1][L0][2 RG]
+// (rank 3 in 2D, 4 in 3D) with the given box.
+kpm_status make_vec_map(const kpm_handle_s* h, const Plan& p, void* base, int bx, int by, int bz, CUtensorMap* m) {
+    EncodeFn enc = get_encode();
+    if (!enc) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const int rank = h->ndim + 1;
+    cuuint64_t dims[4] = {(cuuint64_t)2 * p.RG, (cuuint64_t)h->L[0], (cuuint64_t)h->L[1], (cuuint64_t)h->L[2]};
+    cuuint64_t strides[3] = {(cuuint64_t)p.RG * 16, (cuuint64_t)p.RG * 16 * h->L[0], (cuuint64_t)p.RG * 16 * h->L[0] * h->L[1]};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * p.TL), (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+    if (h->ndim == 2) box[2] = 1;
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled (vectors) failed: %d", (int)r);
+    return KPM_OK;
+}
+
+kpm_status make_eps_map(const kpm_handle_s* h, const Plan& p, CUtensorMap* m) {
+    EncodeFn enc = get_encode();
+    if (!enc) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const int rank = h->ndim;
+    cuuint64_t dims[3] = {(cuuint64_t)h->L[0], (cuuint64_t)h->L[1], (cuuint64_t)h->L[2]};
+    cuuint64_t strides[2] = {(cuuint64_t)h->L[0] * 8, (cuuint64_t)h->L[0] * h->L[1] * 8};
+    cuuint32_t box[3] = {(cuuint32_t)p.TX, (cuuint32_t)(h->ndim == 3 ? p.TY : 1), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, h->d_eps, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled (eps) failed: %d", (int)r);
+    return KPM_OK;
+}
+
+// Maps of one vector buffer in the a_n role (main, x-halo column, y-halo row) and the a_{n-1} role.
+struct BufMaps {
+    CUtensorMap A, Col, Row, P;
+};
+
+kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMaps* bm) {
+    KPM_TRY(make_vec_map(h, p, base, p.TX, p.TY, 1, &bm->A));
+    KPM_TRY(make_vec_map(h, p, base, 1, p.TY, 1, &bm->Col));
+    KPM_TRY(make_vec_map(h, p, base, p.TX, 1, 1, &bm->Row));
+    bm->P = bm->A;
+    return KPM_OK;
+}
+
+template <int NDIM, bool ONSITE, bool PEIERLS>
+kpm_status launch_tma_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
+                        const kpm::TmaGeom& g, int tail) {
+    auto kern = kpm::kpm_step_tma_kernel<NDIM, ONSITE, PEIERLS>;
+    static size_t configured = 0;
+    if (configured < p.tma_smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma_smem));
+        configured = p.tma_smem;
+    }
+    kern<<<p.tma_grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.A, cur.Col, cur.Row, prev.P, E, g, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
+kpm_status launch_tma(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
+                      const kpm::TmaGeom& g, int tail) {
+    const bool on = h->d_eps != nullptr;
+    if (h->ndim == 2) {
+        if (is_cplx(h)) {
+            if (on) return launch_tma_t<2, true, true>(h, p, cur, prev, E, g, tail);
+            return launch_tma_t<2, false, true>(h, p, cur, prev, E, g, tail);
+        }
+        if (on) return launch_tma_t<2, true, false>(h, p, cur, prev, E, g, tail);
+        return launch_tma_t<2, false, false>(h, p, cur, prev, E, g, tail);
+    }
+    if (on) return launch_tma_t<3, true, false>(h, p, cur, prev, E, g, tail);
+    return launch_tma_t<3, false, false>(h, p, cur, prev, E, g, tail);
 }
 
 kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) {
@@ -527,6 +670,31 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
 
     // Recursion steps (Eq 18), a_{n+1} over a_{n-1}; swap roles after each step.
     const int nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
+    BufMaps mapsP, mapsC;
+    CUtensorMap mapE;
+    memset(&mapE, 0, sizeof mapE);
+    kpm::TmaGeom tg{};
+    if (p.use_tma && nsteps > 0) {
+        KPM_TRY(make_buf_maps(h, p, P, &mapsP));
+        KPM_TRY(make_buf_maps(h, p, C, &mapsC));
+        if (h->d_eps) KPM_TRY(make_eps_map(h, p, &mapE));
+        tg.L0 = (int)h->L[0];
+        tg.L1 = (int)h->L[1];
+        tg.L2 = (int)h->L[2];
+        tg.TX = p.TX;
+        tg.TY = p.TY;
+        tg.TL = p.TL;
+        tg.RG = p.RG;
+        tg.G_L = p.RG / p.TL;
+        tg.PX = (int)(h->L[0] / p.TX);
+        tg.PY = h->ndim == 3 ? (int)(h->L[1] / p.TY) : 1;
+        tg.Lm = (int)(h->ndim == 2 ? h->L[1] : h->L[2]);
+        tg.W = (long long)tg.G_L * tg.PX * tg.PY * tg.Lm;
+        tg.RP = p.RP;
+        tg.t = h->t_scaled;
+        tg.shift = -h->b / h->a;
+        tg.phase = h->d_phase;
+    }
     KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
     double2* cur = C;   // a_n
     double2* prev = P;  // a_{n-1}
@@ -542,7 +710,15 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
             v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
             const bool tail = (N & 1) && n == nsteps;    // odd N: <a_M|a_M> -> mu_{N-1}
             v.red2 = tail ? part + (size_t)(2 * n + 2) * slot : nullptr;
-            KPM_TRY(launch(h, p, kpm::STEP, v, tail));
+            if (p.use_tma) {
+                tg.red0 = v.red0;
+                tg.red1 = v.red1;
+                tg.red2 = v.red2;
+                tg.out = prev;
+                KPM_TRY(launch_tma(h, p, cur == C ? mapsC : mapsP, cur == C ? mapsP : mapsC, mapE, tg, tail));
+            } else {
+                KPM_TRY(launch(h, p, kpm::STEP, v, tail));
+            }
         }
         h->step_launches++;
         std::swap(cur, prev);
@@ -660,6 +836,21 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
     }
     if (step_launches) *step_launches = h->step_launches;
     if (total_launches) *total_launches = h->total_launches;
+    return KPM_OK;
+}
+
+kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[8]) {
+    if (!h || !info) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
+    Plan p;
+    KPM_TRY(make_plan(h, N, R, flags, false, &p));
+    info[0] = p.use_tma;
+    info[1] = p.TL;
+    info[2] = p.TX;
+    info[3] = p.TY;
+    info[4] = p.gx;
+    info[5] = (int64_t)p.tma_smem;
+    info[6] = p.RG;
+    info[7] = 0;
     return KPM_OK;
 }
 

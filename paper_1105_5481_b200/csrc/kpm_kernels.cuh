@@ -212,13 +212,13 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
     sred[2 * nthr + tid] = acc2;
     __syncthreads();
     if (threadIdx.y == 0 && active) {
-        double* rows[3] = {v.red0, v.red1, tail ? v.red2 : nullptr};
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
-            if (rows[k] == nullptr) continue;
+            double* rowk = k == 0 ? v.red0 : (k == 1 ? v.red1 : (tail ? v.red2 : nullptr));
+            if (rowk == nullptr) continue;
             double2 s = make_double2(0.0, 0.0);
             for (int ty = 0; ty < TS; ++ty) s = add2(s, sred[k * nthr + ty * TR + threadIdx.x]);
-            double* row = rows[k] + (size_t)blockIdx.x * v.RP;
+            double* row = rowk + (size_t)blockIdx.x * v.RP;
             if (CPLX) {
                 row[rg] = s.x;
             } else {

@@ -31,7 +31,7 @@ KPM_PART_NONE, KPM_PART_VECTORS = 0, 1
 EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershgorin_stencil",
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
-           "kpm_step_bytes", "kpm_destroy", "kpm_last_error", "kpm_version"]
+           "kpm_step_bytes", "kpm_plan_info", "kpm_destroy", "kpm_last_error", "kpm_version"]
 
 
 class kpm_stencil_desc(ctypes.Structure):
@@ -60,6 +60,7 @@ _SIG = {
     "kpm_dos": [_P, _i32, _i32, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_last_timing": [_P, _P, _P, _P],
     "kpm_step_bytes": [_P, _i64, _P],
+    "kpm_plan_info": [_P, _i32, _i64, _u32, _P],
 }
 for _name, _args in _SIG.items():
     _fn = getattr(_lib, _name)
@@ -214,6 +215,12 @@ class Handle:
         ms, sl, tl = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
         _check(_lib.kpm_last_timing(self._h, ctypes.byref(ms), ctypes.byref(sl), ctypes.byref(tl)))
         return ms.value, sl.value, tl.value
+
+    def plan_info(self, N, R, flags=0):
+        info = np.zeros(8, dtype=np.int64)
+        _check(_lib.kpm_plan_info(self._h, int(N), int(R), int(flags), _ptr(info)))
+        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "_"]
+        return {k: int(v) for k, v in zip(keys, info) if k != "_"}
 
     def step_bytes(self, R):
         b = ctypes.c_double()

@@ -72,6 +72,40 @@ def test_moments_match_oracle(kpm, case, form):
     assert np.array_equal(h.moments(N, R, 11), mu), "not deterministic"
 
 
+# shapes that take the TMA-pipelined march kernel (lanes per site a multiple of 8, tiles
+# dividing the lattice), incl. more planes than CTAs (ranges crossing pencils), PX = PY = 1
+TMA_CASES = {
+    "2d_R64": (lat_of(2, (64, 200)), 40, 64),
+    "2d_anderson_R16": (lat_of(2, (128, 24), W=2.0), 33, 16),
+    "2d_peierls_R32": (lat_of(2, (64, 16), flux=1 / 8), 41, 32),
+    "2d_peierls_anderson_R16": (lat_of(2, (32, 30), flux=1 / 4, W=1.0), 30, 16),
+    "3d_R16": (lat_of(3, (32, 32, 40)), 24, 16),
+    "3d_anderson_R32": (lat_of(3, (16, 16, 10), W=2.0), 31, 32),
+    "3d_single_pencil": (lat_of(3, (16, 8, 6), W=1.0), 20, 16),
+    "3d_anderson_R48": (lat_of(3, (32, 16, 12), W=2.0), 19, 48),
+}
+
+
+@pytest.mark.parametrize("case", sorted(TMA_CASES))
+def test_tma_march_matches_oracle(kpm, case):
+    lat, N, R = TMA_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b -= 0.03 * a
+    a *= 1.05
+    r = ki.rademacher(21, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b)
+    info = h.plan_info(N, R)
+    assert info["tma"] == 1, info
+    mu = h.moments(N, R, 21)
+    assert normwise(mu, ref) < TOL
+    pv = h.moments_ex(N, R, 21, flags=kpm.KPM_PER_VECTOR)
+    assert normwise(pv, ref_pv) < TOL
+    assert np.array_equal(h.moments(N, R, 21), mu), "not deterministic"
+    assert np.array_equal(h.moments_ex(N, R, 21, r0=r), mu)
+
+
 @pytest.mark.parametrize("case", ["2d", "3d_anderson", "peierls"])
 def test_direct_mode_matches_oracle_direct(kpm, case):
     """KPM_DIRECT: the paper's own estimator, Eq (19): mu_n = <r|a_n>, N-1 products."""
