@@ -96,6 +96,19 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profiled_traffic(config, plan):
+    """dram__bytes_read.sum + dram__bytes_write.sum per step launch from the committed ncu
+    capture of this config's step kernel (profiles/*.json), or None."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        rec = json.load(open(p))[config]
+    except Exception:
+        return None
+    if rec.get("tma") != plan["tma"]:
+        return None
+    return rec["dram_bytes_per_launch"]
+
+
 def oracle_sample(cfg, lat, a, b, seconds_target=15.0):
     """The oracle as it stands, on a bounded sample of the workload: full D and N,
     R' = #threads vectors (more if that is quick).  Returns value in D*N*R/s."""
@@ -223,6 +236,9 @@ def main():
 
     # roofline of the dominant kernel: the fused recursion step
     peak, peak_kind = peak_hbm()
+    plan = h.plan_info(N, R)
+    kname = ("kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan["tma"]
+             else "kpm_step_kernel (fused stencil SpMM + recursion + reductions)")
     step_bytes = h.step_bytes(R)
     avg_step_ms = steps_ms / max(step_launches, 1)
     achieved = step_bytes / (avg_step_ms / 1000.0) / 1e9
@@ -275,10 +291,11 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Rademacher vectors, lattice H)",
                 "config": config_obj(args, cfg, lat, world),
                 "hbm_gbs_alg": step_bytes * (N // 2) / (ms_per_step / 1000.0) / 1e9 * world,
-                "roofline": {"bound": "hbm", "kernel": "kpm_step_kernel (fused SpMM + recursion + reductions)",
-                             "achieved": achieved, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                             "frac": achieved / peak, "traffic": None, "alg_bytes_per_launch": step_bytes,
-                             "avg_launch_ms": avg_step_ms},
+                "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                             "traffic": profiled_traffic(args.config, plan),
+                             "alg_bytes_per_launch": step_bytes, "avg_launch_ms": avg_step_ms,
+                             "frac_of_8TBs_spec": achieved / 8000.0, "plan": plan},
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
                                                         "max_abs_mu": float(np.abs(mu_host).max())}}

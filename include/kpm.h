@@ -154,9 +154,15 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
 
 /* Raw sums S[N] (summed over all ranks) -> mu[N]: mu_0 = S_0/(D R), mu_1 = S_1/(D R),
  * mu_{2n} = 2 S_{2n}/(D R) - mu_0, mu_{2n+1} = 2 S_{2n+1}/(D R) - mu_1; with KPM_DIRECT
- * mu_n = S_n/(D R).  KPM_DEVICE_OUT: S and mu are device pointers (handle's stream). */
-kpm_status kpm_assemble(kpm_handle h, const double* S, int32_t N, int64_t R, uint32_t flags,
+ * mu_n = S_n/(D R).  D = number of sites, R = global number of vectors.
+ * Default: S and mu are host arrays and the transform runs on the host (h may be NULL).
+ * KPM_DEVICE_OUT: S and mu are device pointers; a kernel on h's stream does it. */
+kpm_status kpm_assemble(kpm_handle h, const double* S, int32_t N, int64_t D, int64_t R, uint32_t flags,
                         double* mu);
+
+/* The random-vector partition (KPM_PART_VECTORS): rank owns global vectors
+ * [begin, begin + count) = [R*rank/world, R*(rank+1)/world).  Host only. */
+kpm_status kpm_vector_range(int64_t R, int32_t rank, int32_t world, int64_t* begin, int64_t* count);
 
 /* Eq (6) mapped back to omega (Eq 11-12; X9):
  *   rho(omega_k) = [g_0 mu_0 + 2 sum_{n=1}^{N-1} g_n mu_n T_n(x_k)] / (pi a sqrt(1 - x_k^2)),

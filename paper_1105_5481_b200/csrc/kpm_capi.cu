@@ -189,17 +189,21 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     return KPM_OK;
 }
 
+// Workspace from the device's stream-ordered pool (release threshold raised at handle
+// creation), so creating/destroying handles per call does not pay cudaMalloc/cudaFree.
 kpm_status ensure_workspace(kpm_handle_s* h, size_t bytes) {
     if (h->ws_bytes >= bytes) return KPM_OK;
     if (!h->ws_own) return fail(KPM_ERR_OOM, "caller workspace has %zu bytes, need %zu", h->ws_bytes, bytes);
-    if (h->ws) cudaFree(h->ws);
+    if (h->ws) cudaFreeAsync(h->ws, h->stream);
     h->ws = nullptr;
     h->ws_bytes = 0;
-    cudaError_t e = cudaMalloc(&h->ws, bytes);
+    void* p = nullptr;
+    cudaError_t e = cudaMallocAsync(&p, bytes, h->stream);
     if (e != cudaSuccess) {
         cudaGetLastError();
-        return fail(KPM_ERR_OOM, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+        return fail(KPM_ERR_OOM, "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
     }
+    h->ws = static_cast<char*>(p);
     h->ws_bytes = bytes;
     return KPM_OK;
 }
@@ -367,6 +371,11 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
     h->device = device;
     if (dist) h->dist = *dist;
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t keep = UINT64_MAX;  // keep freed workspace in the pool for the next handle
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+    }
     cudaError_t e = cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev_begin);
     if (e == cudaSuccess) e = cudaEventCreate(&h->ev_end);
@@ -414,8 +423,8 @@ const char* kpm_version(void) { return "kpm-b200 0.1 (sm_100a)"; }
 void kpm_destroy(kpm_handle h) {
     if (!h) return;
     cudaSetDevice(h->device);
+    if (h->ws_own && h->ws) cudaFreeAsync(h->ws, h->stream);
     if (h->stream) cudaStreamSynchronize(h->stream);
-    if (h->ws_own && h->ws) cudaFree(h->ws);
     cudaFree(h->d_eps);
     cudaFree(h->d_phase);
     cudaFree(h->d_col);
@@ -603,8 +612,8 @@ kpm_status kpm_set_workspace(kpm_handle h, void* dev_ptr, size_t bytes) {
     if (dev_ptr && (reinterpret_cast<uintptr_t>(dev_ptr) % kAlign) != 0)
         return fail(KPM_ERR_INVALID_ARG, "workspace must be %zu-byte aligned", kAlign);
     KPM_CUDA(cudaSetDevice(h->device));
+    if (h->ws_own && h->ws) cudaFreeAsync(h->ws, h->stream);
     cudaStreamSynchronize(h->stream);
-    if (h->ws_own && h->ws) cudaFree(h->ws);
     h->ws = static_cast<char*>(dev_ptr);
     h->ws_bytes = dev_ptr ? bytes : 0;
     h->ws_own = dev_ptr == nullptr;
@@ -775,29 +784,30 @@ kpm_status kpm_moments(kpm_handle h, int32_t N, int64_t R, uint64_t seed, double
     return kpm_moments_ex(h, N, R, seed, nullptr, 0u, mu);
 }
 
-kpm_status kpm_assemble(kpm_handle h, const double* S, int32_t N, int64_t R, uint32_t flags, double* mu) {
-    if (!h || !S || !mu || N < 1 || R < 1) return fail(KPM_ERR_INVALID_ARG, "bad kpm_assemble arguments");
-    KPM_CUDA(cudaSetDevice(h->device));
+kpm_status kpm_assemble(kpm_handle h, const double* S, int32_t N, int64_t D, int64_t R, uint32_t flags, double* mu) {
+    if (!S || !mu || N < 1 || R < 1 || D < 1) return fail(KPM_ERR_INVALID_ARG, "bad kpm_assemble arguments");
     const int direct = (flags & KPM_DIRECT) ? 1 : 0;
-    const double c = 1.0 / ((double)h->D * (double)R);
-    double* dS = nullptr;
-    double* dmu = nullptr;
-    const bool dev = (flags & KPM_DEVICE_OUT) != 0;
-    if (dev) {
-        dS = const_cast<double*>(S);
-        dmu = mu;
-    } else {
-        KPM_CUDA(cudaMallocAsync(&dS, 2 * (size_t)N * sizeof(double), h->stream));
-        dmu = dS + N;
-        KPM_CUDA(cudaMemcpyAsync(dS, S, (size_t)N * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    const double c = 1.0 / ((double)D * (double)R);
+    if (!(flags & KPM_DEVICE_OUT)) {
+        // host: the same transform as assemble_kernel (a6: N multiply-adds)
+        for (int n = 0; n < N; ++n) {
+            const double x = S[n] * c;
+            mu[n] = (direct || n < 2) ? x : 2.0 * x - ((n & 1) ? S[1] * c : S[0] * c);
+        }
+        return KPM_OK;
     }
-    kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(dS, N, c, direct, dmu);
+    if (!h) return fail(KPM_ERR_INVALID_ARG, "device kpm_assemble needs a handle (stream)");
+    KPM_CUDA(cudaSetDevice(h->device));
+    kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, c, direct, mu);
     KPM_CUDA(cudaGetLastError());
-    if (!dev) {
-        KPM_CUDA(cudaMemcpyAsync(mu, dmu, (size_t)N * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
-        KPM_CUDA(cudaFreeAsync(dS, h->stream));
-        KPM_CUDA(cudaStreamSynchronize(h->stream));
-    }
+    return KPM_OK;
+}
+
+kpm_status kpm_vector_range(int64_t R, int32_t rank, int32_t world, int64_t* begin, int64_t* count) {
+    if (R < 1 || world < 1 || rank < 0 || rank >= world || !begin || !count)
+        return fail(KPM_ERR_INVALID_ARG, "bad kpm_vector_range arguments");
+    *begin = R * rank / world;
+    *count = R * (rank + 1) / world - *begin;
     return KPM_OK;
 }
 

@@ -31,7 +31,7 @@ KPM_PART_NONE, KPM_PART_VECTORS = 0, 1
 EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershgorin_stencil",
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
-           "kpm_step_bytes", "kpm_plan_info", "kpm_destroy", "kpm_last_error", "kpm_version"]
+           "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_destroy", "kpm_last_error", "kpm_version"]
 
 
 class kpm_stencil_desc(ctypes.Structure):
@@ -56,7 +56,8 @@ _SIG = {
     "kpm_set_workspace": [_P, _P, _sz],
     "kpm_moments": [_P, _i32, _i64, _u64, _P],
     "kpm_moments_ex": [_P, _i32, _i64, _u64, _P, _u32, _P],
-    "kpm_assemble": [_P, _P, _i32, _i64, _u32, _P],
+    "kpm_assemble": [_P, _P, _i32, _i64, _i64, _u32, _P],
+    "kpm_vector_range": [_i64, _i32, _i32, _P, _P],
     "kpm_dos": [_P, _i32, _i32, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_last_timing": [_P, _P, _P, _P],
     "kpm_step_bytes": [_P, _i64, _P],
@@ -170,8 +171,7 @@ class Handle:
         if self.dist is None or self.dist[0] != KPM_PART_VECTORS:
             return 0, int(R)
         _, rank, world = self.dist
-        lo, hi = R * rank // world, R * (rank + 1) // world
-        return lo, hi - lo
+        return kpm_vector_range(R, rank, world)
 
     def moments(self, N, R, seed):
         mu = np.zeros(int(N), dtype=np.float64)
@@ -202,14 +202,12 @@ class Handle:
         return res
 
     def assemble(self, S, N, R, flags=0, out=None):
+        """Raw sums -> moments (kpm_assemble); S: host array, or int device pointer with out."""
         if isinstance(S, (int, np.integer)):
-            _check(_lib.kpm_assemble(self._h, ctypes.c_void_p(int(S)), int(N), int(R),
+            _check(_lib.kpm_assemble(self._h, ctypes.c_void_p(int(S)), int(N), self.D, int(R),
                                      int(flags) | KPM_DEVICE_OUT, ctypes.c_void_p(int(out))))
             return None
-        S = np.ascontiguousarray(S, dtype=np.float64)
-        mu = np.zeros(int(N), dtype=np.float64)
-        _check(_lib.kpm_assemble(self._h, _ptr(S), int(N), int(R), int(flags) & ~KPM_DEVICE_OUT, _ptr(mu)))
-        return mu
+        return kpm_assemble_host(S, N, self.D, R, flags)
 
     def last_timing(self):
         ms, sl, tl = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
@@ -269,6 +267,21 @@ def kpm_assemble(h: Handle, S, N, R, flags=0, out=None):
     return h.assemble(S, N, R, flags=flags, out=out)
 
 
+def kpm_assemble_host(S, N, D, R, flags=0):
+    """kpm_assemble on host arrays (no GPU needed)."""
+    S = np.ascontiguousarray(S, dtype=np.float64)
+    mu = np.zeros(int(N), dtype=np.float64)
+    _check(_lib.kpm_assemble(None, _ptr(S), int(N), int(D), int(R), int(flags) & ~KPM_DEVICE_OUT, _ptr(mu)))
+    return mu
+
+
+def kpm_vector_range(R, rank, world):
+    """(begin, count) of the global vectors rank owns under KPM_PART_VECTORS."""
+    b, c = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.kpm_vector_range(int(R), int(rank), int(world), ctypes.byref(b), ctypes.byref(c)))
+    return b.value, c.value
+
+
 def kpm_dos(mu, a, b, omega, kernel=KPM_KERNEL_JACKSON, device=0):
     mu = np.ascontiguousarray(mu, dtype=np.float64)
     om = np.ascontiguousarray(omega, dtype=np.float64)
@@ -282,18 +295,27 @@ def kpm_destroy(h: Handle):
     h.close()
 
 
-def moments_distributed(h: Handle, N, R, seed, group=None, flags=0):
-    """Vector partition across ranks (one process per GPU): each rank runs its share of
-    the R vectors, the raw sums S[N] are summed over ranks with ONE all-reduce
-    (torch.distributed over NCCL), then assembled into mu on the device."""
+def moments_distributed(h, N, R, seed, group=None, flags=0, device=None):
+    """Random-vector partition across ranks (one process per GPU): each rank runs its
+    share of the R vectors (global vector indices, so the vector set does not depend on
+    the number of ranks), the raw sums S[N] are summed over ranks with ONE all-reduce
+    (torch.distributed; NCCL over NVLink on GPUs), then assembled into mu.
+    device: torch device for the sums (default: the current CUDA device; a CPU device
+    uses host sums, e.g. with the gloo backend)."""
     import torch
     import torch.distributed as dist
-    dev = torch.device("cuda", torch.cuda.current_device())
-    S = torch.empty(int(N), dtype=torch.float64, device=dev)
-    h.moments_ex(N, R, seed, flags=flags | KPM_RAW_SUMS | KPM_DEVICE_OUT, out=S.data_ptr())
-    torch.cuda.synchronize(dev)
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.type == "cuda":
+        S = torch.empty(int(N), dtype=torch.float64, device=device)
+        h.moments_ex(N, R, seed, flags=flags | KPM_RAW_SUMS | KPM_DEVICE_OUT, out=S.data_ptr())
+        torch.cuda.synchronize(device)
+        dist.all_reduce(S, op=dist.ReduceOp.SUM, group=group)
+        mu = torch.empty_like(S)
+        h.assemble(S.data_ptr(), N, R, flags=flags & KPM_DIRECT, out=mu.data_ptr())
+        torch.cuda.synchronize(device)
+        return mu.cpu().numpy()
+    S = torch.from_numpy(np.ascontiguousarray(h.moments_ex(N, R, seed, flags=flags | KPM_RAW_SUMS)))
     dist.all_reduce(S, op=dist.ReduceOp.SUM, group=group)
-    mu = torch.empty_like(S)
-    h.assemble(S.data_ptr(), N, R, flags=flags & KPM_DIRECT, out=mu.data_ptr())
-    torch.cuda.synchronize(dev)
-    return mu.cpu().numpy()
+    return h.assemble(S.numpy(), N, R, flags=flags & KPM_DIRECT)
