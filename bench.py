@@ -109,21 +109,31 @@ def profiled_traffic(config, plan):
     return rec["dram_bytes_per_launch"]
 
 
-def oracle_sample(cfg, lat, a, b, seconds_target=15.0):
-    """The oracle as it stands, on a bounded sample of the workload: full D and N,
-    R' = #threads vectors (more if that is quick).  Returns value in D*N*R/s."""
+def oracle_sample(cfg, lat, a, b, target_s=15.0):
+    """The oracle as it stands, on a bounded sample of the workload: full D, R' vectors
+    (one per host thread, fewer for huge D), and the first N' <= N moments chosen from a
+    short calibration run so the sample takes ~target_s.  Returns D*N'*R'/s."""
     import oracle
     H = oracle.lattice_csr(lat)
     threads = oracle.num_threads()
-    Rs = threads
-    r = ki.rademacher(cfg["seed"], Rs, lat["D"])
+    D = lat["D"]
+    Rs = threads if D <= (1 << 24) else max(1, min(threads, 4))
+    r = ki.rademacher(cfg["seed"], Rs, D)
     t0 = time.perf_counter()
-    oracle.moments_doubling(H, a, b, r, cfg["N"])
+    oracle.moments_doubling(H, a, b, r, 4)                    # 2 products per vector
+    t4 = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.moments_doubling(H, a, b, r, 12)                   # 6 products per vector
+    per_product = max((time.perf_counter() - t0 - t4) / 4, t4 / 8)
+    Ns = int(min(cfg["N"], max(4, 2 * int(target_s / max(per_product, 1e-9)))))
+    t0 = time.perf_counter()
+    oracle.moments_doubling(H, a, b, r, Ns)
     dt = time.perf_counter() - t0
-    value = lat["D"] * cfg["N"] * Rs / dt
-    sample = (f"{Rs} of {cfg['R']} vectors (global vectors 0..{Rs - 1}) at full D={lat['D']} and N={cfg['N']}; "
-              f"{dt:.2f} s of CPU time on {threads} OpenMP threads; CSR build excluded")
-    return value, threads, sample, dt
+    value = D * Ns * Rs / dt
+    cores = min(threads, Rs)
+    sample = (f"{Rs} of {cfg['R']} vectors (global 0..{Rs - 1}), full D={D}, first {Ns} of N={cfg['N']} moments "
+              f"({Ns // 2} products per vector); {dt:.2f} s wall on {cores} OpenMP threads; CSR build excluded")
+    return value, cores, sample, dt
 
 
 def run_reference(args, cfg, lat, a, b, rank, world):

@@ -182,7 +182,8 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
 /* Execution plan kpm_moments_ex would use for (N, R, flags): info[0] = 1 if the
  * TMA-pipelined march kernel runs the recursion steps (2D/3D stencils), else 0;
  * info[1..3] = lanes per tile TL, tile TX, TY; info[4] = CTAs per step launch;
- * info[5] = dynamic shared memory bytes of the step kernel; info[6] = lanes per site. */
+ * info[5] = dynamic shared memory bytes of the step kernel; info[6] = lanes per site;
+ * info[7] = 1 if whole (lane group, pencil) columns are dealt round-robin to CTAs. */
 kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[8]);
 
 /* Algorithmic HBM bytes of one recursion-step launch. */

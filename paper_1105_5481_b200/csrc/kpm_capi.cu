@@ -99,7 +99,7 @@ struct Plan {
     int nslots = 0;      // moment slots = N
     // TMA-pipelined step kernel (2D/3D stencils), see kpm_tma.cuh
     bool use_tma = false;
-    int TL = 0, TX = 0, TY = 0, tma_grid = 0;
+    int TL = 0, TX = 0, TY = 0, tma_grid = 0, tma_rr = 0;
     size_t tma_smem = 0;
     size_t lane_bytes = 0;
     size_t off_P = 0, off_C = 0, off_R = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0, total = 0;
@@ -149,6 +149,9 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     p->TX = TX;
     p->TY = TY;
     p->tma_grid = (int)std::min<long long>(W, h->num_sms);
+    // 3D: whole columns round-robin when there are enough of them (in-plane halos then hit L2)
+    const long long cols = W / Lm;
+    p->tma_rr = (h->ndim == 3 && cols >= 4LL * p->tma_grid && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
     p->use_tma = true;
 }
 
@@ -699,6 +702,7 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
         tg.PY = h->ndim == 3 ? (int)(h->L[1] / p.TY) : 1;
         tg.Lm = (int)(h->ndim == 2 ? h->L[1] : h->L[2]);
         tg.W = (long long)tg.G_L * tg.PX * tg.PY * tg.Lm;
+        tg.rr = p.tma_rr;
         tg.RP = p.RP;
         tg.t = h->t_scaled;
         tg.shift = -h->b / h->a;
@@ -860,7 +864,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[4] = p.gx;
     info[5] = (int64_t)p.tma_smem;
     info[6] = p.RG;
-    info[7] = 0;
+    info[7] = p.tma_rr;
     return KPM_OK;
 }
 

@@ -273,10 +273,11 @@ __global__ void finish_kernel(const double* __restrict__ partial, int nCTA, int 
 
 // Doubling transform + normalisation (north_star; Eq 19 for direct):
 // mu_0 = S_0 c, mu_1 = S_1 c, mu_{2n} = 2 S_{2n} c - mu_0, mu_{2n+1} = 2 S_{2n+1} c - mu_1.
+// (explicitly rounded ops: no FMA contraction, so the host path of kpm_assemble gives the same bits)
 __device__ __forceinline__ double assemble_one(const double* S, long long stride, int n, double c, int direct) {
-    const double x = S[(size_t)n * stride] * c;
+    const double x = __dmul_rn(S[(size_t)n * stride], c);
     if (direct || n < 2) return x;
-    return 2.0 * x - ((n & 1) ? S[stride] * c : S[0] * c);
+    return __dsub_rn(__dmul_rn(2.0, x), __dmul_rn((n & 1) ? S[stride] : S[0], c));
 }
 
 __global__ void assemble_kernel(const double* __restrict__ S, int N, double c, int direct, double* __restrict__ mu) {

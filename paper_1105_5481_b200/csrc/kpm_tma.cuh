@@ -109,6 +109,7 @@ struct TmaGeom {
     int PX, PY;       // pencils along x, y (PY = 1 in 2D)
     int Lm;           // march extent (L1 in 2D, L2 in 3D)
     long long W;      // total output planes = G_L * PX * PY * Lm
+    int rr;           // 1: round-robin whole columns over CTAs; 0: contiguous plane ranges
     int RP;           // padded vectors (partial row length)
     double t;         // t / a
     double shift;     // -b / a (no on-site array)
@@ -140,21 +141,49 @@ struct SlotLayout {
     }
 };
 
-// Segment iterator over the CTA's contiguous range of output planes.
+// Work schedule.  A "column" is one (lane group, pencil) marched over all Lm planes.
+//  * contiguous (rr == 0): CTA c owns output planes [W c/G, W (c+1)/G) of the
+//    column-major plane order -- used when there are fewer columns than CTAs (2D);
+//  * round-robin (rr == 1): CTA c owns whole columns c, c+G, c+2G, ...; all CTAs
+//    march spatially adjacent pencils through the same planes at the same time, so
+//    the in-plane halos one CTA loads are the main tiles its neighbours load a moment
+//    earlier or later -- L2 hits instead of DRAM re-reads (3D).
 struct Seg {
     int lg, px, py, m0, m1;  // lane group, pencil, planes [m0, m1)
 };
-__device__ __forceinline__ bool next_seg(const TmaGeom& g, long long& w, long long w_end, Seg& s) {
-    if (w >= w_end) return false;
-    const long long col = w / g.Lm;
-    s.m0 = (int)(w - col * g.Lm);
-    const long long seg_end = min(w_end, (col + 1) * (long long)g.Lm);
-    s.m1 = s.m0 + (int)(seg_end - w);
+struct Sched {
+    long long w, w_end;  // contiguous: plane cursor; round-robin: column cursor / count
+};
+__device__ __forceinline__ Sched sched_begin(const TmaGeom& g) {
+    Sched q;
+    if (g.rr) {
+        q.w = blockIdx.x;
+        q.w_end = g.W / g.Lm;
+    } else {
+        q.w = g.W * blockIdx.x / gridDim.x;
+        q.w_end = g.W * (blockIdx.x + 1) / gridDim.x;
+    }
+    return q;
+}
+__device__ __forceinline__ bool next_seg(const TmaGeom& g, Sched& q, Seg& s) {
+    if (q.w >= q.w_end) return false;
+    long long col;
+    if (g.rr) {
+        col = q.w;
+        s.m0 = 0;
+        s.m1 = g.Lm;
+        q.w += gridDim.x;
+    } else {
+        col = q.w / g.Lm;
+        s.m0 = (int)(q.w - col * g.Lm);
+        const long long seg_end = min(q.w_end, (col + 1) * (long long)g.Lm);
+        s.m1 = s.m0 + (int)(seg_end - q.w);
+        q.w = seg_end;
+    }
     const int pencil = (int)(col % ((long long)g.PX * g.PY));
     s.lg = (int)(col / ((long long)g.PX * g.PY));
     s.px = pencil % g.PX;
     s.py = pencil / g.PX;
-    w = seg_end;
     return true;
 }
 
@@ -195,8 +224,6 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (int i = threadIdx.x; i < 3 * g.RP; i += blockDim.x) sacc[i] = 0.0;
     __syncthreads();
 
-    const long long w_begin = g.W * blockIdx.x / gridDim.x;
-    const long long w_end = g.W * (blockIdx.x + 1) / gridDim.x;
 
     if (warp == kTmaConsumerWarps) {
         // ---------------------------------------------------------------- producer
@@ -210,9 +237,9 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const uint32_t bytesA = tile_bytes + 2 * g.TY * SL.site_bytes + (NDIM == 3 ? 2 * g.TX * SL.site_bytes : 0) +
                                     (ONSITE ? g.TX * g.TY * 8 : 0);
             long long ia = 0, ip = 0;  // load counters
-            long long w = w_begin;
+            Sched sq = sched_begin(g);
             Seg s;
-            while (next_seg(g, w, w_end, s)) {
+            while (next_seg(g, sq, s)) {
                 const int c0 = 2 * s.lg * g.TL;
                 const int x0 = s.px * g.TX, y0 = s.py * g.TY;
                 const int xl = (x0 - 1 + g.L0) % g.L0, xr = (x0 + g.TX) % g.L0;
@@ -260,7 +287,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         const int npass = g.TX * g.TY / kstep;
         double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0;
         long long ia = 0, ip = 0;
-        long long w = w_begin;
+        Sched sq = sched_begin(g);
         Seg s;
         int cur_lg = -1;
         auto flush = [&](int lg) {
@@ -285,7 +312,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             named_bar_sync(1, CONS);
             acc0 = acc1 = acc2 = make_double2(0.0, 0.0);
         };
-        while (next_seg(g, w, w_end, s)) {
+        while (next_seg(g, sq, s)) {
             if (cur_lg != -1 && s.lg != cur_lg) flush(cur_lg);
             cur_lg = s.lg;
             const int x0 = s.px * g.TX, y0 = s.py * g.TY;

@@ -217,8 +217,8 @@ class Handle:
     def plan_info(self, N, R, flags=0):
         info = np.zeros(8, dtype=np.int64)
         _check(_lib.kpm_plan_info(self._h, int(N), int(R), int(flags), _ptr(info)))
-        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "_"]
-        return {k: int(v) for k, v in zip(keys, info) if k != "_"}
+        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "round_robin"]
+        return {k: int(v) for k, v in zip(keys, info)}
 
     def step_bytes(self, R):
         b = ctypes.c_double()

@@ -83,6 +83,7 @@ TMA_CASES = {
     "3d_anderson_R32": (lat_of(3, (16, 16, 10), W=2.0), 31, 32),
     "3d_single_pencil": (lat_of(3, (16, 8, 6), W=1.0), 20, 16),
     "3d_anderson_R48": (lat_of(3, (32, 16, 12), W=2.0), 19, 48),
+    "3d_round_robin": (lat_of(3, (256, 128, 4), W=2.0), 17, 64),  # 4 lane groups x 256 pencils
 }
 
 
@@ -98,6 +99,7 @@ def test_tma_march_matches_oracle(kpm, case):
     h = make(kpm, lat, a, b)
     info = h.plan_info(N, R)
     assert info["tma"] == 1, info
+    assert info["round_robin"] == (case == "3d_round_robin"), info
     mu = h.moments(N, R, 21)
     assert normwise(mu, ref) < TOL
     pv = h.moments_ex(N, R, 21, flags=kpm.KPM_PER_VECTOR)
