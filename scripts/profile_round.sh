@@ -1,0 +1,20 @@
+#!/bin/bash
+# Profiling pass for profiles/: per config (1) the launch list of one bench step
+# (gpu__time_duration, clock-control none), (2) steady-state DRAM bytes per step launch,
+# (3) one `ncu --set full` capture of the step kernel.
+set -u
+cd "${GRAFT_REPO_ROOT:-/root/repo}"
+OUT=gpurun_out/$1; shift
+CONFIGS=${*:-c2 c3 c4 c5}
+mkdir -p $OUT
+python -c "import __graft_entry__ as g; g.build()"
+B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
+for c in $CONFIGS; do
+  timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
+    --log-file $OUT/launchlist_$c.csv $B --config $c > /dev/null 2>&1
+  timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
+    -k regex:kpm_step -s 4 -c 8 --csv --log-file $OUT/dram_$c.csv $B --config $c > /dev/null 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:kpm_step -s 5 -c 1 \
+    -o $OUT/full_$c $B --config $c > $OUT/full_$c.log 2>&1
+done
+ls -la $OUT

@@ -1,0 +1,128 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+The GPU runs every config whole (all R vectors, full N, KPM_PER_VECTOR output); the
+oracle recomputes sampled vectors one by one (first N_s moments where the full N would
+take minutes on the host) and the per-vector moments must agree to 1e-10 normwise
+(X17).  Properties that hold at any size are checked on everything: mu_0 = 1
+exactly, |mu_n| <= mu_0 (Eq 3), the mean of the per-vector moments equals mu, and for the
+clean lattices the estimator's deviation from the exact trace (analytic spectra, O5) is
+within 5.5 sigma of the exact Rademacher variance (Q9)."""
+import numpy as np
+import pytest
+
+import kpm_inputs as ki
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+# config -> (sampled vector indices, number of moments checked against the oracle)
+SAMPLES = {"c1": ([0, 3, 7], None), "c2": ([0, 63], None), "c3": ([0, 127], 256),
+           "c4": ([0, 255], 512), "c5": ([0, 31], 16)}
+
+
+@pytest.fixture(scope="module")
+def kpm():
+    import torch
+    assert torch.cuda.is_available()
+    from paper_1105_5481_b200 import kpm as k
+    return k
+
+
+def run_full(kpm, name):
+    cfg = ki.CONFIGS[name]
+    lat = ki.lattice(cfg)
+    a, b = kpm.kpm_gershgorin_stencil(lat["ndim"], lat["L"], lat["t"], onsite=lat["onsite"], flux=lat["flux"])
+    h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"])
+    pv = h.moments_ex(cfg["N"], cfg["R"], cfg["seed"], flags=kpm.KPM_PER_VECTOR)
+    mu = h.moments(cfg["N"], cfg["R"], cfg["seed"])
+    plan = h.plan_info(cfg["N"], cfg["R"])
+    h.close()
+    return cfg, lat, a, b, pv, mu, plan
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_fullsize_sampled_parity(kpm, name):
+    cfg, lat, a, b, pv, mu, plan = run_full(kpm, name)
+    N, R = cfg["N"], cfg["R"]
+    assert pv.shape == (R, N)
+    if name != "c1":
+        assert plan["tma"] == 1
+    # properties at full size
+    assert mu[0] == 1.0 and np.all(pv[:, 0] == 1.0)
+    assert np.abs(mu).max() <= 1.0 + 1e-12
+    assert np.abs(pv.mean(axis=0) - mu).max() < 1e-13
+    # sampled vectors against the oracle (a, b from the oracle's own Gerschgorin must agree)
+    H = oracle.lattice_csr(lat)
+    ao, bo = oracle.gershgorin(H)
+    assert abs(ao - a) < 1e-14 * a and abs(bo - b) < 1e-14 * a
+    idx, Ns = SAMPLES[name]
+    Ns = Ns or N
+    for r in idx:
+        rv = ki.rademacher(cfg["seed"], 1, lat["D"], r_offset=r, D_total=lat["D"])
+        ref = oracle.moments_doubling(H, ao, bo, rv, Ns)
+        err = np.abs(pv[r, :Ns] - ref).max() / np.abs(ref).max()
+        assert err < 1e-10, (name, r, err)
+    if name == "c1":
+        ref = oracle.moments_doubling(H, ao, bo, ki.rademacher(cfg["seed"], R, lat["D"]), N)
+        assert np.array_equal(mu, ref)  # Q4: bitwise
+
+
+def exact_variance_z(mu, lam, a, b, D, R):
+    """z-scores of mu against the exact trace for a translation-invariant real or Hermitian H
+    with eigenvalues lam: Var = 2 (sum_k T_n(lam_k)^2 - D mu_n^2) / (D^2 R) (Q9, real vectors)."""
+    x = np.clip((lam - b) / a, -1, 1)
+    th = np.arccos(x)
+    N = len(mu)
+    ex = np.zeros(N)
+    sq = np.zeros(N)
+    for s in range(0, len(th), 1 << 15):
+        T = np.cos(np.outer(np.arange(N), th[s:s + (1 << 15)]))
+        ex += T.sum(axis=1)
+        sq += (T * T).sum(axis=1)
+    ex /= D
+    var = 2 * (sq - D * ex ** 2) / (D * D * R)
+    ok = var > 1e-30
+    return (mu[ok] - ex[ok]) / np.sqrt(var[ok]), ex
+
+
+def test_c2_fullsize_against_exact_trace(kpm):
+    """Q5: the c2 estimate is an unbiased estimate of the exact plane-wave trace."""
+    cfg, lat, a, b, pv, mu, _ = run_full(kpm, "c2")
+    lam = oracle.lattice_spectrum(2, lat["L"], lat["t"])
+    z, ex = exact_variance_z(mu, lam, a, b, lat["D"], cfg["R"])
+    assert np.abs(z).max() < 5.5
+    assert np.abs(ex[1::2]).max() < 1e-13  # bipartite lattice: odd moments vanish (Q8)
+
+
+def test_c4_fullsize_against_harper_trace(kpm):
+    """Q6: the complex128 Peierls estimate (c4) against the exact Harper spectrum; real
+    Rademacher vectors on a complex H give variance <= the real-H formula's bound, so the
+    z-test uses 2 sum T_n^2 / (D^2 R) as a conservative sigma."""
+    cfg, lat, a, b, pv, mu, _ = run_full(kpm, "c4")
+    L0, L1 = lat["L"][0], lat["L"][1]
+    q = 8
+    s = np.arange(q)
+    ky = 2 * np.pi * np.arange(L1) / L1
+    kx = 2 * np.pi * np.arange(L0 // q) / L0
+    KY, KX = np.meshgrid(ky, kx, indexing="ij")
+    M = np.zeros(KY.shape + (q, q), dtype=np.complex128)
+    M[..., s, s] = 2 * lat["t"] * np.cos(2 * np.pi * lat["flux"] * s[None, None, :] - KY[..., None])
+    for u in range(q - 1):
+        M[..., u, u + 1] += lat["t"]
+        M[..., u + 1, u] += lat["t"]
+    M[..., q - 1, 0] += lat["t"] * np.exp(1j * KX * q)
+    M[..., 0, q - 1] += lat["t"] * np.exp(-1j * KX * q)
+    lam = np.linalg.eigvalsh(M).ravel()
+    assert len(lam) == lat["D"]
+    N = 512
+    x = np.clip((lam - b) / a, -1, 1)
+    th = np.arccos(x)
+    ex = np.zeros(N)
+    sq = np.zeros(N)
+    for st in range(0, len(th), 1 << 15):
+        T = np.cos(np.outer(np.arange(N), th[st:st + (1 << 15)]))
+        ex += T.sum(axis=1)
+        sq += (T * T).sum(axis=1)
+    ex /= lat["D"]
+    sig = np.sqrt(2 * sq / (lat["D"] ** 2 * cfg["R"]))
+    assert np.abs((mu[:N] - ex) / sig).max() < 5.5
