@@ -223,7 +223,7 @@ def main():
     torch.cuda.synchronize(dev)
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    steps_ms, step_launches, launches = 0.0, 0, 0
+    steps_ms, step_launches, launches, steps_bytes = 0.0, 0, 0, 0.0
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -231,6 +231,7 @@ def main():
             ms, sl, tl = h.last_timing()   # events the library records on its stream
             steps_ms += ms
             step_launches += sl
+            steps_bytes += h.step_bytes()  # algorithmic bytes of those step launches
             launches += tl + 1             # + the assemble kernel
         ev1.record(stream)
         stream.synchronize()
@@ -247,11 +248,12 @@ def main():
     # roofline of the dominant kernel: the fused recursion step
     peak, peak_kind = peak_hbm()
     plan = h.plan_info(N, R)
-    kname = ("kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan["tma"]
+    kname = ("kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
+             else "kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan["tma"]
              else "kpm_step_kernel (fused stencil SpMM + recursion + reductions)")
-    step_bytes = h.step_bytes(R)
     avg_step_ms = steps_ms / max(step_launches, 1)
-    achieved = step_bytes / (avg_step_ms / 1000.0) / 1e9
+    step_bytes = steps_bytes / max(step_launches, 1)
+    achieved = steps_bytes / (steps_ms / 1000.0) / 1e9
     mu_host = mu.cpu().numpy()
 
     # end-to-end through the public API with host buffers: create (H2D of H~'s data),
@@ -300,7 +302,7 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Rademacher vectors, lattice H)",
                 "config": config_obj(args, cfg, lat, world),
-                "hbm_gbs_alg": step_bytes * (N // 2) / (ms_per_step / 1000.0) / 1e9 * world,
+                "hbm_gbs_alg": steps_bytes / args.steps / (ms_per_step / 1000.0) / 1e9 * world,
                 "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
                              "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
                              "traffic": profiled_traffic(args.config, plan),

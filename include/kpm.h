@@ -183,11 +183,15 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
  * TMA-pipelined march kernel runs the recursion steps (2D/3D stencils), else 0;
  * info[1..3] = lanes per tile TL, tile TX, TY; info[4] = CTAs per step launch;
  * info[5] = dynamic shared memory bytes of the step kernel; info[6] = lanes per site;
- * info[7] = 1 if whole (lane group, pencil) columns are dealt round-robin to CTAs. */
+ * info[7] bit 0: whole (lane group, pencil) columns are dealt round-robin to CTAs;
+ *         bit 1: two recursion steps per launch (temporal blocking, 2D; 4 vector blocks). */
 kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[8]);
 
-/* Algorithmic HBM bytes of one recursion-step launch. */
-kpm_status kpm_step_bytes(kpm_handle h, int64_t R, double* bytes);
+/* Algorithmic HBM bytes moved by the recursion-step launches of the last kpm_moments_ex
+ * call: 3 D R s per single step (read a_n, read a_{n-1}, write
+ * a_{n+1}), 4 D R s per two-step launch, plus 8 D per launch for an on-site array and
+ * K D (4 + s) per launch for ELL.  Divide by kpm_last_timing's steps_ms. */
+kpm_status kpm_step_bytes(kpm_handle h, double* bytes);
 
 void kpm_destroy(kpm_handle h); /* NULL-safe */
 const char* kpm_last_error(void);

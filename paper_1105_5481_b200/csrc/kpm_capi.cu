@@ -21,6 +21,7 @@
 #include "../../include/kpm.h"
 #include "kpm_kernels.cuh"
 #include "kpm_tma.cuh"
+#include "kpm_tma2.cuh"
 
 namespace {
 
@@ -87,6 +88,7 @@ struct kpm_handle_s {
     // timing of the last call
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     int step_launches = 0, total_launches = 0;
+    double steps_bytes = 0.0;  // algorithmic HBM bytes of the recursion-step launches of the last call
 };
 
 namespace {
@@ -101,16 +103,21 @@ struct Plan {
     bool use_tma = false;
     int TL = 0, TX = 0, TY = 0, tma_grid = 0, tma_rr = 0;
     size_t tma_smem = 0;
+    // two steps per launch (temporal blocking, 2D), see kpm_tma2.cuh; needs 4 vector blocks
+    bool use_tma2 = false, no_fused = false;
+    size_t tma2_smem = 0;
     size_t lane_bytes = 0;
-    size_t off_P = 0, off_C = 0, off_R = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0, total = 0;
+    size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
+           total = 0;
 };
 
 bool is_cplx(const kpm_handle_s* h) { return h->dtype == KPM_COMPLEX128; }
 
-bool tma_disabled() {
-    const char* e = getenv("KPM_NO_TMA");
+bool env_on(const char* name) {
+    const char* e = getenv(name);
     return e && e[0] && e[0] != '0';
 }
+bool tma_disabled() { return env_on("KPM_NO_TMA"); }
 
 // Tile choice for the TMA march: ~16 KB main tiles (TX*TY*TL = 1024 lanes), full passes
 // of the 256 consumer threads, tiles dividing the lattice, lane groups dividing RG.
@@ -153,15 +160,23 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     const long long cols = W / Lm;
     p->tma_rr = (h->ndim == 3 && cols >= 4LL * p->tma_grid && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
     p->use_tma = true;
+    // two-step kernel: 2D lattices with L0 >= 4, same tiles, shared memory permitting
+    p->use_tma2 = false;
+    if (h->ndim == 2 && !p->no_fused && !env_on("KPM_NO_TMA2") && h->L[0] >= 4 && h->L[1] >= 4 && TX * TL == 1024) {
+        p->tma2_smem = kpm::step2_smem_bytes(TX, TL, h->d_eps != nullptr, p->RP);
+        p->use_tma2 = p->tma2_smem <= 227 * 1024;
+    }
 }
 
-kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p) {
+kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p,
+                     bool no_fused = false) {
     if (N < 1) return fail(KPM_ERR_INVALID_ARG, "N must be >= 1 (got %d)", N);
     if (R < 1) return fail(KPM_ERR_INVALID_ARG, "R must be >= 1 (got %lld)", (long long)R);
     const int world = h->dist.partition == KPM_PART_VECTORS ? h->dist.world : 1;
     const int rank = h->dist.partition == KPM_PART_VECTORS ? h->dist.rank : 0;
     p->N = N;
     p->M = N / 2;
+    p->no_fused = no_fused;
     p->r_off = (long long)(R * rank / world);
     p->R_loc = (long long)(R * (rank + 1) / world) - p->r_off;
     if (p->R_loc < 1) return fail(KPM_ERR_INVALID_ARG, "rank %d of %d owns no vectors (R=%lld)", rank, world, (long long)R);
@@ -183,6 +198,12 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
     p->off_R = off;
     if ((flags & KPM_DIRECT) && with_r0) off = align_up(off + p->lane_bytes);
+    if (p->use_tma2 && p->M - 1 >= 2) {
+        p->off_X2 = off; off = align_up(off + p->lane_bytes);
+        p->off_X3 = off; off = align_up(off + p->lane_bytes);
+    } else {
+        p->use_tma2 = false;
+    }
     p->off_part = off; off = align_up(off + (size_t)N * p->gx * p->RP * sizeof(double));
     p->off_Sv = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
     p->off_S = off; off = align_up(off + (size_t)N * sizeof(double));
@@ -316,15 +337,69 @@ kpm_status make_eps_map(const kpm_handle_s* h, const Plan& p, CUtensorMap* m) {
 
 // Maps of one vector buffer in the a_n role (main, x-halo column, y-halo row) and the a_{n-1} role.
 struct BufMaps {
-    CUtensorMap A, Col, Row, P;
+    const void* base = nullptr;
+    CUtensorMap A, Col, Row, P, Col2;  // main, 1-site column, row, (=main), 2-site column (2D)
 };
 
 kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMaps* bm) {
+    bm->base = base;
     KPM_TRY(make_vec_map(h, p, base, p.TX, p.TY, 1, &bm->A));
     KPM_TRY(make_vec_map(h, p, base, 1, p.TY, 1, &bm->Col));
     KPM_TRY(make_vec_map(h, p, base, p.TX, 1, 1, &bm->Row));
+    if (h->ndim == 2) KPM_TRY(make_vec_map(h, p, base, 2, 1, 1, &bm->Col2));
     bm->P = bm->A;
     return KPM_OK;
+}
+
+// eps~ map with a given box width along x (2D: {bx, 1}; 3D: {bx, TY, 1})
+kpm_status make_eps_map_w(const kpm_handle_s* h, const Plan& p, int bx, CUtensorMap* m) {
+    EncodeFn enc = get_encode();
+    if (!enc) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[3] = {(cuuint64_t)h->L[0], (cuuint64_t)h->L[1], (cuuint64_t)h->L[2]};
+    cuuint64_t strides[2] = {(cuuint64_t)h->L[0] * 8, (cuuint64_t)h->L[0] * h->L[1] * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)(h->ndim == 3 ? p.TY : 1), 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, h->ndim, h->d_eps, dims, strides, box, es,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled (eps) failed: %d", (int)r);
+    return KPM_OK;
+}
+
+template <int TL, int TX, bool ONSITE, bool PEIERLS>
+kpm_status launch_tma2_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                         const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
+    auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS>;
+    static size_t configured = 0;
+    if (configured < p.tma2_smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma2_smem));
+        configured = p.tma2_smem;
+    }
+    kern<<<p.tma_grid, kpm::kThreads2, p.tma2_smem, h->stream>>>(A.A, A.Col2, P.P, P.Col, E, E2, g, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
+template <int TL, int TX>
+kpm_status launch_tma2_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                         const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_tma2_t<TL, TX, true, true>(h, p, A, P, E, E2, g, tail);
+        return launch_tma2_t<TL, TX, false, true>(h, p, A, P, E, E2, g, tail);
+    }
+    if (on) return launch_tma2_t<TL, TX, true, false>(h, p, A, P, E, E2, g, tail);
+    return launch_tma2_t<TL, TX, false, false>(h, p, A, P, E, E2, g, tail);
+}
+
+// instantiated tile shapes of the two-step kernel (TX * TL = 1024 lanes per row tile)
+kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                       const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
+    if (p.TL == 32 && p.TX == 32) return launch_tma2_s<32, 32>(h, p, A, P, E, E2, g, tail);
+    if (p.TL == 16 && p.TX == 64) return launch_tma2_s<16, 64>(h, p, A, P, E, E2, g, tail);
+    if (p.TL == 8 && p.TX == 128) return launch_tma2_s<8, 128>(h, p, A, P, E, E2, g, tail);
+    return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX);
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS>
@@ -632,7 +707,12 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
     KPM_CUDA(cudaSetDevice(h->device));
     Plan p;
     KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p));
-    KPM_TRY(ensure_workspace(h, p.total));
+    if (ensure_workspace(h, p.total) != KPM_OK) {
+        if (!p.use_tma2) return KPM_ERR_OOM;
+        // four vector blocks do not fit: fall back to in-place single steps (two blocks)
+        KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p, true));
+        KPM_TRY(ensure_workspace(h, p.total));
+    }
     const bool cplx = is_cplx(h);
     const bool direct = (flags & KPM_DIRECT) != 0;
     double2* P = reinterpret_cast<double2*>(h->ws + p.off_P);
@@ -680,16 +760,27 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
     v.red2 = (!direct && N == 3) ? part + 2 * slot : nullptr;
     KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
 
-    // Recursion steps (Eq 18), a_{n+1} over a_{n-1}; swap roles after each step.
+    // Recursion steps (Eq 18).  Single-step launches write a_{n+1} over a_{n-1} in place;
+    // two-step launches (kpm_tma2.cuh) read (a_n, a_{n-1}) and write (a_{n+1}, a_{n+2}) into
+    // the two spare blocks, after which the pairs swap roles.
     const int nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
-    BufMaps mapsP, mapsC;
-    CUtensorMap mapE;
+    double2* X2 = reinterpret_cast<double2*>(h->ws + p.off_X2);
+    double2* X3 = reinterpret_cast<double2*>(h->ws + p.off_X3);
+    BufMaps maps[4];
+    int nmaps = 0;
+    CUtensorMap mapE, mapE2;
     memset(&mapE, 0, sizeof mapE);
+    memset(&mapE2, 0, sizeof mapE2);
     kpm::TmaGeom tg{};
+    kpm::Tma2Geom tg2{};
     if (p.use_tma && nsteps > 0) {
-        KPM_TRY(make_buf_maps(h, p, P, &mapsP));
-        KPM_TRY(make_buf_maps(h, p, C, &mapsC));
-        if (h->d_eps) KPM_TRY(make_eps_map(h, p, &mapE));
+        double2* bufs[4] = {P, C, X2, X3};
+        nmaps = p.use_tma2 ? 4 : 2;
+        for (int i = 0; i < nmaps; ++i) KPM_TRY(make_buf_maps(h, p, bufs[i], &maps[i]));
+        if (h->d_eps) {
+            KPM_TRY(make_eps_map(h, p, &mapE));
+            if (p.use_tma2) KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
+        }
         tg.L0 = (int)h->L[0];
         tg.L1 = (int)h->L[1];
         tg.L2 = (int)h->L[2];
@@ -707,17 +798,63 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
         tg.t = h->t_scaled;
         tg.shift = -h->b / h->a;
         tg.phase = h->d_phase;
+        tg2.L0 = tg.L0;
+        tg2.L1 = tg.L1;
+        tg2.TX = p.TX;
+        tg2.TL = p.TL;
+        tg2.RG = p.RG;
+        tg2.G_L = tg.G_L;
+        tg2.PX = tg.PX;
+        tg2.W = (long long)tg.G_L * tg.PX * tg.L1;
+        tg2.RP = p.RP;
+        tg2.t = tg.t;
+        tg2.shift = tg.shift;
+        tg2.phase = tg.phase;
     }
+    auto maps_of = [&](const void* b) -> const BufMaps& {
+        for (int i = 0; i < nmaps; ++i)
+            if (maps[i].base == b) return maps[i];
+        return maps[0];
+    };
     KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
-    double2* cur = C;   // a_n
-    double2* prev = P;  // a_{n-1}
-    for (int n = 1; n <= nsteps; ++n) {
+    double2* cur = C;    // a_n
+    double2* prev = P;   // a_{n-1}
+    double2* spare0 = X2;
+    double2* spare1 = X3;
+    h->steps_bytes = 0.0;
+    const double s_el = cplx ? 16.0 : 8.0;
+    const double vbytes = (double)h->D * (double)p.R_loc * s_el;
+    const double ebytes = h->d_eps ? 8.0 * (double)h->D : 0.0;
+    const double mbytes = h->kind == KIND_ELL ? (double)h->K * (double)h->D * (4.0 + s_el) : 0.0;
+    int n = 1;
+    while (n <= nsteps) {
+        const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1));
+        if (pair) {
+            // steps n and n+1: slots 2n .. 2n+3 (+ odd-N tail 2n+4)
+            const bool tail = (N & 1) && n + 1 == nsteps;
+            for (int k = 0; k < 4; ++k) tg2.red[k] = part + (size_t)(2 * n + k) * slot;
+            tg2.red[4] = tail ? part + (size_t)(2 * n + 4) * slot : nullptr;
+            tg2.outB = spare0;
+            tg2.outC = spare1;
+            KPM_TRY(launch_tma2(h, p, maps_of(cur), maps_of(prev), mapE, mapE2, tg2, tail));
+            double2* oc = cur;
+            double2* op = prev;
+            cur = spare1;
+            prev = spare0;
+            spare0 = oc;
+            spare1 = op;
+            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->step_launches++;
+            n += 2;
+            continue;
+        }
         v.C = cur;
         v.P = prev;
         if (direct) {
             v.red0 = part + (size_t)(n + 1) * slot;  // <r|a_{n+1}> -> mu_{n+1}
             v.red1 = v.red2 = nullptr;
             KPM_TRY(launch(h, p, r0 ? kpm::DIRECT_BUF : kpm::DIRECT_GEN, v, 0));
+            h->steps_bytes += 3.0 * vbytes + ebytes + mbytes + (r0 ? vbytes : 0.0);
         } else {
             v.red0 = part + (size_t)(2 * n) * slot;      // <a_n|a_n>     -> mu_{2n}
             v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
@@ -728,13 +865,15 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
                 tg.red1 = v.red1;
                 tg.red2 = v.red2;
                 tg.out = prev;
-                KPM_TRY(launch_tma(h, p, cur == C ? mapsC : mapsP, cur == C ? mapsP : mapsC, mapE, tg, tail));
+                KPM_TRY(launch_tma(h, p, maps_of(cur), maps_of(prev), mapE, tg, tail));
             } else {
                 KPM_TRY(launch(h, p, kpm::STEP, v, tail));
             }
+            h->steps_bytes += 3.0 * vbytes + ebytes + mbytes;
         }
         h->step_launches++;
         std::swap(cur, prev);
+        ++n;
     }
     KPM_CUDA(cudaEventRecord(h->ev_end, h->stream));
 
@@ -864,23 +1003,13 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[4] = p.gx;
     info[5] = (int64_t)p.tma_smem;
     info[6] = p.RG;
-    info[7] = p.tma_rr;
+    info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0);
     return KPM_OK;
 }
 
-kpm_status kpm_step_bytes(kpm_handle h, int64_t R, double* bytes) {
+kpm_status kpm_step_bytes(kpm_handle h, double* bytes) {
     if (!h || !bytes) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
-    Plan p;
-    KPM_TRY(make_plan(h, 2, R, 0u, false, &p));
-    const double s = is_cplx(h) ? 16.0 : 8.0;
-    // read a_n, read a_{n-1}, write a_{n+1} (3 V) + the matrix / on-site data per step.
-    double b = 3.0 * (double)h->D * (double)p.R_loc * s;
-    if (h->kind == KIND_STENCIL) {
-        if (h->d_eps) b += 8.0 * (double)h->D;
-    } else {
-        b += (double)h->K * (double)h->D * (4.0 + s);
-    }
-    *bytes = b;
+    *bytes = h->steps_bytes;
     return KPM_OK;
 }
 

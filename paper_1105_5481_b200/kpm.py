@@ -60,7 +60,7 @@ _SIG = {
     "kpm_vector_range": [_i64, _i32, _i32, _P, _P],
     "kpm_dos": [_P, _i32, _i32, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_last_timing": [_P, _P, _P, _P],
-    "kpm_step_bytes": [_P, _i64, _P],
+    "kpm_step_bytes": [_P, _P],
     "kpm_plan_info": [_P, _i32, _i64, _u32, _P],
 }
 for _name, _args in _SIG.items():
@@ -217,12 +217,16 @@ class Handle:
     def plan_info(self, N, R, flags=0):
         info = np.zeros(8, dtype=np.int64)
         _check(_lib.kpm_plan_info(self._h, int(N), int(R), int(flags), _ptr(info)))
-        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "round_robin"]
-        return {k: int(v) for k, v in zip(keys, info)}
+        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "_"]
+        d = {k: int(v) for k, v in zip(keys, info) if k != "_"}
+        d["round_robin"] = int(info[7] & 1)
+        d["two_step"] = int((info[7] >> 1) & 1)
+        return d
 
-    def step_bytes(self, R):
+    def step_bytes(self):
+        """Algorithmic HBM bytes of the recursion-step launches of the last call."""
         b = ctypes.c_double()
-        _check(_lib.kpm_step_bytes(self._h, int(R), ctypes.byref(b)))
+        _check(_lib.kpm_step_bytes(self._h, ctypes.byref(b)))
         return b.value
 
 

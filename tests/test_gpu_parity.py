@@ -100,12 +100,32 @@ def test_tma_march_matches_oracle(kpm, case):
     info = h.plan_info(N, R)
     assert info["tma"] == 1, info
     assert info["round_robin"] == (case == "3d_round_robin"), info
+    assert info["two_step"] == (lat["ndim"] == 2 and info["TX"] * info["TL"] == 1024), info
     mu = h.moments(N, R, 21)
     assert normwise(mu, ref) < TOL
     pv = h.moments_ex(N, R, 21, flags=kpm.KPM_PER_VECTOR)
     assert normwise(pv, ref_pv) < TOL
     assert np.array_equal(h.moments(N, R, 21), mu), "not deterministic"
     assert np.array_equal(h.moments_ex(N, R, 21, r0=r), mu)
+
+
+@pytest.mark.parametrize("case", [c for c in sorted(TMA_CASES) if c.startswith("2d")])
+@pytest.mark.parametrize("N", [5, 6, 7, 8, 9])
+def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
+    """2D: the two-step kernel (temporal blocking) and the single-step kernel give the oracle's
+    moments for every parity of the step count and of N (odd-N tail inside a pair)."""
+    lat, _, R = TMA_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(5, R, lat["D"]), N)
+    h = make(kpm, lat, a, b)
+    info = h.plan_info(N, R)
+    assert info["two_step"] == (N // 2 - 1 >= 2 and info["TX"] * info["TL"] == 1024)
+    mu2 = h.moments(N, R, 5)
+    monkeypatch.setenv("KPM_NO_TMA2", "1")
+    assert h.plan_info(N, R)["two_step"] == 0
+    mu1 = h.moments(N, R, 5)
+    assert normwise(mu2, ref) < TOL and normwise(mu1, ref) < TOL
 
 
 @pytest.mark.parametrize("case", ["2d", "3d_anderson", "peierls"])
