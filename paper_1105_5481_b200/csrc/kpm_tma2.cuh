@@ -43,7 +43,7 @@ struct Tma2Geom {
     double2* outC;       // a_{n+2}
 };
 
-constexpr int kThreads2 = 512;  // 16 warps
+constexpr int kThreads2 = 256;  // 8 warps
 constexpr int kSA2 = 5;         // a_n ring
 constexpr int kSP2 = 3;         // a_{n-1} ring
 constexpr int kSB2 = 3;         // a_{n+1} ring (computed)
@@ -254,6 +254,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
         int ps = ip % kSP2;
         int rB = (m0 - 1 + g.L1) % g.L1;              // a_{n+1} row r
         int rC = (m0 - 2 + g.L1) % g.L1;              // a_{n+2} row r-1
+        // values this thread needs again in later rows, kept in registers (per pass p):
+        // a_n at rows r-1, r, r+1; a_{n+1} at rows r-2, r-1; eps~ at row r-1
+        double2 am[NPI], ac[NPI], ap[NPI], bm[NPI], bc[NPI];
+        double em[NPI];
         for (int q = 0; q < H + 2; ++q) {
             const int i0 = ia_seg + q;
             const int s1 = s0 + 1 == kSA2 ? 0 : s0 + 1;
@@ -270,9 +274,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const unsigned char* Pq = ringP + ps * SL.p_bytes;   // a_{n-1} row r
             unsigned char* Bq = ringB + sB * SL.b_bytes;         // a_{n+1} row r (written now)
             const int sBc = sB == 0 ? kSB2 - 1 : sB - 1;
-            const int sBm = sBc == 0 ? kSB2 - 1 : sBc - 1;
             const unsigned char* Bc = ringB + sBc * SL.b_bytes;  // a_{n+1} row r-1
-            const unsigned char* Bm = ringB + sBm * SL.b_bytes;  // a_{n+1} row r-2
             const bool own_b = (q >= 1 && q <= H);
             const bool do_c = (q >= 2);
             double2* outB = g.outB + rB * growstep + g0;
@@ -283,11 +285,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 const int oa = (lx + 2) * SITE + lo;  // a_n slot index
                 const int ob = (lx + 1) * SITE + lo;  // a_{n+1} / a_{n-1} slot index
                 const double2 ph = PEIERLS ? sphase[lx + 1] : make_double2(0.0, 0.0);
+                if (q == 0) {
+                    am[p] = ld(A0 + oa);
+                    ac[p] = ld(A1 + oa);
+                    if (ONSITE) em[p] = reinterpret_cast<const double*>(A0 + SL.eps_m)[lx];
+                }
+                ap[p] = ld(A2 + oa);
                 // first step: a_{n+1}(row r, lx)
-                const double2 x = ld(A1 + oa);
+                const double2 x = ac[p];
                 const double e1 = ONSITE ? reinterpret_cast<const double*>(A1 + SL.eps_m)[lx] : g.shift;
-                const double2 b = step_val(x, ld(A1 + oa - SITE), ld(A1 + oa + SITE), ld(A0 + oa), ld(A2 + oa), e1, ph,
-                                           ld(Pq + ob));
+                const double2 b = step_val(x, ld(A1 + oa - SITE), ld(A1 + oa + SITE), am[p], ap[p], e1, ph, ld(Pq + ob));
                 *reinterpret_cast<double2*>(Bq + ob) = b;
                 if (own_b) {
                     __stcs(outB + p * gstep, b);
@@ -295,16 +302,21 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     dot_acc<PEIERLS>(acc[1], x, b);
                     dot_acc<PEIERLS>(acc[2], b, b);
                 }
-                // second step: a_{n+2}(row r-1, lx); its a_{n+1}(row r) neighbour is b
+                // second step: a_{n+2}(row r-1, lx); centre a_{n+1}(r-1) and y-neighbours
+                // a_{n+1}(r-2), a_{n+1}(r) are this thread's own values
                 if (do_c) {
-                    const double2 bc = ld(Bc + ob);
-                    const double e0 = ONSITE ? reinterpret_cast<const double*>(A0 + SL.eps_m)[lx] : g.shift;
-                    const double2 c = step_val(bc, ld(Bc + ob - SITE), ld(Bc + ob + SITE), ld(Bm + ob), b, e0, ph,
-                                               ld(A0 + oa));
+                    const double e0 = ONSITE ? em[p] : g.shift;
+                    const double2 c = step_val(bc[p], ld(Bc + ob - SITE), ld(Bc + ob + SITE), bm[p], b, e0, ph, am[p]);
                     __stcs(outC + p * gstep, c);
-                    dot_acc<PEIERLS>(acc[3], bc, c);
+                    dot_acc<PEIERLS>(acc[3], bc[p], c);
                     if (tail) dot_acc<PEIERLS>(acc[4], c, c);
                 }
+                // roll the per-thread values one row down
+                am[p] = ac[p];
+                ac[p] = ap[p];
+                bm[p] = bc[p];
+                bc[p] = b;
+                if (ONSITE) em[p] = e1;
             }
             if (hs >= 0) {  // halo a_{n+1} site (recomputed here, owned by the neighbouring pencil)
                 const int oa = (hlx + 2) * SITE + lo;
