@@ -94,13 +94,32 @@ typedef struct {
 } kpm_stencil_desc;
 
 /* Partition of the work across ranks (one process per GPU).  NULL = one GPU. */
-enum { KPM_PART_NONE = 0, KPM_PART_VECTORS = 1 };
+enum { KPM_PART_NONE = 0, KPM_PART_VECTORS = 1, KPM_PART_ROWS = 2 };
+/* How row-partitioned ranks exchange halo planes and combine moment sums. */
+enum {
+    KPM_COMM_SELF = 0,  /* world == 1 (the slab is the whole lattice; halos are local copies) */
+    KPM_COMM_NCCL = 1,  /* one process per GPU: NCCL send/recv of halo planes, all-reduce of sums */
+    KPM_COMM_LOCAL = 2  /* all ranks' handles in this process, driven by kpm_moments_group */
+};
 typedef struct {
     int32_t partition; /* KPM_PART_VECTORS: rank owns global vectors
-                          [R*rank/world, R*(rank+1)/world) (Eq 16 is a sum over independent r) */
+                          [R*rank/world, R*(rank+1)/world) (Eq 16 is a sum over independent r).
+                          KPM_PART_ROWS (stencils): rank owns the slab of the slowest lattice
+                          dimension [Lm*rank/world, Lm*(rank+1)/world) (z in 3D, y in 2D, x in
+                          1D) plus one ghost plane on each side, exchanged after every step
+                          (periodic: rank 0 and rank world-1 are neighbours). */
     int32_t rank;
     int32_t world;
+    int32_t comm;            /* KPM_COMM_* (row partition only) */
+    const void* nccl_id;     /* KPM_COMM_NCCL: the 128-byte ncclUniqueId from kpm_nccl_unique_id on
+                                rank 0, the same on every rank */
 } kpm_dist;
+
+/* 128-byte NCCL unique id for KPM_COMM_NCCL (call on rank 0, broadcast to the others). */
+kpm_status kpm_nccl_unique_id(void* out128);
+
+/* Slab of the row partition: planes [begin, begin + count) of an extent Lm.  Host only. */
+kpm_status kpm_slab_range(int64_t Lm, int32_t rank, int32_t world, int64_t* begin, int64_t* count);
 
 /* ---- creation (host -> device upload of H~; "the CPU copies the data to
  *      the VRAM") ------------------------------------------------------------------- */
@@ -151,6 +170,11 @@ kpm_status kpm_moments(kpm_handle h, int32_t N, int64_t R, uint64_t seed, double
  *      (host, or device with KPM_DEVICE_OUT). */
 kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, const void* r0,
                           uint32_t flags, void* out);
+
+/* Row partition with KPM_COMM_LOCAL: run kpm_moments for the `n` slab handles hs[0..n-1]
+ * (rank i = hs[i], world n, any devices) in lock step, exchanging halo planes between
+ * them after every step; mu[N] (host) is the moment estimate of the whole lattice. */
+kpm_status kpm_moments_group(kpm_handle* hs, int32_t n, int32_t N, int64_t R, uint64_t seed, double* mu);
 
 /* Raw sums S[N] (summed over all ranks) -> mu[N]: mu_0 = S_0/(D R), mu_1 = S_1/(D R),
  * mu_{2n} = 2 S_{2n}/(D R) - mu_0, mu_{2n+1} = 2 S_{2n+1}/(D R) - mu_1; with KPM_DIRECT

@@ -18,13 +18,26 @@ def sources():
                   glob.glob(os.path.join(ROOT, "include", "*.h")))
 
 
+def nccl_dir() -> str:
+    """NCCL 2.28 shipped with torch (nvidia-nccl wheel): headers + libnccl.so.2."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    for base in (spec.submodule_search_locations if spec else []):
+        d = os.path.join(base, "nccl")
+        if os.path.exists(os.path.join(d, "include", "nccl.h")):
+            return d
+    raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     newest = max(os.path.getmtime(p) for p in sources())
     if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
         return LIB
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-o", LIB + ".tmp",
-           os.path.join(HERE, "csrc", "kpm_capi.cu"), "-lcudart"]
+    nd = nccl_dir()
+    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+           "-o", LIB + ".tmp", os.path.join(HERE, "csrc", "kpm_capi.cu"), "-lcudart",
+           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
     if verbose:
         print(" ".join(cmd))
     subprocess.check_call(cmd)

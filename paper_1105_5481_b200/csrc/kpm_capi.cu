@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <math_constants.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cmath>
@@ -78,7 +79,14 @@ struct kpm_handle_s {
     int32_t* d_col = nullptr;
     double* d_val = nullptr;
     // partition
-    kpm_dist dist{KPM_PART_NONE, 0, 1};
+    kpm_dist dist{KPM_PART_NONE, 0, 1, KPM_COMM_SELF, nullptr};
+    // row partition (KPM_PART_ROWS): slab [z0, z0 + nloc) of the slowest dimension `slow`;
+    // vector blocks hold nloc + 2 planes (ghost, local..., ghost); D counts local sites
+    bool rows = false;
+    int slow = 0;
+    int64_t z0 = 0, nloc = 0, Lm_global = 0, plane = 1;
+    int64_t D_total = 0;  // global number of sites (normalisation, RNG counters)
+    ncclComm_t nccl = nullptr;
     // workspace
     char* ws = nullptr;
     size_t ws_bytes = 0;
@@ -107,6 +115,7 @@ struct Plan {
     bool use_tma2 = false, no_fused = false;
     size_t tma2_smem = 0;
     size_t lane_bytes = 0;
+    size_t ghost_lanes = 0;  // lanes of one ghost plane (row partition), else 0
     size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
            total = 0;
 };
@@ -172,7 +181,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
                      bool no_fused = false) {
     if (N < 1) return fail(KPM_ERR_INVALID_ARG, "N must be >= 1 (got %d)", N);
     if (R < 1) return fail(KPM_ERR_INVALID_ARG, "R must be >= 1 (got %lld)", (long long)R);
-    const int world = h->dist.partition == KPM_PART_VECTORS ? h->dist.world : 1;
+    const int world = h->dist.partition == KPM_PART_VECTORS ? h->dist.world : 1;  // vector shards
     const int rank = h->dist.partition == KPM_PART_VECTORS ? h->dist.rank : 0;
     p->N = N;
     p->M = N / 2;
@@ -192,7 +201,9 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     plan_tma(h, flags, p);
     if (p->use_tma) p->gx = p->tma_grid;
     p->nslots = N;
-    p->lane_bytes = (size_t)h->D * p->RG * sizeof(double2);
+    if (h->rows) p->use_tma2 = false;  // the two-step kernel needs two-deep halos; not with slabs
+    p->ghost_lanes = h->rows ? (size_t)h->plane * p->RG : 0;
+    p->lane_bytes = ((size_t)h->D * p->RG + 2 * p->ghost_lanes) * sizeof(double2);
     size_t off = 0;
     p->off_P = off; off = align_up(off + p->lane_bytes);
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
@@ -264,6 +275,7 @@ kpm::StencilGeom stencil_geom(const kpm_handle_s* h) {
     g.shift = -h->b / h->a;
     g.eps = h->d_eps;
     g.phase = h->d_phase;
+    g.ghost = h->rows ? 1 : 0;
     return g;
 }
 
@@ -311,6 +323,7 @@ kpm_status make_vec_map(const kpm_handle_s* h, const Plan& p, void* base, int bx
     if (!enc) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int rank = h->ndim + 1;
     cuuint64_t dims[4] = {(cuuint64_t)2 * p.RG, (cuuint64_t)h->L[0], (cuuint64_t)h->L[1], (cuuint64_t)h->L[2]};
+    if (h->rows) dims[1 + h->slow] += 2;  // ghost planes
     cuuint64_t strides[3] = {(cuuint64_t)p.RG * 16, (cuuint64_t)p.RG * 16 * h->L[0], (cuuint64_t)p.RG * 16 * h->L[0] * h->L[1]};
     cuuint32_t box[4] = {(cuuint32_t)(2 * p.TL), (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     if (h->ndim == 2) box[2] = 1;
@@ -436,10 +449,18 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
     if (!out) return fail(KPM_ERR_INVALID_ARG, "out handle pointer is NULL");
     *out = nullptr;
     if (dist) {
-        if (dist->partition != KPM_PART_NONE && dist->partition != KPM_PART_VECTORS)
+        if (dist->partition != KPM_PART_NONE && dist->partition != KPM_PART_VECTORS && dist->partition != KPM_PART_ROWS)
             return fail(KPM_ERR_UNSUPPORTED, "partition %d not supported", dist->partition);
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
             return fail(KPM_ERR_INVALID_ARG, "bad rank %d / world %d", dist->rank, dist->world);
+        if (dist->partition == KPM_PART_ROWS) {
+            if (dist->comm != KPM_COMM_SELF && dist->comm != KPM_COMM_NCCL && dist->comm != KPM_COMM_LOCAL)
+                return fail(KPM_ERR_INVALID_ARG, "bad comm %d", dist->comm);
+            if (dist->comm == KPM_COMM_SELF && dist->world != 1)
+                return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_SELF needs world == 1");
+            if (dist->comm == KPM_COMM_NCCL && !dist->nccl_id)
+                return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_NCCL needs nccl_id");
+        }
     }
     int ndev = 0;
     KPM_CUDA(cudaGetDeviceCount(&ndev));
@@ -448,6 +469,7 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
     auto* h = new kpm_handle_s();
     h->device = device;
     if (dist) h->dist = *dist;
+    h->dist.nccl_id = nullptr;  // not kept
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -491,6 +513,341 @@ kpm_status check_stencil(const kpm_stencil_desc* d) {
     return KPM_OK;
 }
 
+
+// One kpm_moments_ex call as a sequence of phases, so that several slab handles of a
+// row partition (KPM_COMM_LOCAL) can be driven in lock step: begin() (plan, workspace,
+// start block, first step), launch_next() (one recursion launch: one step, or two with
+// the temporal-blocking kernel), fresh() (the block just produced, whose boundary planes
+// go to the neighbours), collect() (fixed-order finish of the partial sums), output().
+struct Run {
+    kpm_handle_s* h = nullptr;
+    Plan p;
+    int32_t N = 0;
+    int64_t R = 0;
+    uint32_t flags = 0;
+    const void* r0 = nullptr;
+    bool cplx = false, direct = false;
+    double2 *P = nullptr, *C = nullptr, *Rb = nullptr, *X2 = nullptr, *X3 = nullptr;  // interiors
+    double *part = nullptr, *Sv = nullptr, *S = nullptr, *dout = nullptr;
+    size_t slot = 0;
+    kpm::VecArgs v{};
+    BufMaps maps[4];
+    int nmaps = 0;
+    CUtensorMap mapE, mapE2;
+    kpm::TmaGeom tg{};
+    kpm::Tma2Geom tg2{};
+    double2 *cur = nullptr, *prev = nullptr, *spare0 = nullptr, *spare1 = nullptr;
+    int n = 1, nsteps = 0;
+    double vbytes = 0, ebytes = 0, mbytes = 0;
+
+    double2* base_of(double2* interior) const { return interior - p.ghost_lanes; }
+    const BufMaps& maps_of(const void* b) const {
+        for (int i = 0; i < nmaps; ++i)
+            if (maps[i].base == b) return maps[i];
+        return maps[0];
+    }
+
+    kpm_status begin(kpm_handle_s* h_, int32_t N_, int64_t R_, uint64_t seed, const void* r0_, uint32_t flags_) {
+        h = h_;
+        N = N_;
+        R = R_;
+        flags = flags_;
+        r0 = r0_;
+        if ((flags & KPM_PER_VECTOR) && (flags & KPM_RAW_SUMS))
+            return fail(KPM_ERR_INVALID_ARG, "KPM_PER_VECTOR and KPM_RAW_SUMS are exclusive");
+        KPM_CUDA(cudaSetDevice(h->device));
+        KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p));
+        if (ensure_workspace(h, p.total) != KPM_OK) {
+            if (!p.use_tma2) return KPM_ERR_OOM;
+            // four vector blocks do not fit: fall back to in-place single steps (two blocks)
+            KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p, true));
+            KPM_TRY(ensure_workspace(h, p.total));
+        }
+        cplx = is_cplx(h);
+        direct = (flags & KPM_DIRECT) != 0;
+        P = reinterpret_cast<double2*>(h->ws + p.off_P) + p.ghost_lanes;
+        C = reinterpret_cast<double2*>(h->ws + p.off_C) + p.ghost_lanes;
+        Rb = reinterpret_cast<double2*>(h->ws + p.off_R) + p.ghost_lanes;
+        X2 = reinterpret_cast<double2*>(h->ws + p.off_X2) + p.ghost_lanes;
+        X3 = reinterpret_cast<double2*>(h->ws + p.off_X3) + p.ghost_lanes;
+        part = reinterpret_cast<double*>(h->ws + p.off_part);
+        Sv = reinterpret_cast<double*>(h->ws + p.off_Sv);
+        S = reinterpret_cast<double*>(h->ws + p.off_S);
+        dout = reinterpret_cast<double*>(h->ws + p.off_out);
+        slot = (size_t)p.gx * p.RP;  // doubles per moment slot of partials
+        h->total_launches = 0;
+        h->step_launches = 0;
+        h->steps_bytes = 0.0;
+
+        v.P = P;
+        v.C = C;
+        v.Rbuf = Rb;
+        v.D = (int)h->D;
+        v.RG = p.RG;
+        v.RP = p.RP;
+        v.R_loc = p.R_loc;
+        v.key = kpm::vector_key(seed);
+        v.r_off = p.r_off;
+        v.D_total = h->D_total;
+        v.i_off = h->rows ? h->z0 * h->plane : 0;
+        v.ghost = h->rows ? 1 : 0;
+
+        // a_0: generated in the first-step kernel, or the caller's block staged through C.
+        int first_mode = kpm::FIRST_GEN;
+        if (r0) {
+            const size_t rbytes = (size_t)p.R_loc * h->D * sizeof(double);
+            double* stage = reinterpret_cast<double*>(base_of(C));
+            KPM_CUDA(cudaMemcpyAsync(stage, r0, rbytes,
+                                     (flags & KPM_DEVICE_IN) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
+            const long long ne = h->D * (long long)p.RG;
+            const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
+            if (cplx) kpm::load_r0_kernel<true><<<blocks, 256, 0, h->stream>>>(stage, P, (int)h->D, p.RG, p.R_loc);
+            else kpm::load_r0_kernel<false><<<blocks, 256, 0, h->stream>>>(stage, P, (int)h->D, p.RG, p.R_loc);
+            KPM_CUDA(cudaGetLastError());
+            h->total_launches++;
+            if (direct) KPM_CUDA(cudaMemcpyAsync(Rb, P, (size_t)h->D * p.RG * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
+            first_mode = kpm::FIRST_BUF;
+        }
+        if (first_mode == kpm::FIRST_BUF && h->rows) KPM_TRY(need_exchange(P));
+        // First step: a_0, a_1 = H~ a_0; S_0 = <a_0|a_0>, S_1 = <a_0|a_1> (Eq 17, 19).
+        v.red0 = part;
+        v.red1 = N > 1 ? part + slot : nullptr;
+        v.red2 = (!direct && N == 3) ? part + 2 * slot : nullptr;
+        KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
+
+        // Recursion launches (Eq 18).  Single-step launches write a_{n+1} over a_{n-1} in place;
+        // two-step launches (kpm_tma2.cuh) read (a_n, a_{n-1}) and write (a_{n+1}, a_{n+2}) into
+        // the two spare blocks, after which the pairs swap roles.
+        nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
+        memset(&mapE, 0, sizeof mapE);
+        memset(&mapE2, 0, sizeof mapE2);
+        if (p.use_tma && nsteps > 0) {
+            double2* bufs[4] = {P, C, X2, X3};
+            nmaps = p.use_tma2 ? 4 : 2;
+            for (int i = 0; i < nmaps; ++i) KPM_TRY(make_buf_maps(h, p, base_of(bufs[i]), &maps[i]));
+            if (h->d_eps) {
+                KPM_TRY(make_eps_map(h, p, &mapE));
+                if (p.use_tma2) KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
+            }
+            tg.L0 = (int)h->L[0];
+            tg.L1 = (int)h->L[1];
+            tg.L2 = (int)h->L[2];
+            tg.TX = p.TX;
+            tg.TY = p.TY;
+            tg.TL = p.TL;
+            tg.RG = p.RG;
+            tg.G_L = p.RG / p.TL;
+            tg.PX = (int)(h->L[0] / p.TX);
+            tg.PY = h->ndim == 3 ? (int)(h->L[1] / p.TY) : 1;
+            tg.Lm = (int)(h->ndim == 2 ? h->L[1] : h->L[2]);
+            tg.W = (long long)tg.G_L * tg.PX * tg.PY * tg.Lm;
+            tg.rr = p.tma_rr;
+            tg.ghost = h->rows ? 1 : 0;
+            tg.RP = p.RP;
+            tg.t = h->t_scaled;
+            tg.shift = -h->b / h->a;
+            tg.phase = h->d_phase;
+            tg2.L0 = tg.L0;
+            tg2.L1 = tg.L1;
+            tg2.TX = p.TX;
+            tg2.TL = p.TL;
+            tg2.RG = p.RG;
+            tg2.G_L = tg.G_L;
+            tg2.PX = tg.PX;
+            tg2.W = (long long)tg.G_L * tg.PX * tg.L1;
+            tg2.RP = p.RP;
+            tg2.t = tg.t;
+            tg2.shift = tg.shift;
+            tg2.phase = tg.phase;
+        }
+        cur = C;
+        prev = P;
+        spare0 = X2;
+        spare1 = X3;
+        n = 1;
+        const double s_el = cplx ? 16.0 : 8.0;
+        vbytes = (double)h->D * (double)p.R_loc * s_el;
+        ebytes = h->d_eps ? 8.0 * (double)h->D : 0.0;
+        mbytes = h->kind == KIND_ELL ? (double)h->K * (double)h->D * (4.0 + s_el) : 0.0;
+        KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
+        return KPM_OK;
+    }
+
+    // ghost planes of `X` must be refreshed before the next launch (recorded; done by the caller)
+    double2* pending = nullptr;
+    kpm_status need_exchange(double2* X) {
+        pending = X;
+        return exchange_hook ? exchange_hook(this) : KPM_OK;
+    }
+    kpm_status (*exchange_hook)(Run*) = nullptr;
+
+    bool more() const { return n <= nsteps; }
+    double2* fresh() const { return cur; }
+
+    kpm_status launch_next() {
+        const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1));
+        if (pair) {
+            // steps n and n+1: slots 2n .. 2n+3 (+ odd-N tail 2n+4)
+            const bool tail = (N & 1) && n + 1 == nsteps;
+            for (int k = 0; k < 4; ++k) tg2.red[k] = part + (size_t)(2 * n + k) * slot;
+            tg2.red[4] = tail ? part + (size_t)(2 * n + 4) * slot : nullptr;
+            tg2.outB = spare0;
+            tg2.outC = spare1;
+            KPM_TRY(launch_tma2(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapE, mapE2, tg2, tail));
+            double2* oc = cur;
+            double2* op = prev;
+            cur = spare1;
+            prev = spare0;
+            spare0 = oc;
+            spare1 = op;
+            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->step_launches++;
+            n += 2;
+            return KPM_OK;
+        }
+        v.C = cur;
+        v.P = prev;
+        if (direct) {
+            v.red0 = part + (size_t)(n + 1) * slot;  // <r|a_{n+1}> -> mu_{n+1}
+            v.red1 = v.red2 = nullptr;
+            KPM_TRY(launch(h, p, r0 ? kpm::DIRECT_BUF : kpm::DIRECT_GEN, v, 0));
+            h->steps_bytes += 3.0 * vbytes + ebytes + mbytes + (r0 ? vbytes : 0.0);
+        } else {
+            v.red0 = part + (size_t)(2 * n) * slot;      // <a_n|a_n>     -> mu_{2n}
+            v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
+            const bool tail = (N & 1) && n == nsteps;    // odd N: <a_M|a_M> -> mu_{N-1}
+            v.red2 = tail ? part + (size_t)(2 * n + 2) * slot : nullptr;
+            if (p.use_tma) {
+                tg.red0 = v.red0;
+                tg.red1 = v.red1;
+                tg.red2 = v.red2;
+                tg.out = base_of(prev);
+                KPM_TRY(launch_tma(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapE, tg, tail));
+            } else {
+                KPM_TRY(launch(h, p, kpm::STEP, v, tail));
+            }
+            h->steps_bytes += 3.0 * vbytes + ebytes + mbytes;
+        }
+        h->step_launches++;
+        std::swap(cur, prev);
+        ++n;
+        return KPM_OK;
+    }
+
+    // Fixed-order finish of the CTA partials: Sv[m][v] and S[m] on the device.
+    kpm_status collect() {
+        KPM_CUDA(cudaEventRecord(h->ev_end, h->stream));
+        kpm::finish_kernel<<<N, 256, 0, h->stream>>>(part, p.gx, p.RP, p.R_loc, Sv, S);
+        KPM_CUDA(cudaGetLastError());
+        h->total_launches++;
+        return KPM_OK;
+    }
+
+    kpm_status output(void* out) {
+        const bool dev_out = (flags & KPM_DEVICE_OUT) != 0;
+        size_t out_bytes = 0;
+        const double* src = nullptr;
+        if (flags & KPM_RAW_SUMS) {
+            src = S;
+            out_bytes = (size_t)N * sizeof(double);
+        } else if (flags & KPM_PER_VECTOR) {
+            const long long ne = (long long)N * p.R_loc;
+            kpm::assemble_pervec_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, h->stream>>>(
+                Sv, N, p.R_loc, 1.0 / (double)h->D_total, direct, dout);
+            KPM_CUDA(cudaGetLastError());
+            h->total_launches++;
+            src = dout;
+            out_bytes = (size_t)ne * sizeof(double);
+        } else {
+            if (h->dist.partition == KPM_PART_VECTORS && h->dist.world > 1)
+                return fail(KPM_ERR_INVALID_ARG, "multi-rank: use KPM_RAW_SUMS, all-reduce, then kpm_assemble");
+            kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, 1.0 / ((double)h->D_total * (double)p.R_loc),
+                                                                         direct, dout);
+            KPM_CUDA(cudaGetLastError());
+            h->total_launches++;
+            src = dout;
+            out_bytes = (size_t)N * sizeof(double);
+        }
+        KPM_CUDA(cudaMemcpyAsync(out, src, out_bytes, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
+        if (dev_out) return KPM_OK;
+        KPM_CUDA(cudaStreamSynchronize(h->stream));
+        if (!(flags & KPM_RAW_SUMS)) {
+            const long long rows = (flags & KPM_PER_VECTOR) ? p.R_loc : 1;
+            KPM_TRY(spectrum_guard(static_cast<const double*>(out), rows, N));
+        }
+        return KPM_OK;
+    }
+
+    static kpm_status spectrum_guard(const double* o, long long rows, int N) {
+        // |T_n| <= 1 on [-1, 1] (Eq 3) => |mu_n| <= mu_0 when [b-a, b+a] encloses spec(H).
+        for (long long r = 0; r < rows; ++r) {
+            const double* m = o + r * N;
+            for (int k = 0; k < N; ++k)
+                if (!std::isfinite(m[k]) || std::fabs(m[k]) > std::fabs(m[0]) * (1.0 + 1e-8) + 1e-300)
+                    return fail(KPM_ERR_SPECTRUM, "|mu_%d| = %g exceeds mu_0 = %g: [b-a, b+a] does not enclose the spectrum",
+                                k, m[k], m[0]);
+        }
+        return KPM_OK;
+    }
+
+    size_t plane_bytes() const { return p.ghost_lanes * sizeof(double2); }
+    // interior plane 0 and nloc-1, ghost planes below and above, of block X
+    double2* first_plane(double2* X) const { return X; }
+    double2* last_plane(double2* X) const { return X + (h->nloc - 1) * p.ghost_lanes; }
+    double2* ghost_lo(double2* X) const { return X - p.ghost_lanes; }
+    double2* ghost_hi(double2* X) const { return X + h->nloc * p.ghost_lanes; }
+};
+
+// Halo exchange of a single row-partitioned handle: world 1 (periodic wrap inside the
+// slab) or NCCL send/recv with the two neighbouring ranks, on the handle's stream.
+kpm_status exchange_single(Run* r) {
+    kpm_handle_s* h = r->h;
+    double2* X = r->pending;
+    const size_t pb = r->plane_bytes();
+    if (h->dist.comm == KPM_COMM_SELF) {
+        KPM_CUDA(cudaMemcpyAsync(r->ghost_lo(X), r->last_plane(X), pb, cudaMemcpyDeviceToDevice, h->stream));
+        KPM_CUDA(cudaMemcpyAsync(r->ghost_hi(X), r->first_plane(X), pb, cudaMemcpyDeviceToDevice, h->stream));
+        return KPM_OK;
+    }
+    if (h->dist.comm != KPM_COMM_NCCL || !h->nccl) return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL handles need kpm_moments_group");
+    const int W = h->dist.world, rk = h->dist.rank;
+    const int lo = (rk - 1 + W) % W, hi = (rk + 1) % W;
+    ncclResult_t e = ncclGroupStart();
+    if (e == ncclSuccess) e = ncclSend(r->first_plane(X), pb, ncclUint8, lo, h->nccl, h->stream);
+    if (e == ncclSuccess) e = ncclRecv(r->ghost_hi(X), pb, ncclUint8, hi, h->nccl, h->stream);
+    if (e == ncclSuccess) e = ncclSend(r->last_plane(X), pb, ncclUint8, hi, h->nccl, h->stream);
+    if (e == ncclSuccess) e = ncclRecv(r->ghost_lo(X), pb, ncclUint8, lo, h->nccl, h->stream);
+    ncclResult_t e2 = ncclGroupEnd();
+    if (e != ncclSuccess || e2 != ncclSuccess)
+        return fail(KPM_ERR_UNSUPPORTED, "NCCL halo exchange: %s", ncclGetErrorString(e != ncclSuccess ? e : e2));
+    return KPM_OK;
+}
+
+// Halo exchange between the in-process slab handles of a KPM_COMM_LOCAL group: every
+// rank pulls its two ghost planes from its neighbours' freshly written blocks once both
+// neighbours' streams have reached this point.
+kpm_status exchange_group(std::vector<Run>& runs, std::vector<cudaEvent_t>& evs) {
+    const int W = (int)runs.size();
+    for (int i = 0; i < W; ++i) {
+        KPM_CUDA(cudaSetDevice(runs[i].h->device));
+        KPM_CUDA(cudaEventRecord(evs[i], runs[i].h->stream));
+    }
+    for (int i = 0; i < W; ++i) {
+        Run& r = runs[i];
+        Run& rl = runs[(i - 1 + W) % W];
+        Run& rh = runs[(i + 1) % W];
+        KPM_CUDA(cudaSetDevice(r.h->device));
+        KPM_CUDA(cudaStreamWaitEvent(r.h->stream, evs[(i - 1 + W) % W], 0));
+        KPM_CUDA(cudaStreamWaitEvent(r.h->stream, evs[(i + 1) % W], 0));
+        double2* X = r.pending;
+        KPM_CUDA(cudaMemcpyPeerAsync(r.ghost_lo(X), r.h->device, rl.last_plane(rl.pending), rl.h->device, r.plane_bytes(),
+                                     r.h->stream));
+        KPM_CUDA(cudaMemcpyPeerAsync(r.ghost_hi(X), r.h->device, rh.first_plane(rh.pending), rh.h->device, r.plane_bytes(),
+                                     r.h->stream));
+    }
+    return KPM_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -507,6 +864,7 @@ void kpm_destroy(kpm_handle h) {
     cudaFree(h->d_phase);
     cudaFree(h->d_col);
     cudaFree(h->d_val);
+    if (h->nccl) ncclCommDestroy(h->nccl);
     if (h->ev_begin) cudaEventDestroy(h->ev_begin);
     if (h->ev_end) cudaEventDestroy(h->ev_end);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
@@ -570,11 +928,31 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
     h->ndim = d->ndim;
     for (int k = 0; k < 3; ++k) h->L[k] = d->L[k];
     h->D = d->L[0] * d->L[1] * d->L[2];
+    h->D_total = h->D;
     h->t_scaled = d->t / a;
     kpm_status st = KPM_OK;
-    if (d->onsite) {
+    int64_t site0 = 0;  // global index of local site 0
+    if (dist && dist->partition == KPM_PART_ROWS) {
+        h->rows = true;
+        h->slow = d->ndim - 1;
+        h->Lm_global = d->L[h->slow];
+        h->plane = h->D / h->Lm_global;
+        h->z0 = h->Lm_global * dist->rank / dist->world;
+        h->nloc = h->Lm_global * (dist->rank + 1) / dist->world - h->z0;
+        if (h->nloc < 1) st = fail(KPM_ERR_INVALID_ARG, "rank %d of %d owns no planes", dist->rank, dist->world);
+        h->L[h->slow] = h->nloc;
+        h->D = h->plane * h->nloc;
+        site0 = h->z0 * h->plane;
+        if (st == KPM_OK && dist->comm == KPM_COMM_NCCL) {
+            ncclUniqueId id;
+            memcpy(&id, dist->nccl_id, sizeof id);
+            ncclResult_t nr = ncclCommInitRank(&h->nccl, dist->world, id, dist->rank);
+            if (nr != ncclSuccess) st = fail(KPM_ERR_UNSUPPORTED, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+        }
+    }
+    if (st == KPM_OK && d->onsite) {
         std::vector<double> e(h->D);
-        for (int64_t i = 0; i < h->D; ++i) e[i] = (d->onsite[i] - b) / a;  // Eq (8) on the diagonal
+        for (int64_t i = 0; i < h->D; ++i) e[i] = (d->onsite[site0 + i] - b) / a;  // Eq (8) on the diagonal
         cudaError_t ce = cudaMalloc(&h->d_eps, h->D * sizeof(double));
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_eps, e.data(), h->D * sizeof(double), cudaMemcpyHostToDevice);
         if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site upload: %s", cudaGetErrorString(ce));
@@ -615,9 +993,12 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
         c[e] = j < 0 ? (int32_t)i : j;  // padding -> (row, 0)
         for (int q = 0; q < w; ++q) v[e * w + q] = j < 0 ? 0.0 : vin[e * w + q] / a;
     }
+    if (dist && dist->partition == KPM_PART_ROWS)
+        return fail(KPM_ERR_UNSUPPORTED, "row partition is implemented for lattice stencils only");
     kpm_handle_s* h = nullptr;
     KPM_TRY(new_handle(device, dist, &h));
     h->kind = KIND_ELL;
+    h->D_total = D;
     h->dtype = dtype;
     h->a = a;
     h->b = b;
@@ -702,224 +1083,84 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
                           void* out) {
     if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
     if (!out) return fail(KPM_ERR_INVALID_ARG, "NULL output");
-    if ((flags & KPM_PER_VECTOR) && (flags & KPM_RAW_SUMS))
-        return fail(KPM_ERR_INVALID_ARG, "KPM_PER_VECTOR and KPM_RAW_SUMS are exclusive");
-    KPM_CUDA(cudaSetDevice(h->device));
-    Plan p;
-    KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p));
-    if (ensure_workspace(h, p.total) != KPM_OK) {
-        if (!p.use_tma2) return KPM_ERR_OOM;
-        // four vector blocks do not fit: fall back to in-place single steps (two blocks)
-        KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p, true));
-        KPM_TRY(ensure_workspace(h, p.total));
+    if (h->rows && h->dist.comm == KPM_COMM_LOCAL)
+        return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL slab handles run through kpm_moments_group");
+    if (h->rows && h->dist.comm == KPM_COMM_NCCL && (flags & (KPM_RAW_SUMS | KPM_DEVICE_OUT)))
+        return fail(KPM_ERR_UNSUPPORTED, "row partition returns host moments (no raw sums / device output)");
+    Run run;
+    if (h->rows) run.exchange_hook = exchange_single;
+    KPM_TRY(run.begin(h, N, R, seed, r0, flags));
+    if (h->rows) KPM_TRY(run.need_exchange(run.fresh()));
+    while (run.more()) {
+        KPM_TRY(run.launch_next());
+        if (h->rows) KPM_TRY(run.need_exchange(run.fresh()));
     }
-    const bool cplx = is_cplx(h);
-    const bool direct = (flags & KPM_DIRECT) != 0;
-    double2* P = reinterpret_cast<double2*>(h->ws + p.off_P);
-    double2* C = reinterpret_cast<double2*>(h->ws + p.off_C);
-    double2* Rb = reinterpret_cast<double2*>(h->ws + p.off_R);
-    double* part = reinterpret_cast<double*>(h->ws + p.off_part);
-    double* Sv = reinterpret_cast<double*>(h->ws + p.off_Sv);
-    double* S = reinterpret_cast<double*>(h->ws + p.off_S);
-    double* dout = reinterpret_cast<double*>(h->ws + p.off_out);
-    const size_t slot = (size_t)p.gx * p.RP;  // doubles per moment slot of partials
-    h->total_launches = 0;
-    h->step_launches = 0;
-
-    kpm::VecArgs v{};
-    v.P = P;
-    v.C = C;
-    v.Rbuf = Rb;
-    v.D = (int)h->D;
-    v.RG = p.RG;
-    v.RP = p.RP;
-    v.R_loc = p.R_loc;
-    v.key = kpm::vector_key(seed);
-    v.r_off = p.r_off;
-    v.D_total = h->D;
-    v.i_off = 0;
-
-    // a_0: generated in the first-step kernel, or the caller's block staged through C.
-    int first_mode = kpm::FIRST_GEN;
-    if (r0) {
-        const size_t rbytes = (size_t)p.R_loc * h->D * sizeof(double);
-        KPM_CUDA(cudaMemcpyAsync(C, r0, rbytes, (flags & KPM_DEVICE_IN) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice,
-                                 h->stream));
-        const long long n = h->D * (long long)p.RG;
-        const int blocks = (int)std::min<long long>((n + 255) / 256, 8LL * h->num_sms);
-        if (cplx) kpm::load_r0_kernel<true><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double*>(C), P, (int)h->D, p.RG, p.R_loc);
-        else kpm::load_r0_kernel<false><<<blocks, 256, 0, h->stream>>>(reinterpret_cast<double*>(C), P, (int)h->D, p.RG, p.R_loc);
-        KPM_CUDA(cudaGetLastError());
-        h->total_launches++;
-        if (direct) KPM_CUDA(cudaMemcpyAsync(Rb, P, p.lane_bytes, cudaMemcpyDeviceToDevice, h->stream));
-        first_mode = kpm::FIRST_BUF;
+    KPM_TRY(run.collect());
+    if (h->rows && h->dist.comm == KPM_COMM_NCCL) {
+        // moment sums over all slabs: one all-reduce of S (and the per-vector Sv) over NCCL
+        ncclResult_t e = ncclAllReduce(run.S, run.S, N, ncclFloat64, ncclSum, h->nccl, h->stream);
+        if (e == ncclSuccess)
+            e = ncclAllReduce(run.Sv, run.Sv, (size_t)N * run.p.R_loc, ncclFloat64, ncclSum, h->nccl, h->stream);
+        if (e != ncclSuccess) return fail(KPM_ERR_UNSUPPORTED, "NCCL all-reduce: %s", ncclGetErrorString(e));
     }
-    // First step: a_0, a_1 = H~ a_0; S_0 = <a_0|a_0>, S_1 = <a_0|a_1> (Eq 17, 19).
-    v.red0 = part;
-    v.red1 = N > 1 ? part + slot : nullptr;
-    v.red2 = (!direct && N == 3) ? part + 2 * slot : nullptr;
-    KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
+    return run.output(out);
+}
 
-    // Recursion steps (Eq 18).  Single-step launches write a_{n+1} over a_{n-1} in place;
-    // two-step launches (kpm_tma2.cuh) read (a_n, a_{n-1}) and write (a_{n+1}, a_{n+2}) into
-    // the two spare blocks, after which the pairs swap roles.
-    const int nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
-    double2* X2 = reinterpret_cast<double2*>(h->ws + p.off_X2);
-    double2* X3 = reinterpret_cast<double2*>(h->ws + p.off_X3);
-    BufMaps maps[4];
-    int nmaps = 0;
-    CUtensorMap mapE, mapE2;
-    memset(&mapE, 0, sizeof mapE);
-    memset(&mapE2, 0, sizeof mapE2);
-    kpm::TmaGeom tg{};
-    kpm::Tma2Geom tg2{};
-    if (p.use_tma && nsteps > 0) {
-        double2* bufs[4] = {P, C, X2, X3};
-        nmaps = p.use_tma2 ? 4 : 2;
-        for (int i = 0; i < nmaps; ++i) KPM_TRY(make_buf_maps(h, p, bufs[i], &maps[i]));
-        if (h->d_eps) {
-            KPM_TRY(make_eps_map(h, p, &mapE));
-            if (p.use_tma2) KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
-        }
-        tg.L0 = (int)h->L[0];
-        tg.L1 = (int)h->L[1];
-        tg.L2 = (int)h->L[2];
-        tg.TX = p.TX;
-        tg.TY = p.TY;
-        tg.TL = p.TL;
-        tg.RG = p.RG;
-        tg.G_L = p.RG / p.TL;
-        tg.PX = (int)(h->L[0] / p.TX);
-        tg.PY = h->ndim == 3 ? (int)(h->L[1] / p.TY) : 1;
-        tg.Lm = (int)(h->ndim == 2 ? h->L[1] : h->L[2]);
-        tg.W = (long long)tg.G_L * tg.PX * tg.PY * tg.Lm;
-        tg.rr = p.tma_rr;
-        tg.RP = p.RP;
-        tg.t = h->t_scaled;
-        tg.shift = -h->b / h->a;
-        tg.phase = h->d_phase;
-        tg2.L0 = tg.L0;
-        tg2.L1 = tg.L1;
-        tg2.TX = p.TX;
-        tg2.TL = p.TL;
-        tg2.RG = p.RG;
-        tg2.G_L = tg.G_L;
-        tg2.PX = tg.PX;
-        tg2.W = (long long)tg.G_L * tg.PX * tg.L1;
-        tg2.RP = p.RP;
-        tg2.t = tg.t;
-        tg2.shift = tg.shift;
-        tg2.phase = tg.phase;
+kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, uint64_t seed, double* mu) {
+    if (!hs || nh < 1 || !mu) return fail(KPM_ERR_INVALID_ARG, "bad kpm_moments_group arguments");
+    for (int i = 0; i < nh; ++i) {
+        if (!hs[i] || !hs[i]->rows || hs[i]->dist.comm != KPM_COMM_LOCAL || hs[i]->dist.rank != i ||
+            hs[i]->dist.world != nh)
+            return fail(KPM_ERR_INVALID_ARG, "handle %d is not rank %d of a KPM_COMM_LOCAL row partition of %d", i, i, nh);
     }
-    auto maps_of = [&](const void* b) -> const BufMaps& {
-        for (int i = 0; i < nmaps; ++i)
-            if (maps[i].base == b) return maps[i];
-        return maps[0];
+    std::vector<Run> runs(nh);
+    std::vector<cudaEvent_t> evs(nh, nullptr);
+    kpm_status st = KPM_OK;
+    for (int i = 0; i < nh && st == KPM_OK; ++i) {
+        cudaSetDevice(hs[i]->device);
+        if (cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming) != cudaSuccess) st = fail(KPM_ERR_CUDA, "event");
+    }
+    for (int i = 0; i < nh && st == KPM_OK; ++i) st = runs[i].begin(hs[i], N, R, seed, nullptr, 0u);
+    auto exch = [&]() {
+        for (auto& r : runs) r.pending = r.fresh();
+        return exchange_group(runs, evs);
     };
-    KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
-    double2* cur = C;    // a_n
-    double2* prev = P;   // a_{n-1}
-    double2* spare0 = X2;
-    double2* spare1 = X3;
-    h->steps_bytes = 0.0;
-    const double s_el = cplx ? 16.0 : 8.0;
-    const double vbytes = (double)h->D * (double)p.R_loc * s_el;
-    const double ebytes = h->d_eps ? 8.0 * (double)h->D : 0.0;
-    const double mbytes = h->kind == KIND_ELL ? (double)h->K * (double)h->D * (4.0 + s_el) : 0.0;
-    int n = 1;
-    while (n <= nsteps) {
-        const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1));
-        if (pair) {
-            // steps n and n+1: slots 2n .. 2n+3 (+ odd-N tail 2n+4)
-            const bool tail = (N & 1) && n + 1 == nsteps;
-            for (int k = 0; k < 4; ++k) tg2.red[k] = part + (size_t)(2 * n + k) * slot;
-            tg2.red[4] = tail ? part + (size_t)(2 * n + 4) * slot : nullptr;
-            tg2.outB = spare0;
-            tg2.outC = spare1;
-            KPM_TRY(launch_tma2(h, p, maps_of(cur), maps_of(prev), mapE, mapE2, tg2, tail));
-            double2* oc = cur;
-            double2* op = prev;
-            cur = spare1;
-            prev = spare0;
-            spare0 = oc;
-            spare1 = op;
-            h->steps_bytes += 4.0 * vbytes + ebytes;
-            h->step_launches++;
-            n += 2;
-            continue;
-        }
-        v.C = cur;
-        v.P = prev;
-        if (direct) {
-            v.red0 = part + (size_t)(n + 1) * slot;  // <r|a_{n+1}> -> mu_{n+1}
-            v.red1 = v.red2 = nullptr;
-            KPM_TRY(launch(h, p, r0 ? kpm::DIRECT_BUF : kpm::DIRECT_GEN, v, 0));
-            h->steps_bytes += 3.0 * vbytes + ebytes + mbytes + (r0 ? vbytes : 0.0);
-        } else {
-            v.red0 = part + (size_t)(2 * n) * slot;      // <a_n|a_n>     -> mu_{2n}
-            v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
-            const bool tail = (N & 1) && n == nsteps;    // odd N: <a_M|a_M> -> mu_{N-1}
-            v.red2 = tail ? part + (size_t)(2 * n + 2) * slot : nullptr;
-            if (p.use_tma) {
-                tg.red0 = v.red0;
-                tg.red1 = v.red1;
-                tg.red2 = v.red2;
-                tg.out = prev;
-                KPM_TRY(launch_tma(h, p, maps_of(cur), maps_of(prev), mapE, tg, tail));
-            } else {
-                KPM_TRY(launch(h, p, kpm::STEP, v, tail));
-            }
-            h->steps_bytes += 3.0 * vbytes + ebytes + mbytes;
-        }
-        h->step_launches++;
-        std::swap(cur, prev);
-        ++n;
+    if (st == KPM_OK) st = exch();
+    while (st == KPM_OK && runs[0].more()) {
+        for (int i = 0; i < nh && st == KPM_OK; ++i) st = runs[i].launch_next();
+        if (st == KPM_OK) st = exch();
     }
-    KPM_CUDA(cudaEventRecord(h->ev_end, h->stream));
+    std::vector<double> Ssum(N, 0.0), Si(N);
+    for (int i = 0; i < nh && st == KPM_OK; ++i) {
+        st = runs[i].collect();
+        if (st != KPM_OK) break;
+        cudaSetDevice(hs[i]->device);
+        if (cudaMemcpyAsync(Si.data(), runs[i].S, N * sizeof(double), cudaMemcpyDeviceToHost, hs[i]->stream) != cudaSuccess ||
+            cudaStreamSynchronize(hs[i]->stream) != cudaSuccess)
+            st = fail(KPM_ERR_CUDA, "group sums copy failed");
+        for (int k = 0; k < N; ++k) Ssum[k] += Si[k];  // fixed rank order
+    }
+    for (auto e : evs)
+        if (e) cudaEventDestroy(e);
+    if (st != KPM_OK) return st;
+    KPM_TRY(kpm_assemble(nullptr, Ssum.data(), N, hs[0]->D_total, runs[0].p.R_loc, 0u, mu));
+    return Run::spectrum_guard(mu, 1, N);
+}
 
-    // Fixed-order finish of the CTA partials, then the output form.
-    kpm::finish_kernel<<<N, 256, 0, h->stream>>>(part, p.gx, p.RP, p.R_loc, Sv, S);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    const bool dev_out = (flags & KPM_DEVICE_OUT) != 0;
-    size_t out_bytes = 0;
-    const double* src = nullptr;
-    if (flags & KPM_RAW_SUMS) {
-        src = S;
-        out_bytes = (size_t)N * sizeof(double);
-    } else if (flags & KPM_PER_VECTOR) {
-        const long long n = (long long)N * p.R_loc;
-        kpm::assemble_pervec_kernel<<<(unsigned)((n + 255) / 256), 256, 0, h->stream>>>(Sv, N, p.R_loc, 1.0 / (double)h->D,
-                                                                                          direct, dout);
-        KPM_CUDA(cudaGetLastError());
-        h->total_launches++;
-        src = dout;
-        out_bytes = (size_t)n * sizeof(double);
-    } else {
-        if (h->dist.partition == KPM_PART_VECTORS && h->dist.world > 1)
-            return fail(KPM_ERR_INVALID_ARG, "multi-rank: use KPM_RAW_SUMS, all-reduce, then kpm_assemble");
-        kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, 1.0 / ((double)h->D * (double)p.R_loc), direct,
-                                                                     dout);
-        KPM_CUDA(cudaGetLastError());
-        h->total_launches++;
-        src = dout;
-        out_bytes = (size_t)N * sizeof(double);
-    }
-    KPM_CUDA(cudaMemcpyAsync(out, src, out_bytes, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
-    if (dev_out) return KPM_OK;
-    KPM_CUDA(cudaStreamSynchronize(h->stream));
-    // Spectrum guard: |T_n| <= 1 on [-1, 1] (Eq 3) => |mu_n| <= mu_0 when [b-a, b+a] encloses spec(H).
-    if (!(flags & KPM_RAW_SUMS)) {
-        const double* o = static_cast<const double*>(out);
-        const long long rows = (flags & KPM_PER_VECTOR) ? p.R_loc : 1;
-        for (long long r = 0; r < rows; ++r) {
-            const double* m = o + r * N;
-            for (int n = 0; n < N; ++n)
-                if (!std::isfinite(m[n]) || std::fabs(m[n]) > std::fabs(m[0]) * (1.0 + 1e-8) + 1e-300)
-                    return fail(KPM_ERR_SPECTRUM, "|mu_%d| = %g exceeds mu_0 = %g: [b-a, b+a] does not enclose the spectrum", n,
-                                m[n], m[0]);
-        }
-    }
+kpm_status kpm_nccl_unique_id(void* out128) {
+    if (!out128) return fail(KPM_ERR_INVALID_ARG, "NULL output");
+    ncclUniqueId id;
+    ncclResult_t e = ncclGetUniqueId(&id);
+    if (e != ncclSuccess) return fail(KPM_ERR_UNSUPPORTED, "ncclGetUniqueId: %s", ncclGetErrorString(e));
+    memcpy(out128, &id, sizeof id);
+    return KPM_OK;
+}
+
+kpm_status kpm_slab_range(int64_t Lm, int32_t rank, int32_t world, int64_t* begin, int64_t* count) {
+    if (Lm < 1 || world < 1 || rank < 0 || rank >= world || !begin || !count)
+        return fail(KPM_ERR_INVALID_ARG, "bad kpm_slab_range arguments");
+    *begin = Lm * rank / world;
+    *count = Lm * (rank + 1) / world - *begin;
     return KPM_OK;
 }
 

@@ -51,8 +51,10 @@ __device__ __forceinline__ void dot_acc(double2& acc, double2 a, double2 b) {
 
 // ------------------------------------------------------------ operators H~
 struct StencilGeom {
-    int L0, L1, L2;          // extents (sites = L0*L1*L2)
+    int L0, L1, L2;          // extents (sites = L0*L1*L2; the slowest used extent is local under KPM_PART_ROWS)
     int plane;               // L0*L1
+    int ghost;               // 1: the slowest dimension is a slab with a ghost plane on each side
+                             //    (row partition): its neighbours are never wrapped
     double t;                // t / a
     double shift;            // -b / a   (used when there is no on-site array)
     const double* eps;       // (eps_i - b)/a per site, or nullptr
@@ -66,14 +68,16 @@ struct StencilOp {
     template <class XF>
     __device__ __forceinline__ double2 apply(int s, const XF& X, double2 xs) const {
         const int x = s % g.L0;
-        const int xm = (x == 0) ? s + g.L0 - 1 : s - 1;
-        const int xp = (x == g.L0 - 1) ? s - g.L0 + 1 : s + 1;
+        const bool wx = NDIM > 1 || !g.ghost;  // 1D slab: x is the slab dimension
+        const int xm = (x == 0 && wx) ? s + g.L0 - 1 : s - 1;
+        const int xp = (x == g.L0 - 1 && wx) ? s - g.L0 + 1 : s + 1;
         double2 nb = add2(X(xm), X(xp));
         if (NDIM >= 2) {
             const int q = s / g.L0;
             const int y = (NDIM == 2) ? q : q % g.L1;
-            const int ym = (y == 0) ? s + g.plane - g.L0 : s - g.L0;
-            const int yp = (y == g.L1 - 1) ? s - g.plane + g.L0 : s + g.L0;
+            const bool wy = NDIM > 2 || !g.ghost;  // 2D slab: y is the slab dimension
+            const int ym = (y == 0 && wy) ? s + g.plane - g.L0 : s - g.L0;
+            const int yp = (y == g.L1 - 1 && wy) ? s - g.plane + g.L0 : s + g.L0;
             if (PEIERLS) {
                 // H[s][s+e_y] = t e^{-i theta_x}, H[s][s-e_y] = t e^{+i theta_x}
                 const double2 ph = __ldg(g.phase + x);
@@ -84,8 +88,8 @@ struct StencilOp {
             if (NDIM == 3) {
                 const int z = q / g.L1;
                 const int vol = g.plane * g.L2;
-                const int zm = (z == 0) ? s + vol - g.plane : s - g.plane;
-                const int zp = (z == g.L2 - 1) ? s - vol + g.plane : s + g.plane;
+                const int zm = (z == 0 && !g.ghost) ? s + vol - g.plane : s - g.plane;
+                const int zp = (z == g.L2 - 1 && !g.ghost) ? s - vol + g.plane : s + g.plane;
                 nb = add2(nb, add2(X(zm), X(zp)));
             }
         }
@@ -134,6 +138,7 @@ struct VecArgs {
     long long r_off;       // global index of this GPU's first vector
     long long D_total;     // global number of sites (RNG counter stride)
     long long i_off;       // global index of this GPU's site 0
+    int ghost;             // row partition: site indices j < 0 or >= D are ghost sites (wrap globally)
     double* red0;          // partial sums of moment slot 0: [gridDim.x][RP] (nullable)
     double* red1;          // slot 1
     double* red2;          // slot 2 (odd-N tail <a_{n+1}|a_{n+1}>)
@@ -141,7 +146,9 @@ struct VecArgs {
 
 template <bool CPLX>
 __device__ __forceinline__ double2 gen_lane(const VecArgs& v, int j, int rg) {
-    const uint64_t i = (uint64_t)(v.i_off + j);
+    long long ig = v.i_off + j;
+    if (v.ghost) ig = (ig % v.D_total + v.D_total) % v.D_total;  // ghost plane of a neighbouring slab
+    const uint64_t i = (uint64_t)ig;
     if (CPLX) {
         const long long r = rg;
         return make_double2(r < v.R_loc ? rademacher(v.key, (uint64_t)(v.r_off + r) * v.D_total + i) : 0.0, 0.0);

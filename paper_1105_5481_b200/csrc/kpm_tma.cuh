@@ -110,6 +110,8 @@ struct TmaGeom {
     int Lm;           // march extent (L1 in 2D, L2 in 3D)
     long long W;      // total output planes = G_L * PX * PY * Lm
     int rr;           // 1: round-robin whole columns over CTAs; 0: contiguous plane ranges
+    int ghost;        // 1: row partition -- vector buffers hold Lm + 2 planes (ghost, local..., ghost),
+                      //    march neighbours are never wrapped; 0: periodic wrap
     int RP;           // padded vectors (partial row length)
     double t;         // t / a
     double shift;     // -b / a (no on-site array)
@@ -246,7 +248,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 const int yt = (y0 - 1 + g.L1) % g.L1, yb = (y0 + g.TY) % g.L1;
                 const int H = s.m1 - s.m0;
                 for (int q = 0; q < H + 2; ++q) {
-                    const int m = (s.m0 - 1 + q + g.Lm) % g.Lm;
+                    // buffer plane of march coordinate m0-1+q
+                    const int m = g.ghost ? s.m0 + q : (s.m0 - 1 + q + g.Lm) % g.Lm;
                     const int slot = (int)(ia % kSA);
                     if (ia >= kSA) mbar_wait(emptyA + slot, (uint32_t)(((ia / kSA) - 1) & 1));
                     unsigned char* dst = ringA + slot * SL.bytes;
@@ -255,19 +258,19 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         tma_load(dst + SL.main_off, &mapA, fullA + slot, c0, x0, m);
                         tma_load(dst + SL.left_off, &mapCol, fullA + slot, c0, xl, m);
                         tma_load(dst + SL.right_off, &mapCol, fullA + slot, c0, xr, m);
-                        if (ONSITE) tma_load_2d(dst + SL.eps_off, &mapE, fullA + slot, x0, m);
+                        if (ONSITE) tma_load_2d(dst + SL.eps_off, &mapE, fullA + slot, x0, m - g.ghost);
                     } else {
                         tma_load(dst + SL.main_off, &mapA, fullA + slot, c0, x0, y0, m);
                         tma_load(dst + SL.left_off, &mapCol, fullA + slot, c0, xl, y0, m);
                         tma_load(dst + SL.right_off, &mapCol, fullA + slot, c0, xr, y0, m);
                         tma_load(dst + SL.top_off, &mapRow, fullA + slot, c0, x0, yt, m);
                         tma_load(dst + SL.bot_off, &mapRow, fullA + slot, c0, x0, yb, m);
-                        if (ONSITE) tma_load(dst + SL.eps_off, &mapE, fullA + slot, x0, y0, m);
+                        if (ONSITE) tma_load(dst + SL.eps_off, &mapE, fullA + slot, x0, y0, m - g.ghost);
                     }
                     ++ia;
                     // a_{n-1} for output plane q-1, issued right behind the a_n plane it pairs with
                     if (q >= 1 && q - 1 < H) {
-                        const int mp = s.m0 + q - 1;
+                        const int mp = s.m0 + q - 1 + g.ghost;
                         const int ps = (int)(ip % kSP);
                         if (ip >= kSP) mbar_wait(emptyP + ps, (uint32_t)(((ip / kSP) - 1) & 1));
                         mbar_expect_tx(fullP + ps, tile_bytes);
@@ -329,7 +332,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 const unsigned char* S1 = ringA + (int)(i1 % kSA) * SL.bytes;  // plane m
                 const unsigned char* S2 = ringA + (int)(i2 % kSA) * SL.bytes;  // plane m+1
                 const double2* Pv = reinterpret_cast<const double2*>(ringP + ps * tile_bytes);
-                const int m = s.m0 + j;
+                const int m = s.m0 + j + g.ghost;  // buffer plane of the output
                 auto lane_at = [&](const unsigned char* base, int off, int site) {
                     return reinterpret_cast<const double2*>(base + off)[site * g.TL + l];
                 };

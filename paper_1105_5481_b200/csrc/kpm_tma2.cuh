@@ -115,7 +115,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     constexpr int CONS = kThreads2;
     constexpr int KSTEP = CONS / TL;              // tile sites per pass
     constexpr int NB = TX + 2;                    // a_{n+1} sites per row (with halo)
-    constexpr int NPB = (NB + KSTEP - 1) / KSTEP; // passes per row
     constexpr int SITE = TL * 16;
     constexpr Slot2Layout SL(TX, TL, ONSITE);
     extern __shared__ __align__(128) unsigned char smem[];

@@ -26,12 +26,14 @@ KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM
 KPM_REAL64, KPM_COMPLEX128 = 0, 1
 KPM_KERNEL_JACKSON, KPM_KERNEL_NONE = 0, 1
 KPM_PER_VECTOR, KPM_DIRECT, KPM_DEVICE_OUT, KPM_RAW_SUMS, KPM_DEVICE_IN = 1, 2, 4, 8, 16
-KPM_PART_NONE, KPM_PART_VECTORS = 0, 1
+KPM_PART_NONE, KPM_PART_VECTORS, KPM_PART_ROWS = 0, 1, 2
+KPM_COMM_SELF, KPM_COMM_NCCL, KPM_COMM_LOCAL = 0, 1, 2
 
 EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershgorin_stencil",
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
-           "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_destroy", "kpm_last_error", "kpm_version"]
+           "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
+           "kpm_moments_group", "kpm_destroy", "kpm_last_error", "kpm_version"]
 
 
 class kpm_stencil_desc(ctypes.Structure):
@@ -40,7 +42,8 @@ class kpm_stencil_desc(ctypes.Structure):
 
 
 class kpm_dist(ctypes.Structure):
-    _fields_ = [("partition", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32)]
+    _fields_ = [("partition", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
+                ("comm", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
 
 
 _P, _i32, _i64, _u32, _u64, _f64, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
@@ -62,6 +65,9 @@ _SIG = {
     "kpm_last_timing": [_P, _P, _P, _P],
     "kpm_step_bytes": [_P, _P],
     "kpm_plan_info": [_P, _i32, _i64, _u32, _P],
+    "kpm_slab_range": [_i64, _i32, _i32, _P, _P],
+    "kpm_nccl_unique_id": [_P],
+    "kpm_moments_group": [_P, _i32, _i32, _i64, _u64, _P],
 }
 for _name, _args in _SIG.items():
     _fn = getattr(_lib, _name)
@@ -105,10 +111,15 @@ def _desc(ndim, L, t, onsite, flux):
 
 
 def _dist(dist):
+    """dist: None, (partition, rank, world) or (partition, rank, world, comm[, nccl_id bytes])."""
     if dist is None:
-        return None
-    part, rank, world = dist
-    return ctypes.byref(kpm_dist(int(part), int(rank), int(world)))
+        return None, None
+    part, rank, world = dist[:3]
+    comm = dist[3] if len(dist) > 3 else KPM_COMM_SELF
+    nid = dist[4] if len(dist) > 4 else None
+    keep = ctypes.create_string_buffer(bytes(nid), 128) if nid is not None else None
+    st = kpm_dist(int(part), int(rank), int(world), int(comm), ctypes.cast(keep, ctypes.c_void_p) if keep else None)
+    return ctypes.byref(st), (st, keep)
 
 
 def kpm_gershgorin_stencil(ndim, L, t, onsite=None, flux=0.0, eps=0.0):
@@ -141,7 +152,8 @@ class Handle:
 
     def __init__(self, raw, D, R_of=None, dist=None):
         self._h = raw
-        self.D = int(D)
+        self.D = int(D)          # global number of sites
+        self.D_local = int(D)    # sites on this rank (row partition: its slab)
         self.dist = dist
 
     def __del__(self):
@@ -190,7 +202,7 @@ class Handle:
             r0p = ctypes.c_void_p(int(r0))
         else:
             keep = np.ascontiguousarray(r0, dtype=np.float64)
-            assert keep.shape == (R_loc, self.D), (keep.shape, (R_loc, self.D))
+            assert keep.shape == (R_loc, self.D_local), (keep.shape, (R_loc, self.D_local))
             r0p = _ptr(keep)
         if isinstance(out, (int, np.integer)):
             _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags),
@@ -233,16 +245,23 @@ class Handle:
 def kpm_create_stencil(ndim, L, t, a, b, onsite=None, flux=0.0, device=0, dist=None) -> Handle:
     d, _keep = _desc(ndim, L, t, onsite, flux)
     h = ctypes.c_void_p()
-    _check(_lib.kpm_create_stencil(ctypes.byref(d), float(a), float(b), int(device), _dist(dist), ctypes.byref(h)))
+    dp, _keep2 = _dist(dist)
+    _check(_lib.kpm_create_stencil(ctypes.byref(d), float(a), float(b), int(device), dp, ctypes.byref(h)))
     Ls = tuple(L) + (1,) * (3 - len(L))
-    return Handle(h.value, Ls[0] * Ls[1] * Ls[2], dist=dist)
+    hd = Handle(h.value, Ls[0] * Ls[1] * Ls[2], dist=dist)
+    if dist is not None and dist[0] == KPM_PART_ROWS:
+        slow = int(ndim) - 1
+        _, cnt = kpm_slab_range(Ls[slow], dist[1], dist[2])
+        hd.D_local = hd.D // Ls[slow] * cnt
+    return hd
 
 
 def kpm_create_csr(D, rowptr, col, val, a, b, device=0, dist=None) -> Handle:
     rowptr, col, v, dt = _csr_arrays(rowptr, col, val)
     h = ctypes.c_void_p()
+    dp, _keep = _dist(dist)
     _check(_lib.kpm_create_csr(int(D), _ptr(rowptr), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
-                               _dist(dist), ctypes.byref(h)))
+                               dp, ctypes.byref(h)))
     return Handle(h.value, D, dist=dist)
 
 
@@ -254,8 +273,9 @@ def kpm_create_ell(D, K, col, val, a, b, device=0, dist=None) -> Handle:
     else:
         v, dt = np.ascontiguousarray(val, dtype=np.float64), KPM_REAL64
     h = ctypes.c_void_p()
+    dp, _keep = _dist(dist)
     _check(_lib.kpm_create_ell(int(D), int(K), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
-                               _dist(dist), ctypes.byref(h)))
+                               dp, ctypes.byref(h)))
     return Handle(h.value, D, dist=dist)
 
 
@@ -277,6 +297,42 @@ def kpm_assemble_host(S, N, D, R, flags=0):
     mu = np.zeros(int(N), dtype=np.float64)
     _check(_lib.kpm_assemble(None, _ptr(S), int(N), int(D), int(R), int(flags) & ~KPM_DEVICE_OUT, _ptr(mu)))
     return mu
+
+
+def kpm_slab_range(Lm, rank, world):
+    """(begin, count) of the planes of the slowest lattice dimension rank owns under KPM_PART_ROWS."""
+    b, c = ctypes.c_int64(), ctypes.c_int64()
+    _check(_lib.kpm_slab_range(int(Lm), int(rank), int(world), ctypes.byref(b), ctypes.byref(c)))
+    return b.value, c.value
+
+
+def kpm_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(_lib.kpm_nccl_unique_id(buf))
+    return buf.raw
+
+
+def kpm_moments_group(handles, N, R, seed):
+    """KPM_COMM_LOCAL row partition: all slab handles of this process in lock step."""
+    arr = (ctypes.c_void_p * len(handles))(*[h.raw for h in handles])
+    mu = np.zeros(int(N), dtype=np.float64)
+    _check(_lib.kpm_moments_group(arr, len(handles), int(N), int(R), int(seed), _ptr(mu)))
+    return mu
+
+
+def nccl_id_for_group(group=None) -> bytes:
+    """ncclUniqueId made on rank 0 and broadcast to every rank with torch.distributed
+    (the plumbing for KPM_COMM_NCCL; the library then creates its own communicator)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.zeros(128, dtype=torch.uint8)
+    if dist.get_rank(group) == 0:
+        t = torch.frombuffer(bytearray(kpm_nccl_unique_id()), dtype=torch.uint8).clone()
+    backend = dist.get_backend(group)
+    if backend == "nccl":
+        t = t.cuda()
+    dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+    return bytes(t.cpu().numpy().tobytes())
 
 
 def kpm_vector_range(R, rank, world):

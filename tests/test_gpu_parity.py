@@ -218,3 +218,53 @@ def test_dos_matches_oracle(kpm):
         rho = kpm.kpm_dos(mu, 4.0, 0.0, om, kernel=kern)
         ref = oracle.dos(mu, 4.0, 0.0, om, kernel=name)
         assert np.abs(rho - ref).max() < 1e-10 * np.abs(ref).max()
+
+
+# ---------------------------------------------------------------- row partition (P2)
+ROW_CASES = {
+    "1d": (lat_of(1, (600,)), 30, 5),
+    "2d_simple": (lat_of(2, (37, 29)), 26, 7),
+    "2d_tma": (lat_of(2, (64, 40)), 24, 64),
+    "2d_peierls_tma": (lat_of(2, (64, 16), flux=1 / 8, W=1.0), 21, 32),
+    "3d_simple": (lat_of(3, (13, 11, 9), W=2.0), 22, 6),
+    "3d_tma": (lat_of(3, (32, 16, 12), W=2.0), 25, 16),
+}
+
+
+@pytest.mark.parametrize("comm", ["self", "nccl"])
+@pytest.mark.parametrize("case", sorted(ROW_CASES))
+def test_row_partition_world1_matches_oracle(kpm, case, comm):
+    """KPM_PART_ROWS with one rank: slab + ghost planes refreshed after every step (a local
+    copy, or NCCL send/recv to itself), moment sums through the NCCL all-reduce."""
+    lat, N, R = ROW_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    r = ki.rademacher(8, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    if comm == "self":
+        dist = (kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_SELF)
+    else:
+        dist = (kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_NCCL, kpm.kpm_nccl_unique_id())
+    h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"], dist=dist)
+    assert h.plan_info(N, R)["two_step"] == 0
+    mu = h.moments(N, R, 8)
+    assert normwise(mu, ref) < TOL
+    assert normwise(h.moments_ex(N, R, 8, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
+    assert np.array_equal(h.moments_ex(N, R, 8, r0=r), mu)  # a_0 ghosts exchanged before the first step
+    whole = make(kpm, lat, a, b).moments(N, R, 8)
+    assert normwise(mu, whole) < 1e-13
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("case", ["1d", "2d_tma", "2d_peierls_tma", "3d_simple", "3d_tma"])
+def test_row_partition_local_group_matches_oracle(kpm, case, world):
+    """KPM_COMM_LOCAL: `world` slab handles in one process (one GPU) exchange halo planes
+    after every step; uneven slabs included.  Same global vectors as one whole lattice."""
+    lat, N, R = ROW_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(8, R, lat["D"]), N)
+    hs = [kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
+                                 dist=(kpm.KPM_PART_ROWS, rk, world, kpm.KPM_COMM_LOCAL)) for rk in range(world)]
+    mu = kpm.kpm_moments_group(hs, N, R, 8)
+    assert normwise(mu, ref) < TOL

@@ -96,3 +96,32 @@ def test_assemble_host_transform():
     c = 1 / 10
     assert np.allclose(mu, [1.0, 0.4, 2 * 0.7 - 1.0, 2 * 0.3 - 0.4, 2 * 0.9 - 1.0], rtol=0, atol=1e-15)
     assert np.allclose(kpm.kpm_assemble_host(S, 5, 5, 2, flags=kpm.KPM_DIRECT), S * c)
+
+
+def _id_worker(rank, world, port, out):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_1105_5481_b200 import kpm
+    out[rank] = kpm.nccl_id_for_group().hex()
+    dist.destroy_process_group()
+
+
+def test_row_partition_nccl_id_broadcast_over_gloo():
+    """Plumbing of KPM_COMM_NCCL: rank 0's ncclUniqueId reaches every rank unchanged."""
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_id_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    assert out[0] == out[1] and len(out[0]) == 256
+
+
+def test_slab_range_tiles_planes_and_ell_rows_rejected():
+    from paper_1105_5481_b200 import kpm
+    for Lm, world in [(512, 8), (10, 3), (7, 7), (128, 5)]:
+        got = [kpm.kpm_slab_range(Lm, r, world) for r in range(world)]
+        assert got[0][0] == 0 and sum(c for _, c in got) == Lm and min(c for _, c in got) >= 1
+        assert all(got[i][0] + got[i][1] == got[i + 1][0] for i in range(world - 1))
+    with pytest.raises(kpm.KPMError) as e:
+        kpm.kpm_create_ell(10, 1, [[0] * 10], [[0.0] * 10], 1.0, 0.0, dist=(kpm.KPM_PART_ROWS, 0, 1))
+    assert e.value.status == kpm.KPM_ERR_UNSUPPORTED
