@@ -155,11 +155,14 @@ def run_reference(args, cfg, lat, a, b, rank, world):
 
 
 def config_obj(args, cfg, lat, world):
+    rows = getattr(args, "partition", "vectors") == "rows"
     return {"workload": f"BASELINE.json configs[{int(args.config[1]) - 1}]: {cfg['name']}", "config": args.config,
-            "D": lat["D"], "N": cfg["N"], "R_per_gpu": cfg["R"], "R_total": cfg["R"] * world, "ndim": lat["ndim"],
+            "D": lat["D"], "N": cfg["N"], "R_per_gpu": cfg["R"] if not rows else None,
+            "R_total": cfg["R"] * (1 if rows else world), "ndim": lat["ndim"],
             "L": list(lat["L"]), "t": lat["t"], "anderson_W": cfg["W"], "flux": lat["flux"],
             "vector_seed": cfg["seed"], "disorder_seed": cfg["disorder_seed"],
-            "parallelism": f"vectors{world}", "l2": "inputs larger than L2 (2 x D*R*s vector blocks)"}
+            "parallelism": f"rows{world}" if rows else f"vectors{world}",
+            "l2": "inputs larger than L2 (2 x D*R*s vector blocks)"}
 
 
 def main():
@@ -171,6 +174,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--partition", default="vectors", choices=["vectors", "rows"],
+                    help="vectors: each rank owns R vectors of its own (weak scaling, one all-reduce); rows: "
+                         "the lattice is cut into slabs of the slowest dimension with halo exchange over NCCL "
+                         "every step (strong scaling, BASELINE.json configs[4])")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -195,8 +202,17 @@ def main():
 
     a, b = kpm.kpm_gershgorin_stencil(lat["ndim"], lat["L"], lat["t"], onsite=lat["onsite"], flux=lat["flux"])
     N, R_loc = cfg["N"], cfg["R"]
-    R = R_loc * world
-    part = (kpm.KPM_PART_VECTORS, rank, world)
+    rows = args.partition == "rows"
+    if rows:
+        args.no_e2e = True  # the slab path's host-output call is already what `value` times
+        if world == 1:
+            dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
+                                    rank=0, world_size=1)
+        R = R_loc
+        part = (kpm.KPM_PART_ROWS, rank, world, kpm.KPM_COMM_NCCL, kpm.nccl_id_for_group())
+    else:
+        R = R_loc * world
+        part = (kpm.KPM_PART_VECTORS, rank, world)
     h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
                                device=local_rank, dist=part)
     stream = torch.cuda.Stream(device=dev)
@@ -209,6 +225,9 @@ def main():
     mu = torch.empty(N, dtype=torch.float64, device=dev)
 
     def step():
+        if rows:  # halo exchange and the moment all-reduce run inside the library (NCCL)
+            mu.copy_(torch.from_numpy(h.moments(N, R, cfg["seed"])))
+            return
         h.moments_ex(N, R, cfg["seed"], flags=kpm.KPM_RAW_SUMS | kpm.KPM_DEVICE_OUT, out=S.data_ptr())
         if world > 1:
             with torch.cuda.stream(stream):
@@ -299,7 +318,8 @@ def main():
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+                "scaling": "strong" if rows else "weak",
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Rademacher vectors, lattice H)",
                 "config": config_obj(args, cfg, lat, world),
                 "hbm_gbs_alg": steps_bytes / args.steps / (ms_per_step / 1000.0) / 1e9 * world,
@@ -312,7 +332,7 @@ def main():
                 "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
                                                         "max_abs_mu": float(np.abs(mu_host).max())}}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dist.is_initialized():
         dist.destroy_process_group()
 
 
