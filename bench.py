@@ -104,8 +104,9 @@ def profiled_traffic(config, plan):
         rec = json.load(open(p))[config]
     except Exception:
         return None
-    if rec.get("tma") != plan["tma"]:
-        return None
+    want = "step2" if plan.get("two_step") else ("step_tma" if plan["tma"] else "kpm_step_kernel")
+    if want not in rec.get("kernel", ""):
+        return None  # the committed capture is of another kernel: no traffic claim
     return rec["dram_bytes_per_launch"]
 
 

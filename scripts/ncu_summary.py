@@ -67,7 +67,7 @@ def main(src, rnd):
             rd = sum(agg["dram__bytes_read.sum"]) / n
             wr = sum(agg["dram__bytes_write.sum"]) / n
             t = sum(agg["gpu__time_duration.sum"]) / n
-            traffic[c] = {"tma": int("tma" in (name or "")), "kernel": (name or "")[:100], "launches": n,
+            traffic[c] = {"tma": int("tma" in (name or "")), "kernel": (name or "")[:160], "launches": n,
                           "dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes_per_launch": rd + wr,
                           "mean_duration_ns": t, "round": rnd,
                           "note": "mean over steady-state step launches (ncu, -s 4 -c 8)"}

@@ -13,8 +13,8 @@ for c in $CONFIGS; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file $OUT/launchlist_$c.csv $B --config $c > /dev/null 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:kpm_step -s 4 -c 8 --csv --log-file $OUT/dram_$c.csv $B --config $c > /dev/null 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:kpm_step -s 5 -c 1 \
+    -k regex:"kpm_step2?_tma|kpm_step_kernel" -s 4 -c 8 --csv --log-file $OUT/dram_$c.csv $B --config $c > /dev/null 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kpm_step2?_tma" -s 5 -c 1 \
     -o $OUT/full_$c $B --config $c > $OUT/full_$c.log 2>&1
 done
 ls -la $OUT

@@ -268,3 +268,34 @@ def test_row_partition_local_group_matches_oracle(kpm, case, world):
                                  dist=(kpm.KPM_PART_ROWS, rk, world, kpm.KPM_COMM_LOCAL)) for rk in range(world)]
     mu = kpm.kpm_moments_group(hs, N, R, 8)
     assert normwise(mu, ref) < TOL
+
+
+def test_randomized_shapes_sweep(kpm):
+    """Random small lattices (1D/2D/3D, with/without disorder or flux), R, N and (a, b): all
+    kernel paths (generic, TMA march, two-step) against the oracle."""
+    rng = np.random.default_rng(1234)
+    for trial in range(24):
+        ndim = int(rng.integers(1, 4))
+        if ndim == 1:
+            L = (int(rng.integers(3, 400)),)
+        elif ndim == 2:
+            L = tuple(int(v) for v in rng.choice([4, 6, 16, 32, 64], 2)) if trial % 2 else \
+                tuple(int(v) for v in rng.integers(3, 40, 2))
+        else:
+            L = tuple(int(v) for v in rng.choice([4, 8, 16, 32], 3)) if trial % 2 else \
+                tuple(int(v) for v in rng.integers(3, 14, 3))
+        flux = 0.0
+        if ndim == 2 and rng.random() < 0.4:
+            q = int(rng.choice([2, 4, 8]))
+            if L[0] % q == 0:
+                flux = 1.0 / q
+        W = float(rng.choice([0.0, 1.5]))
+        R = int(rng.choice([1, 3, 8, 16, 32, 64]))
+        N = int(rng.integers(1, 40))
+        lat = lat_of(ndim, L, W=W, flux=flux, dseed=trial)
+        H = oracle.lattice_csr(lat)
+        a, b = oracle.gershgorin(H)
+        a *= 1.0 + 0.1 * rng.random()
+        ref = oracle.moments_doubling(H, a, b, ki.rademacher(trial, R, lat["D"]), N)
+        mu = make(kpm, lat, a, b).moments(N, R, trial)
+        assert normwise(mu, ref) < TOL, (trial, ndim, L, flux, W, R, N)
