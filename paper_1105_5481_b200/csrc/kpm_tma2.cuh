@@ -74,7 +74,7 @@ struct Slot2Layout {
 __host__ __device__ inline size_t step2_smem_bytes(int TX, int TL, bool onsite, int RP) {
     const Slot2Layout S(TX, TL, onsite);
     return (size_t)kSA2 * S.a_bytes + (size_t)kSP2 * S.p_bytes + (size_t)kSB2 * S.b_bytes + 5 * (size_t)RP * 8 +
-           (size_t)kThreads2 * 16 + (size_t)(TX + 2) * 16 + (kSA2 + kSP2 + kSB2) * 8;
+           (size_t)kThreads2 * 16 + (size_t)(TX + 2) * 16 + (kSA2 + kSP2) * 8;
 }
 
 // Walks one CTA's segments (lane group, pencil, rows [m0, m0+H)) and, within a segment,
@@ -129,7 +129,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     double2* sphase = sred + CONS;                                         // [TX + 2]
     uint64_t* fullA = reinterpret_cast<uint64_t*>(sphase + TX + 2);
     uint64_t* fullP = fullA + kSA2;
-    uint64_t* doneB = fullP + kSP2;  // per a_{n+1} ring slot: all warps wrote their part of the row
 
     const int t = threadIdx.x;
     const long long w_begin = g.W * blockIdx.x / gridDim.x;
@@ -173,7 +172,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     if (t == 0) {
         for (int i = 0; i < kSA2; ++i) mbar_init(fullA + i, 1);
         for (int i = 0; i < kSP2; ++i) mbar_init(fullP + i, 1);
-        for (int i = 0; i < kSB2; ++i) mbar_init(doneB + i, kThreads2 / 32);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         prefetch_tmap(&mapA);
         prefetch_tmap(&mapA2);
@@ -240,7 +238,6 @@ __global__ void __launch_bounds__(kThreads2, 1)
     LoadCursor cs;  // segment iterator of the consumers (same sequence)
     cs.init(g, w_begin, w_end, 0);
     int ia = 0, ip = 0, cur_lg = -1;
-    int kb = 0;     // a_{n+1} rows written by this CTA so far (ring slot kb % 3, mbarrier phase)
     while (cs.valid) {
         const int lg = cs.lg, m0 = cs.m0, H = cs.H, x0 = cs.px * TX;
         if (cur_lg != -1 && lg != cur_lg) flush(cur_lg);
@@ -254,6 +251,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             __syncthreads();
         }
         const int ia_seg = ia;
+        int sB = 0;                                   // ring slot of a_{n+1} row q
         int s0 = ia_seg % kSA2;                       // ring slot of a_n row r-1
         int ps = ip % kSP2;
         int rB = (m0 - 1 + g.L1) % g.L1;              // a_{n+1} row r
@@ -262,33 +260,22 @@ __global__ void __launch_bounds__(kThreads2, 1)
         // a_n at rows r-1, r, r+1; a_{n+1} at rows r-2, r-1; eps~ at row r-1
         double2 am[NPI], ac[NPI], ap[NPI], bm[NPI], bc[NPI];
         double em[NPI];
-        double2 amh, ach;  // halo site: a_n rows r-1, r (the slot of row r-1 is refilled during row r)
-        for (int q = 0; q < H + 2; ++q, ++kb) {
+        for (int q = 0; q < H + 2; ++q) {
             const int i0 = ia_seg + q;
             const int s1 = s0 + 1 == kSA2 ? 0 : s0 + 1;
             const int s2 = s1 + 1 == kSA2 ? 0 : s1 + 1;
-            const int sB = kb % kSB2;                     // a_{n+1} row r
-            const int sBc = (kb + kSB2 - 1) % kSB2;       // a_{n+1} row r-1
             if (q == 0) {
                 mbar_wait(fullA + s0, (uint32_t)((i0 / kSA2) & 1));
                 mbar_wait(fullA + s1, (uint32_t)(((i0 + 1) / kSA2) & 1));
-            } else {
-                // row r-1 of a_{n+1} complete: its values are read below, and nobody reads
-                // a_n row r-1 or a_{n-1} row r-1 any more -> their slots can be refilled
-                mbar_wait(doneB + sBc, (uint32_t)(((kb - 1) / kSB2) & 1));
-                if (t == PRODUCER) {  // refills in load-sequence order
-                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                    if (q == 1) issueA(s0 == 0 ? kSA2 - 1 : s0 - 1);  // a_n row m0-2 (read at q = 0 only)
-                    issueA(s0);                                       // a_n row r-1
-                    issueP(ps == 0 ? kSP2 - 1 : ps - 1);              // a_{n-1} row r-1
-                }
             }
             mbar_wait(fullA + s2, (uint32_t)(((i0 + 2) / kSA2) & 1));
             mbar_wait(fullP + ps, (uint32_t)((ip / kSP2) & 1));
+            const unsigned char* A0 = ringA + s0 * SL.a_bytes;   // a_n row r-1
             const unsigned char* A1 = ringA + s1 * SL.a_bytes;   // a_n row r
             const unsigned char* A2 = ringA + s2 * SL.a_bytes;   // a_n row r+1
             const unsigned char* Pq = ringP + ps * SL.p_bytes;   // a_{n-1} row r
             unsigned char* Bq = ringB + sB * SL.b_bytes;         // a_{n+1} row r (written now)
+            const int sBc = sB == 0 ? kSB2 - 1 : sB - 1;
             const unsigned char* Bc = ringB + sBc * SL.b_bytes;  // a_{n+1} row r-1
             const bool own_b = (q >= 1 && q <= H);
             const bool do_c = (q >= 2);
@@ -301,9 +288,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 const int ob = (lx + 1) * SITE + lo;  // a_{n+1} / a_{n-1} slot index
                 const double2 ph = PEIERLS ? sphase[lx + 1] : make_double2(0.0, 0.0);
                 if (q == 0) {
-                    am[p] = ld(ringA + s0 * SL.a_bytes + oa);
+                    am[p] = ld(A0 + oa);
                     ac[p] = ld(A1 + oa);
-                    if (ONSITE) em[p] = reinterpret_cast<const double*>(ringA + s0 * SL.a_bytes + SL.eps_m)[lx];
+                    if (ONSITE) em[p] = reinterpret_cast<const double*>(A0 + SL.eps_m)[lx];
                 }
                 ap[p] = ld(A2 + oa);
                 // first step: a_{n+1}(row r, lx)
@@ -336,35 +323,29 @@ __global__ void __launch_bounds__(kThreads2, 1)
             if (hs >= 0) {  // halo a_{n+1} site (recomputed here, owned by the neighbouring pencil)
                 const int oa = (hlx + 2) * SITE + lo;
                 const int ob = (hlx + 1) * SITE + lo;
-                if (q == 0) {
-                    amh = ld(ringA + s0 * SL.a_bytes + oa);
-                    ach = ld(A1 + oa);
-                }
-                const double2 aph = ld(A2 + oa);
                 const double2 ph = PEIERLS ? sphase[hlx + 1] : make_double2(0.0, 0.0);
                 const double e1 = ONSITE ? SL.eps(A1, hlx, TX) : g.shift;
-                const double2 b = step_val(ach, ld(A1 + oa - SITE), ld(A1 + oa + SITE), amh, aph, e1, ph, ld(Pq + ob));
+                const double2 b = step_val(ld(A1 + oa), ld(A1 + oa - SITE), ld(A1 + oa + SITE), ld(A0 + oa), ld(A2 + oa), e1,
+                                           ph, ld(Pq + ob));
                 *reinterpret_cast<double2*>(Bq + ob) = b;
-                amh = ach;
-                ach = aph;
             }
-            __syncwarp();
-            if ((t & 31) == 0) mbar_arrive(doneB + sB);  // this warp's part of a_{n+1} row r is written
+            __syncthreads();  // row q done: slots of a_n row r-1 and a_{n-1} row r are free
+            if (t == PRODUCER) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issueA(s0);
+                issueP(ps);
+            }
             ++ip;
+            sB = sB + 1 == kSB2 ? 0 : sB + 1;
             s0 = s1;
             ps = ps + 1 == kSP2 ? 0 : ps + 1;
             rB = rB + 1 == g.L1 ? 0 : rB + 1;
             rC = rC + 1 == g.L1 ? 0 : rC + 1;
         }
-        // segment end: every warp done with the last row -> refill the slots still held
-        mbar_wait(doneB + (kb - 1) % kSB2, (uint32_t)(((kb - 1) / kSB2) & 1));
-        if (t == PRODUCER) {
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        if (t == PRODUCER) {  // the segment's last two a_n rows are free too
             issueA((ia_seg + H + 2) % kSA2);
             issueA((ia_seg + H + 3) % kSA2);
-            issueP(ps == 0 ? kSP2 - 1 : ps - 1);
         }
-        __syncthreads();
         ia = ia_seg + H + 4;
         cs.seg(g, 0);
     }
