@@ -205,11 +205,13 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
 
 /* Execution plan kpm_moments_ex would use for (N, R, flags): info[0] = 1 if the
  * TMA-pipelined march kernel runs the recursion steps (2D/3D stencils), else 0;
- * info[1..3] = lanes per tile TL, tile TX, TY; info[4] = CTAs per step launch;
- * info[5] = dynamic shared memory bytes of the step kernel; info[6] = lanes per site;
- * info[7] bit 0: whole (lane group, pencil) columns are dealt round-robin to CTAs;
- *         bit 1: two recursion steps per launch (temporal blocking, 2D; 4 vector blocks). */
-kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[8]);
+ * info[1..3] = lanes per tile TL, tile TX, TY; info[4] = partial-sum rows per moment slot
+ * (CTAs of the widest step kernel); info[5] = dynamic shared memory bytes of the step
+ * kernel; info[6] = lanes per site; info[7] bit 0: whole (lane group, pencil) columns are
+ * dealt round-robin to CTAs; bit 1: two recursion steps per launch (temporal blocking, 2D;
+ * 4 vector blocks); info[8] = two-step tile width TX2; info[9] = two-step CTAs per SM;
+ * info[10] = two-step grid; info[11] = 0. */
+kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[12]);
 
 /* Algorithmic HBM bytes moved by the recursion-step launches of the last kpm_moments_ex
  * call: 3 D R s per single step (read a_n, read a_{n-1}, write

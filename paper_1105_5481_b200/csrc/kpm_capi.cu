@@ -114,6 +114,7 @@ struct Plan {
     // two steps per launch (temporal blocking, 2D), see kpm_tma2.cuh; needs 4 vector blocks
     bool use_tma2 = false, no_fused = false;
     size_t tma2_smem = 0;
+    int TX2 = 0, tma2_minb = 1, tma2_grid = 0;  // two-step tile width, CTAs per SM, grid
     size_t lane_bytes = 0;
     size_t ghost_lanes = 0;  // lanes of one ghost plane (row partition), else 0
     size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
@@ -170,10 +171,24 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     p->tma_rr = (h->ndim == 3 && cols >= 4LL * p->tma_grid && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
     p->use_tma = true;
     // two-step kernel: 2D lattices with L0 >= 4, same tiles, shared memory permitting
+    // One CTA per SM with TX*TL = 1024 lanes per row tile (measured on c2: two co-resident
+    // CTAs with half-width tiles were 5% slower).
     p->use_tma2 = false;
-    if (h->ndim == 2 && !p->no_fused && !env_on("KPM_NO_TMA2") && h->L[0] >= 4 && h->L[1] >= 4 && TX * TL == 1024) {
-        p->tma2_smem = kpm::step2_smem_bytes(TX, TL, h->d_eps != nullptr, p->RP);
-        p->use_tma2 = p->tma2_smem <= 227 * 1024;
+    if (h->ndim == 2 && !p->no_fused && !env_on("KPM_NO_TMA2") && h->L[0] >= 4 && h->L[1] >= 4) {
+        const bool on = h->d_eps != nullptr;
+        const int tx1 = 1024 / TL;
+        const size_t sm1 = kpm::step2_smem_bytes(tx1, TL, on, p->RP);
+        const long long Lm2 = h->L[1];
+        if (h->L[0] % tx1 == 0 && sm1 <= 227 * 1024) {
+            p->TX2 = tx1;
+            p->tma2_minb = 1;
+            p->tma2_smem = sm1;
+        }
+        if (p->TX2) {
+            const long long W2 = (long long)(RG / TL) * (h->L[0] / p->TX2) * Lm2;
+            p->tma2_grid = (int)std::min<long long>(W2, (long long)p->tma2_minb * h->num_sms);
+            p->use_tma2 = true;
+        }
     }
 }
 
@@ -200,6 +215,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->gx = (int)std::min<long long>(site_ctas, 2LL * h->num_sms);
     plan_tma(h, flags, p);
     if (p->use_tma) p->gx = p->tma_grid;
+    if (p->use_tma2) p->gx = std::max(p->gx, p->tma2_grid);  // partial rows per slot (max over kernels)
     p->nslots = N;
     if (h->rows) p->use_tma2 = false;  // the two-step kernel needs two-deep halos; not with slabs
     p->ghost_lanes = h->rows ? (size_t)h->plane * p->RG : 0;
@@ -352,6 +368,7 @@ kpm_status make_eps_map(const kpm_handle_s* h, const Plan& p, CUtensorMap* m) {
 struct BufMaps {
     const void* base = nullptr;
     CUtensorMap A, Col, Row, P, Col2;  // main, 1-site column, row, (=main), 2-site column (2D)
+    CUtensorMap A2;                    // main box of the two-step kernel (width TX2)
 };
 
 kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMaps* bm) {
@@ -360,6 +377,7 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     KPM_TRY(make_vec_map(h, p, base, 1, p.TY, 1, &bm->Col));
     KPM_TRY(make_vec_map(h, p, base, p.TX, 1, 1, &bm->Row));
     if (h->ndim == 2) KPM_TRY(make_vec_map(h, p, base, 2, 1, 1, &bm->Col2));
+    if (p.use_tma2) KPM_TRY(make_vec_map(h, p, base, p.TX2, 1, 1, &bm->A2));
     bm->P = bm->A;
     return KPM_OK;
 }
@@ -379,40 +397,40 @@ kpm_status make_eps_map_w(const kpm_handle_s* h, const Plan& p, int bx, CUtensor
     return KPM_OK;
 }
 
-template <int TL, int TX, bool ONSITE, bool PEIERLS>
+template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB>
 kpm_status launch_tma2_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
-    auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS>;
+    auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS, MINB>;
     static size_t configured = 0;
     if (configured < p.tma2_smem) {
         KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma2_smem));
         configured = p.tma2_smem;
     }
-    kern<<<p.tma_grid, kpm::kThreads2, p.tma2_smem, h->stream>>>(A.A, A.Col2, P.P, P.Col, E, E2, g, tail);
+    kern<<<p.tma2_grid, kpm::kThreads2, p.tma2_smem, h->stream>>>(A.A2, A.Col2, P.A2, P.Col, E, E2, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
     return KPM_OK;
 }
 
-template <int TL, int TX>
+template <int TL, int TX, int MINB>
 kpm_status launch_tma2_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
     const bool on = h->d_eps != nullptr;
     if (is_cplx(h)) {
-        if (on) return launch_tma2_t<TL, TX, true, true>(h, p, A, P, E, E2, g, tail);
-        return launch_tma2_t<TL, TX, false, true>(h, p, A, P, E, E2, g, tail);
+        if (on) return launch_tma2_t<TL, TX, true, true, MINB>(h, p, A, P, E, E2, g, tail);
+        return launch_tma2_t<TL, TX, false, true, MINB>(h, p, A, P, E, E2, g, tail);
     }
-    if (on) return launch_tma2_t<TL, TX, true, false>(h, p, A, P, E, E2, g, tail);
-    return launch_tma2_t<TL, TX, false, false>(h, p, A, P, E, E2, g, tail);
+    if (on) return launch_tma2_t<TL, TX, true, false, MINB>(h, p, A, P, E, E2, g, tail);
+    return launch_tma2_t<TL, TX, false, false, MINB>(h, p, A, P, E, E2, g, tail);
 }
 
 // instantiated tile shapes of the two-step kernel (TX * TL = 1024 lanes per row tile)
 kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                        const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
-    if (p.TL == 32 && p.TX == 32) return launch_tma2_s<32, 32>(h, p, A, P, E, E2, g, tail);
-    if (p.TL == 16 && p.TX == 64) return launch_tma2_s<16, 64>(h, p, A, P, E, E2, g, tail);
-    if (p.TL == 8 && p.TX == 128) return launch_tma2_s<8, 128>(h, p, A, P, E, E2, g, tail);
-    return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX);
+    if (p.TL == 32 && p.TX2 == 32) return launch_tma2_s<32, 32, 1>(h, p, A, P, E, E2, g, tail);
+    if (p.TL == 16 && p.TX2 == 64) return launch_tma2_s<16, 64, 1>(h, p, A, P, E, E2, g, tail);
+    if (p.TL == 8 && p.TX2 == 128) return launch_tma2_s<8, 128, 1>(h, p, A, P, E, E2, g, tail);
+    return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX2);
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS>
@@ -533,7 +551,7 @@ struct Run {
     kpm::VecArgs v{};
     BufMaps maps[4];
     int nmaps = 0;
-    CUtensorMap mapE, mapE2;
+    CUtensorMap mapE, mapE2, mapEf;  // eps~: single-step box, 2-site box, two-step main box
     kpm::TmaGeom tg{};
     kpm::Tma2Geom tg2{};
     double2 *cur = nullptr, *prev = nullptr, *spare0 = nullptr, *spare1 = nullptr;
@@ -621,13 +639,17 @@ struct Run {
         nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
         memset(&mapE, 0, sizeof mapE);
         memset(&mapE2, 0, sizeof mapE2);
+        memset(&mapEf, 0, sizeof mapEf);
         if (p.use_tma && nsteps > 0) {
             double2* bufs[4] = {P, C, X2, X3};
             nmaps = p.use_tma2 ? 4 : 2;
             for (int i = 0; i < nmaps; ++i) KPM_TRY(make_buf_maps(h, p, base_of(bufs[i]), &maps[i]));
             if (h->d_eps) {
                 KPM_TRY(make_eps_map(h, p, &mapE));
-                if (p.use_tma2) KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
+                if (p.use_tma2) {
+                    KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
+                    KPM_TRY(make_eps_map_w(h, p, p.TX2, &mapEf));
+                }
             }
             tg.L0 = (int)h->L[0];
             tg.L1 = (int)h->L[1];
@@ -644,17 +666,18 @@ struct Run {
             tg.rr = p.tma_rr;
             tg.ghost = h->rows ? 1 : 0;
             tg.RP = p.RP;
+            tg.rows_total = p.gx;
             tg.t = h->t_scaled;
             tg.shift = -h->b / h->a;
             tg.phase = h->d_phase;
             tg2.L0 = tg.L0;
             tg2.L1 = tg.L1;
-            tg2.TX = p.TX;
+            tg2.TX = p.TX2;
             tg2.TL = p.TL;
             tg2.RG = p.RG;
             tg2.G_L = tg.G_L;
-            tg2.PX = tg.PX;
-            tg2.W = (long long)tg.G_L * tg.PX * tg.L1;
+            tg2.PX = p.TX2 ? (int)(h->L[0] / p.TX2) : 0;
+            tg2.W = (long long)tg.G_L * tg2.PX * tg.L1;
             tg2.RP = p.RP;
             tg2.t = tg.t;
             tg2.shift = tg.shift;
@@ -693,7 +716,7 @@ struct Run {
             tg2.red[4] = tail ? part + (size_t)(2 * n + 4) * slot : nullptr;
             tg2.outB = spare0;
             tg2.outC = spare1;
-            KPM_TRY(launch_tma2(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapE, mapE2, tg2, tail));
+            KPM_TRY(launch_tma2(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapEf, mapE2, tg2, tail));
             double2* oc = cur;
             double2* op = prev;
             cur = spare1;
@@ -1233,7 +1256,7 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
     return KPM_OK;
 }
 
-kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[8]) {
+kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[12]) {
     if (!h || !info) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
     Plan p;
     KPM_TRY(make_plan(h, N, R, flags, false, &p));
@@ -1245,6 +1268,10 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[5] = (int64_t)p.tma_smem;
     info[6] = p.RG;
     info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0);
+    info[8] = p.use_tma2 ? p.TX2 : 0;
+    info[9] = p.use_tma2 ? p.tma2_minb : 0;
+    info[10] = p.use_tma2 ? p.tma2_grid : 0;
+    info[11] = 0;
     return KPM_OK;
 }
 

@@ -110,6 +110,7 @@ struct TmaGeom {
     int Lm;           // march extent (L1 in 2D, L2 in 3D)
     long long W;      // total output planes = G_L * PX * PY * Lm
     int rr;           // 1: round-robin whole columns over CTAs; 0: contiguous plane ranges
+    int rows_total;   // partial-sum rows per moment slot (>= gridDim.x; extra rows are zeroed)
     int ghost;        // 1: row partition -- vector buffers hold Lm + 2 planes (ghost, local..., ghost),
                       //    march neighbours are never wrapped; 0: periodic wrap
     int RP;           // padded vectors (partial row length)
@@ -393,6 +394,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
         double* rowk = k == 0 ? g.red0 : (k == 1 ? g.red1 : (tail ? g.red2 : nullptr));
         if (rowk == nullptr) continue;
         for (int v = threadIdx.x; v < g.RP; v += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + v] = sacc[k * g.RP + v];
+        for (int rr = blockIdx.x + gridDim.x; rr < g.rows_total; rr += gridDim.x)
+            for (int v = threadIdx.x; v < g.RP; v += blockDim.x) rowk[(size_t)rr * g.RP + v] = 0.0;
     }
 }
 

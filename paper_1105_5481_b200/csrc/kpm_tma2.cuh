@@ -106,8 +106,8 @@ struct LoadCursor {
     }
 };
 
-template <int TL, int TX, bool ONSITE, bool PEIERLS>
-__global__ void __launch_bounds__(kThreads2, 1)
+template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB>
+__global__ void __launch_bounds__(kThreads2, MINB)
     kpm_step2_tma_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
                          const __grid_constant__ CUtensorMap mapA2,   // a_n 2-site box {2TL, 2, 1}
                          const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box

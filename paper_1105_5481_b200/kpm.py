@@ -227,9 +227,9 @@ class Handle:
         return ms.value, sl.value, tl.value
 
     def plan_info(self, N, R, flags=0):
-        info = np.zeros(8, dtype=np.int64)
+        info = np.zeros(12, dtype=np.int64)
         _check(_lib.kpm_plan_info(self._h, int(N), int(R), int(flags), _ptr(info)))
-        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "_"]
+        keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "_", "TX2", "ctas_per_sm2", "grid2"]
         d = {k: int(v) for k, v in zip(keys, info) if k != "_"}
         d["round_robin"] = int(info[7] & 1)
         d["two_step"] = int((info[7] >> 1) & 1)
