@@ -100,7 +100,7 @@ def test_tma_march_matches_oracle(kpm, case):
     info = h.plan_info(N, R)
     assert info["tma"] == 1, info
     assert info["round_robin"] == (case == "3d_round_robin"), info
-    assert info["two_step"] == (lat["ndim"] == 2), info
+    assert info["two_step"] == (lat["ndim"] == 2 and lat["L"][0] % (1024 // info["TL"]) == 0), info
     mu = h.moments(N, R, 21)
     assert normwise(mu, ref) < TOL
     pv = h.moments_ex(N, R, 21, flags=kpm.KPM_PER_VECTOR)
@@ -120,7 +120,7 @@ def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
     ref = oracle.moments_doubling(H, a, b, ki.rademacher(5, R, lat["D"]), N)
     h = make(kpm, lat, a, b)
     info = h.plan_info(N, R)
-    assert info["two_step"] == (N // 2 - 1 >= 2)
+    assert info["two_step"] == (N // 2 - 1 >= 2 and lat["L"][0] % (1024 // info["TL"]) == 0)
     mu2 = h.moments(N, R, 5)
     monkeypatch.setenv("KPM_NO_TMA2", "1")
     assert h.plan_info(N, R)["two_step"] == 0
