@@ -175,6 +175,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: all-reduce through host memory; lets several "
+                         "ranks share one GPU to test the multi-rank path)")
     ap.add_argument("--partition", default="vectors", choices=["vectors", "rows"],
                     help="vectors: each rank owns R vectors of its own (weak scaling, one all-reduce); rows: "
                          "the lattice is cut into slabs of the slowest dimension with halo exchange over NCCL "
@@ -196,9 +199,13 @@ def main():
     import torch
     import torch.distributed as dist
     from paper_1105_5481_b200 import kpm
+    local_rank = local_rank % max(torch.cuda.device_count(), 1)  # several ranks may share a GPU (gloo tests)
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group("gloo")
     dev = torch.device("cuda", local_rank)
 
     a, b = kpm.kpm_gershgorin_stencil(lat["ndim"], lat["L"], lat["t"], onsite=lat["onsite"], flux=lat["flux"])
@@ -231,8 +238,14 @@ def main():
             return
         h.moments_ex(N, R, cfg["seed"], flags=kpm.KPM_RAW_SUMS | kpm.KPM_DEVICE_OUT, out=S.data_ptr())
         if world > 1:
-            with torch.cuda.stream(stream):
-                dist.all_reduce(S)
+            if args.dist_backend == "nccl":
+                with torch.cuda.stream(stream):
+                    dist.all_reduce(S)  # the one collective of the vector partition (NCCL, NVLink)
+            else:
+                stream.synchronize()
+                Sh = S.cpu()
+                dist.all_reduce(Sh)
+                S.copy_(Sh)
         h.assemble(S.data_ptr(), N, R, out=mu.data_ptr())
 
     for _ in range(args.warmup):
@@ -257,7 +270,8 @@ def main():
         stream.synchronize()
     torch.cuda.synchronize(dev)
     ms_total = ev0.elapsed_time(ev1)
-    t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+    rdev = dev if (world == 1 or args.dist_backend == "nccl") else torch.device("cpu")
+    t = torch.tensor([ms_total], dtype=torch.float64, device=rdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         dist.barrier()
@@ -290,7 +304,8 @@ def main():
             h2 = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=pinned_onsite,
                                         flux=lat["flux"], device=local_rank, dist=part)
             if world > 1:
-                out = kpm.moments_distributed(h2, N, R, cfg["seed"])
+                out = kpm.moments_distributed(h2, N, R, cfg["seed"],
+                                              device=None if args.dist_backend == "nccl" else torch.device("cpu"))
             else:
                 out = h2.moments(N, R, cfg["seed"])
             h2.close()
@@ -303,7 +318,7 @@ def main():
             e2e_out = e2e_step()
         k = max(1, min(args.steps, 5))
         e2e_ms = (time.perf_counter() - t0) * 1000 / k
-        te = torch.tensor([e2e_ms], dtype=torch.float64, device=dev)
+        te = torch.tensor([e2e_ms], dtype=torch.float64, device=rdev)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_ms = float(te.item())
