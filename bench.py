@@ -163,6 +163,7 @@ def config_obj(args, cfg, lat, world):
             "L": list(lat["L"]), "t": lat["t"], "anderson_W": cfg["W"], "flux": lat["flux"],
             "vector_seed": cfg["seed"], "disorder_seed": cfg["disorder_seed"],
             "parallelism": f"rows{world}" if rows else f"vectors{world}",
+            "H_format": getattr(args, "format", "stencil"),
             "l2": "inputs larger than L2 (2 x D*R*s vector blocks)"}
 
 
@@ -175,6 +176,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--format", default="stencil", choices=["stencil", "csr"],
+                    help="how H reaches the library: lattice-stencil descriptor, or the same H as CSR "
+                         "(kpm_create_csr -> ELL; general sparse path)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: all-reduce through host memory; lets several "
                          "ranks share one GPU to test the multi-rank path)")
@@ -211,8 +215,8 @@ def main():
     a, b = kpm.kpm_gershgorin_stencil(lat["ndim"], lat["L"], lat["t"], onsite=lat["onsite"], flux=lat["flux"])
     N, R_loc = cfg["N"], cfg["R"]
     rows = args.partition == "rows"
-    if rows:
-        args.no_e2e = True  # the slab path's host-output call is already what `value` times
+    if rows or args.format == "csr":
+        args.no_e2e = True  # (e2e below re-creates a stencil handle)
         if world == 1:
             dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
                                     rank=0, world_size=1)
@@ -221,8 +225,14 @@ def main():
     else:
         R = R_loc * world
         part = (kpm.KPM_PART_VECTORS, rank, world)
-    h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
-                               device=local_rank, dist=part)
+    if args.format == "csr":
+        assert not rows, "the row partition is implemented for stencils"
+        rowptr, col, val = ki.lattice_csr(lat)
+        a, b = kpm.kpm_gershgorin_csr(lat["D"], rowptr, col, val)
+        h = kpm.kpm_create_csr(lat["D"], rowptr, col, val, a, b, device=local_rank, dist=part)
+    else:
+        h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
+                                   device=local_rank, dist=part)
     stream = torch.cuda.Stream(device=dev)
     h.set_stream(stream.cuda_stream)
     ws_bytes = h.workspace_size(N, R)
@@ -282,7 +292,9 @@ def main():
     # roofline of the dominant kernel: the fused recursion step
     peak, peak_kind = peak_hbm()
     plan = h.plan_info(N, R)
-    kname = ("kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
+    kname = ("kpm_step_kernel<EllOp> (ELL SpMM over the vector block + recursion + reductions)"
+             if args.format == "csr" else
+             "kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
              else "kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan["tma"]
              else "kpm_step_kernel (fused stencil SpMM + recursion + reductions)")
     avg_step_ms = steps_ms / max(step_launches, 1)

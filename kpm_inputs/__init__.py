@@ -108,3 +108,35 @@ def lattice(cfg: dict, **overrides) -> dict:
     onsite = anderson_onsite(c["disorder_seed"], D, c["W"]) if c.get("W", 0.0) != 0.0 else None
     return dict(ndim=int(c["ndim"]), L=L, D=D, t=float(c["t"]), onsite=onsite,
                 flux=float(c.get("flux", 0.0)))
+
+
+def lattice_csr(lat: dict):
+    """The lattice Hamiltonian of a descriptor as CSR arrays (rowptr int64, col int32, val
+    float64 or complex128), built with numpy for feeding kpm_create_csr.  Input
+    construction only (the same H the stencil descriptor defines: periodic nearest-neighbour
+    bonds t, Peierls phase e^{+i 2 pi phi x} on the y-bond (x,y)->(x,y+1), on-site eps)."""
+    ndim, L = lat["ndim"], tuple(int(v) for v in lat["L"])
+    D = L[0] * L[1] * L[2]
+    idx = np.arange(D, dtype=np.int64)
+    c = [idx % L[0], (idx // L[0]) % L[1], idx // (L[0] * L[1])]
+    cols, vals = [], []
+    flux, t = float(lat.get("flux", 0.0)), float(lat["t"])
+    if lat.get("onsite") is not None:
+        cols.append(idx)
+        vals.append(np.asarray(lat["onsite"], dtype=np.float64).astype(np.complex128))
+    for d in range(ndim):
+        stride = [1, L[0], L[0] * L[1]][d]
+        for s in (+1, -1):
+            nd = (c[d] + s) % L[d]
+            j = idx + (nd - c[d]) * stride
+            # bond (u -> u + e_d) carries H[u+e_d][u] = t e^{i theta(u)}, theta = 2 pi phi x_u on y-bonds
+            theta = 2.0 * np.pi * flux * c[0] if d == 1 else np.zeros(D)
+            h = t * np.exp(-1j * theta) if s == +1 else t * np.exp(1j * theta)
+            cols.append(j)
+            vals.append(h)
+    col = np.stack(cols, axis=1).astype(np.int32)
+    val = np.stack(vals, axis=1)
+    rowptr = np.arange(D + 1, dtype=np.int64) * col.shape[1]
+    if flux == 0.0:
+        val = val.real.copy()
+    return rowptr, col.ravel(), val.ravel()

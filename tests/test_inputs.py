@@ -43,3 +43,21 @@ def test_configs_match_baseline_json():
     assert (ki.num_sites(c["c3"]["L"]), c["c3"]["N"], c["c3"]["R"]) == (2097152, 2048, 128)
     assert (ki.num_sites(c["c4"]["L"]), c["c4"]["N"], c["c4"]["R"]) == (1048576, 4096, 256)
     assert (ki.num_sites(c["c5"]["L"]), c["c5"]["N"], c["c5"]["R"]) == (134217728, 1024, 32)
+
+
+def test_lattice_csr_input_equals_oracle_matrix():
+    """kpm_inputs.lattice_csr (the CSR fed to kpm_create_csr in bench.py) is the same H the
+    oracle builds (oracle O1, itself pinned in test_oracle_pins.py)."""
+    import oracle
+    cases = [dict(ndim=2, L=(16, 8, 1), t=-1.0, onsite=None, flux=0.125),
+             dict(ndim=3, L=(5, 4, 3), t=-1.3, onsite=ki.anderson_onsite(1, 60, 2.0), flux=0.0),
+             dict(ndim=1, L=(7, 1, 1), t=-1.0, onsite=None, flux=0.0),
+             dict(ndim=2, L=(2, 6, 1), t=-0.5, onsite=ki.anderson_onsite(2, 12, 1.0), flux=0.5)]
+    for lat in cases:
+        rp, col, val = ki.lattice_csr(lat)
+        D = rp.size - 1
+        Hd = np.zeros((D, D), dtype=complex)
+        for i in range(D):
+            for k in range(rp[i], rp[i + 1]):
+                Hd[i, col[k]] += val[k]
+        assert np.array_equal(Hd, oracle.lattice_csr(lat).dense())
