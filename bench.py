@@ -216,7 +216,8 @@ def main():
     N, R_loc = cfg["N"], cfg["R"]
     rows = args.partition == "rows"
     if rows or args.format == "csr":
-        args.no_e2e = True  # (e2e below re-creates a stencil handle)
+        args.no_e2e = True  # (e2e below re-creates a plain stencil handle)
+    if rows:
         if world == 1:
             dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
                                     rank=0, world_size=1)

@@ -109,15 +109,25 @@ struct EllOp {
     template <class XF>
     __device__ __forceinline__ double2 apply(int s, const XF& X, double2 xs) const {
         double2 h = scale2(shift, xs);
-        for (int k = 0; k < K; ++k) {
-            const size_t e = (size_t)k * D + s;
-            const int j = __ldg(col + e);
-            if (CPLX) {
-                const double2 v = __ldg(reinterpret_cast<const double2*>(val) + e);
-                h = add2(h, cmul(v, X(j)));
-            } else {
-                h = fma2(__ldg(val + e), X(j), h);
+        // chunks of 8 entries: all column indices and values first, then all gathers, then the
+        // sums -- 8 independent loads in flight instead of a load->gather->fma chain per entry
+        constexpr int CH = 8;
+        for (int k0 = 0; k0 < K; k0 += CH) {
+            int j[CH];
+            double2 v[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) {
+                const int k = k0 + u;
+                const size_t e = (size_t)(k < K ? k : K - 1) * D + s;
+                j[u] = __ldg(col + e);
+                v[u] = CPLX ? __ldg(reinterpret_cast<const double2*>(val) + e) : make_double2(__ldg(val + e), 0.0);
+                if (k >= K) v[u] = make_double2(0.0, 0.0);
             }
+            double2 xj[CH];
+#pragma unroll
+            for (int u = 0; u < CH; ++u) xj[u] = X(j[u]);
+#pragma unroll
+            for (int u = 0; u < CH; ++u) h = CPLX ? add2(h, cmul(v[u], xj[u])) : fma2(v[u].x, xj[u], h);
         }
         return h;
     }
