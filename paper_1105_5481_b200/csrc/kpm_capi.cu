@@ -23,6 +23,7 @@
 #include "kpm_kernels.cuh"
 #include "kpm_tma.cuh"
 #include "kpm_tma2.cuh"
+#include "kpm_ell.cuh"
 
 namespace {
 
@@ -295,9 +296,29 @@ kpm::StencilGeom stencil_geom(const kpm_handle_s* h) {
     return g;
 }
 
+// ELL recursion step with cp.async-prefetched row entries (kpm_ell.cuh).
+template <bool CPLX>
+kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail) {
+    dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
+    const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX);
+    auto kern = kpm::kpm_ell_step_kernel<CPLX>;
+    static size_t configured = 0;
+    if (configured < smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        configured = smem;
+    }
+    const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a};
+    kern<<<grid, block, smem, h->stream>>>(op, v, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
 // Dispatch on the operator type of the handle.
 kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& v, int tail) {
     using namespace kpm;
+    if (h->kind == KIND_ELL && mode == STEP && h->K > 0 && h->K <= kEllKMax && !env_on("KPM_ELL_GENERIC"))
+        return is_cplx(h) ? launch_ell_t<true>(h, p, v, tail) : launch_ell_t<false>(h, p, v, tail);
     if (h->kind == KIND_ELL) {
         if (is_cplx(h)) return launch_mode<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, mode, v, tail);
         return launch_mode<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, mode, v, tail);
