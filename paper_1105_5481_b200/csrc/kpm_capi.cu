@@ -24,6 +24,7 @@
 #include "kpm_tma.cuh"
 #include "kpm_tma2.cuh"
 #include "kpm_ell.cuh"
+#include "kpm_small.cuh"
 
 namespace {
 
@@ -116,6 +117,9 @@ struct Plan {
     bool use_tma2 = false, no_fused = false;
     size_t tma2_smem = 0;
     int TX2 = 0, tma2_minb = 1, tma2_grid = 0;  // two-step tile width, CTAs per SM, grid
+    // whole recursion in one launch with the vector blocks in shared memory (kpm_small.cuh)
+    bool use_small = false;
+    size_t small_smem = 0;
     size_t lane_bytes = 0;
     size_t ghost_lanes = 0;  // lanes of one ghost plane (row partition), else 0
     size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
@@ -216,6 +220,13 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->gx = (int)std::min<long long>(site_ctas, 2LL * h->num_sms);
     plan_tma(h, flags, p);
     if (p->use_tma) p->gx = p->tma_grid;
+    p->small_smem = 2 * (size_t)h->D * p->TR * sizeof(double2);
+    p->use_small = !h->rows && !(flags & KPM_DIRECT) && p->small_smem <= kpm::kSmallSmemMax && !env_on("KPM_NO_SMALL");
+    if (p->use_small) {
+        p->use_tma = p->use_tma2 = false;
+        p->TS = kpm::kSmallThreads / p->TR;
+        p->gx = p->TS;  // partial-sum rows per slot = thread rows of the single CTA
+    }
     if (p->use_tma2) p->gx = std::max(p->gx, p->tma2_grid);  // partial rows per slot (max over kernels)
     p->nslots = N;
     if (h->rows) p->use_tma2 = false;  // the two-step kernel needs two-deep halos; not with slabs
@@ -312,6 +323,43 @@ kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, i
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
     return KPM_OK;
+}
+
+template <bool CPLX, class OP>
+kpm_status launch_small_t(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int from_buf, int N,
+                          double* part) {
+    auto kern = kpm::kpm_small_kernel<OP, CPLX>;
+    static size_t configured = 0;
+    if (configured < p.small_smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.small_smem));
+        configured = p.small_smem;
+    }
+    kern<<<dim3(1, p.gy), dim3(p.TR, p.TS), p.small_smem, h->stream>>>(op, v, from_buf, N, part);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
+kpm_status launch_small(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int from_buf, int N, double* part) {
+    using namespace kpm;
+    if (h->kind == KIND_ELL) {
+        if (is_cplx(h)) return launch_small_t<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, v, from_buf, N, part);
+        return launch_small_t<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, v, from_buf, N, part);
+    }
+    const StencilGeom g = stencil_geom(h);
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_small_t<true>(h, p, StencilOp<2, true, true>{g}, v, from_buf, N, part);
+        return launch_small_t<true>(h, p, StencilOp<2, false, true>{g}, v, from_buf, N, part);
+    }
+    switch (h->ndim * 2 + (on ? 1 : 0)) {
+        case 2: return launch_small_t<false>(h, p, StencilOp<1, false, false>{g}, v, from_buf, N, part);
+        case 3: return launch_small_t<false>(h, p, StencilOp<1, true, false>{g}, v, from_buf, N, part);
+        case 4: return launch_small_t<false>(h, p, StencilOp<2, false, false>{g}, v, from_buf, N, part);
+        case 5: return launch_small_t<false>(h, p, StencilOp<2, true, false>{g}, v, from_buf, N, part);
+        case 6: return launch_small_t<false>(h, p, StencilOp<3, false, false>{g}, v, from_buf, N, part);
+        default: return launch_small_t<false>(h, p, StencilOp<3, true, false>{g}, v, from_buf, N, part);
+    }
 }
 
 // Dispatch on the operator type of the handle.
@@ -648,6 +696,14 @@ struct Run {
             first_mode = kpm::FIRST_BUF;
         }
         if (first_mode == kpm::FIRST_BUF && h->rows) KPM_TRY(need_exchange(P));
+        if (p.use_small) {  // the whole recursion in one launch (kpm_small.cuh)
+            KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
+            KPM_TRY(launch_small(h, p, v, first_mode == kpm::FIRST_BUF, N, part));
+            h->step_launches = 1;
+            nsteps = 0;
+            n = 1;
+            return KPM_OK;
+        }
         // First step: a_0, a_1 = H~ a_0; S_0 = <a_0|a_0>, S_1 = <a_0|a_1> (Eq 17, 19).
         v.red0 = part;
         v.red1 = N > 1 ? part + slot : nullptr;

@@ -2,6 +2,8 @@
 seeded inputs.  Bar (X17): normwise max_n |mu_gpu - mu_orc| <= 1e-10 *
 max_n |mu_orc|; bitwise for config c1 (every a_n is integer-valued, Q4) and for the
 Rademacher generator (integer work)."""
+import os
+
 import numpy as np
 import pytest
 
@@ -52,9 +54,14 @@ CASES = {
 }
 
 
+@pytest.mark.parametrize("path", ["default", "no_small"])
 @pytest.mark.parametrize("form", ["stencil", "csr"])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_moments_match_oracle(kpm, case, form):
+def test_moments_match_oracle(kpm, case, form, path, monkeypatch):
+    """default: these sizes run the single-launch shared-memory path (kpm_small.cuh);
+    no_small: the per-step launch path (first-step + generic/ELL step kernels)."""
+    if path == "no_small":
+        monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat, N, R = CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -88,7 +95,8 @@ TMA_CASES = {
 
 
 @pytest.mark.parametrize("case", sorted(TMA_CASES))
-def test_tma_march_matches_oracle(kpm, case):
+def test_tma_march_matches_oracle(kpm, case, monkeypatch):
+    monkeypatch.setenv("KPM_NO_SMALL", "1")  # some of these fit the single-launch smem path
     lat, N, R = TMA_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -114,6 +122,7 @@ def test_tma_march_matches_oracle(kpm, case):
 def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
     """2D: the two-step kernel (temporal blocking) and the single-step kernel give the oracle's
     moments for every parity of the step count and of N (odd-N tail inside a pair)."""
+    monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat, _, R = TMA_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -152,9 +161,12 @@ def test_c1_bitwise(kpm):
     assert mu[0] == 1.0
 
 
+@pytest.mark.parametrize("path", ["default", "no_small"])
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8, 9])
 @pytest.mark.parametrize("R", [1, 2, 3])
-def test_small_N_and_R_edges(kpm, N, R):
+def test_small_N_and_R_edges(kpm, N, R, path, monkeypatch):
+    if path == "no_small":
+        monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat = lat_of(2, (9, 7), W=1.0)
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -293,9 +305,11 @@ def test_randomized_shapes_sweep(kpm):
         R = int(rng.choice([1, 3, 8, 16, 32, 64]))
         N = int(rng.integers(1, 40))
         lat = lat_of(ndim, L, W=W, flux=flux, dseed=trial)
+        os.environ["KPM_NO_SMALL"] = "1" if trial % 2 else "0"  # both launch paths
         H = oracle.lattice_csr(lat)
         a, b = oracle.gershgorin(H)
         a *= 1.0 + 0.1 * rng.random()
         ref = oracle.moments_doubling(H, a, b, ki.rademacher(trial, R, lat["D"]), N)
         mu = make(kpm, lat, a, b).moments(N, R, trial)
         assert normwise(mu, ref) < TOL, (trial, ndim, L, flux, W, R, N)
+    os.environ.pop("KPM_NO_SMALL", None)
