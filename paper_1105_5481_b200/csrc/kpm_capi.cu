@@ -122,6 +122,8 @@ struct Plan {
     size_t small_smem = 0;
     size_t lane_bytes = 0;
     size_t ghost_lanes = 0;  // lanes of one ghost plane (row partition), else 0
+    int xpad = 0;            // 3D stencils: x-row frame of periodic images (row pitch L0 + 2 xpad)
+    size_t mem_sites = 0;    // memory sites of the local block (with frames, without ghost planes)
     size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
            total = 0;
 };
@@ -230,8 +232,13 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->use_tma2) p->gx = std::max(p->gx, p->tma2_grid);  // partial rows per slot (max over kernels)
     p->nslots = N;
     if (h->rows) p->use_tma2 = false;  // the two-step kernel needs two-deep halos; not with slabs
-    p->ghost_lanes = h->rows ? (size_t)h->plane * p->RG : 0;
-    p->lane_bytes = ((size_t)h->D * p->RG + 2 * p->ghost_lanes) * sizeof(double2);
+    p->xpad = (h->kind == KIND_STENCIL && h->ndim == 3) ? 2 : 0;
+    const size_t rows_of_x = (size_t)(h->D / h->L[0]);
+    p->mem_sites = (size_t)h->D + 2 * (size_t)p->xpad * rows_of_x;
+    const size_t plane_mem = !h->rows ? 0
+                             : p->xpad ? (size_t)(h->plane / h->L[0]) * (h->L[0] + 2 * p->xpad) : (size_t)h->plane;
+    p->ghost_lanes = plane_mem * p->RG;
+    p->lane_bytes = (p->mem_sites * p->RG + 2 * p->ghost_lanes) * sizeof(double2);
     size_t off = 0;
     p->off_P = off; off = align_up(off + p->lane_bytes);
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
@@ -409,7 +416,9 @@ kpm_status make_vec_map(const kpm_handle_s* h, const Plan& p, void* base, int bx
     const int rank = h->ndim + 1;
     cuuint64_t dims[4] = {(cuuint64_t)2 * p.RG, (cuuint64_t)h->L[0], (cuuint64_t)h->L[1], (cuuint64_t)h->L[2]};
     if (h->rows) dims[1 + h->slow] += 2;  // ghost planes
-    cuuint64_t strides[3] = {(cuuint64_t)p.RG * 16, (cuuint64_t)p.RG * 16 * h->L[0], (cuuint64_t)p.RG * 16 * h->L[0] * h->L[1]};
+    if (p.xpad) dims[1] += 2 * p.xpad;    // x-row frames (3D)
+    cuuint64_t pitch = (cuuint64_t)h->L[0] + 2 * p.xpad;
+    cuuint64_t strides[3] = {(cuuint64_t)p.RG * 16, (cuuint64_t)p.RG * 16 * pitch, (cuuint64_t)p.RG * 16 * pitch * h->L[1]};
     cuuint32_t box[4] = {(cuuint32_t)(2 * p.TL), (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     if (h->ndim == 2) box[2] = 1;
     cuuint32_t es[4] = {1, 1, 1, 1};
@@ -678,6 +687,8 @@ struct Run {
         v.D_total = h->D_total;
         v.i_off = h->rows ? h->z0 * h->plane : 0;
         v.ghost = h->rows ? 1 : 0;
+        v.L0 = (int)h->L[0];
+        v.xpad = p.xpad;
 
         // a_0: generated in the first-step kernel, or the caller's block staged through C.
         int first_mode = kpm::FIRST_GEN;
@@ -688,11 +699,11 @@ struct Run {
                                      (flags & KPM_DEVICE_IN) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
             const long long ne = h->D * (long long)p.RG;
             const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
-            if (cplx) kpm::load_r0_kernel<true><<<blocks, 256, 0, h->stream>>>(stage, P, (int)h->D, p.RG, p.R_loc);
-            else kpm::load_r0_kernel<false><<<blocks, 256, 0, h->stream>>>(stage, P, (int)h->D, p.RG, p.R_loc);
+            if (cplx) kpm::load_r0_kernel<true><<<blocks, 256, 0, h->stream>>>(stage, P, v);
+            else kpm::load_r0_kernel<false><<<blocks, 256, 0, h->stream>>>(stage, P, v);
             KPM_CUDA(cudaGetLastError());
             h->total_launches++;
-            if (direct) KPM_CUDA(cudaMemcpyAsync(Rb, P, (size_t)h->D * p.RG * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
+            if (direct) KPM_CUDA(cudaMemcpyAsync(Rb, P, p.mem_sites * p.RG * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
             first_mode = kpm::FIRST_BUF;
         }
         if (first_mode == kpm::FIRST_BUF && h->rows) KPM_TRY(need_exchange(P));
@@ -744,6 +755,7 @@ struct Run {
             tg.ghost = h->rows ? 1 : 0;
             tg.RP = p.RP;
             tg.rows_total = p.gx;
+            tg.xpad = p.xpad;
             tg.t = h->t_scaled;
             tg.shift = -h->b / h->a;
             tg.phase = h->d_phase;

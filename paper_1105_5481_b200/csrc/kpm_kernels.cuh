@@ -149,10 +149,36 @@ struct VecArgs {
     long long D_total;     // global number of sites (RNG counter stride)
     long long i_off;       // global index of this GPU's site 0
     int ghost;             // row partition: site indices j < 0 or >= D are ghost sites (wrap globally)
+    int L0;                // x extent
+    int xpad;              // 3D lattices: 2 -- vector blocks store each x-row with a 2-site frame of
+                           // periodic images on both sides (row pitch L0 + 4); 0 otherwise
+    // memory site of lattice site j (j may index a ghost plane, i.e. be < 0 or >= D)
+    __device__ __forceinline__ long long mem(long long j) const {
+        if (!xpad) return j;
+        const long long row = j >= 0 ? j / L0 : -((-j + L0 - 1) / L0);
+        return j + 2 * xpad * row + xpad;
+    }
     double* red0;          // partial sums of moment slot 0: [gridDim.x][RP] (nullable)
     double* red1;          // slot 1
     double* red2;          // slot 2 (odd-N tail <a_{n+1}|a_{n+1}>)
 };
+
+// Store the lane of lattice site s (memory site ms), plus its periodic x images in the frame
+// when s is within xpad sites of an x boundary (both images when L0 < 2 xpad).
+__device__ __forceinline__ void store_site(const VecArgs& v, double2* buf, int s, long long ms, int rg, double2 val,
+                                           bool streaming) {
+    auto st = [&](long long m) {
+        double2* p = buf + m * v.RG + rg;
+        if (streaming) __stcs(p, val);
+        else *p = val;
+    };
+    st(ms);
+    if (v.xpad) {
+        const int x = s % v.L0;
+        if (x < v.xpad) st(ms + v.L0);
+        if (x >= v.L0 - v.xpad) st(ms - v.L0);
+    }
+}
 
 template <bool CPLX>
 __device__ __forceinline__ double2 gen_lane(const VecArgs& v, int j, int rg) {
@@ -183,31 +209,32 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
     double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0;
     if (active) {
         for (int s = blockIdx.x * TS + threadIdx.y; s < v.D; s += gridDim.x * TS) {
-            const size_t idx = (size_t)s * v.RG + rg;
+            const long long ms = v.mem(s);
+            const size_t idx = (size_t)ms * v.RG + rg;
             if (MODE == FIRST_GEN) {
                 auto X = [&](int j) { return gen_lane<CPLX>(v, j, rg); };
                 const double2 x = X(s);
                 const double2 y = op.apply(s, X, x);   // a_1 = H~ a_0   (Eq 17)
-                v.P[idx] = x;
-                v.C[idx] = y;
+                store_site(v, v.P, s, ms, rg, x, false);
+                store_site(v, v.C, s, ms, rg, y, false);
                 dot_acc<CPLX>(acc0, x, x);
                 dot_acc<CPLX>(acc1, x, y);
                 if (tail) dot_acc<CPLX>(acc2, y, y);
             } else if (MODE == FIRST_BUF) {
-                auto X = [&](int j) { return __ldg(v.P + (size_t)j * v.RG + rg); };
+                auto X = [&](int j) { return __ldg(v.P + (size_t)v.mem(j) * v.RG + rg); };
                 const double2 x = X(s);
                 const double2 y = op.apply(s, X, x);
-                v.C[idx] = y;
+                store_site(v, v.C, s, ms, rg, y, false);
                 dot_acc<CPLX>(acc0, x, x);
                 dot_acc<CPLX>(acc1, x, y);
                 if (tail) dot_acc<CPLX>(acc2, y, y);
             } else {
-                auto X = [&](int j) { return __ldg(v.C + (size_t)j * v.RG + rg); };
+                auto X = [&](int j) { return __ldg(v.C + (size_t)v.mem(j) * v.RG + rg); };
                 const double2 x = X(s);
                 const double2 h = op.apply(s, X, x);
                 const double2 p = __ldcs(v.P + idx);
                 const double2 y = make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));  // Eq 18
-                __stcs(v.P + idx, y);
+                store_site(v, v.P, s, ms, rg, y, true);
                 if (MODE == STEP) {
                     dot_acc<CPLX>(acc0, x, x);
                     dot_acc<CPLX>(acc1, x, y);
@@ -247,10 +274,11 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
 }
 
 // ------------------------------------------------------------ helpers
-// Caller start vectors, vector-major [R_loc][D] real -> lane layout [D][RG].
+// Caller start vectors, vector-major [R_loc][D] real -> lane layout [D][RG] (memory sites of v).
 template <bool CPLX>
-__global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restrict__ out, int D, int RG,
-                               long long R_loc) {
+__global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restrict__ out, const VecArgs v) {
+    const int D = v.D, RG = v.RG;
+    const long long R_loc = v.R_loc;
     const long long n = (long long)D * RG;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const int s = (int)(e / RG), rg = (int)(e % RG);
@@ -261,7 +289,7 @@ __global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restric
             const long long r = 2LL * rg;
             val = make_double2(r < R_loc ? r0[(size_t)r * D + s] : 0.0, r + 1 < R_loc ? r0[(size_t)(r + 1) * D + s] : 0.0);
         }
-        out[e] = val;
+        store_site(v, out, s, v.mem(s), rg, val, false);
     }
 }
 

@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1)
     double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0;
     if (active) {
         for (int s = threadIdx.y; s < v.D; s += TS) {
-            const double2 x = first_from_buf ? v.P[(size_t)s * v.RG + rg] : gen_lane<CPLX>(v, s, rg);
+            const double2 x = first_from_buf ? v.P[(size_t)v.mem(s) * v.RG + rg] : gen_lane<CPLX>(v, s, rg);
             bufA[(size_t)s * TR + l] = x;
         }
     }

@@ -111,6 +111,7 @@ struct TmaGeom {
     long long W;      // total output planes = G_L * PX * PY * Lm
     int rr;           // 1: round-robin whole columns over CTAs; 0: contiguous plane ranges
     int rows_total;   // partial-sum rows per moment slot (>= gridDim.x; extra rows are zeroed)
+    int xpad;         // 3D: x-rows of the vector blocks carry a frame of xpad periodic images per side
     int ghost;        // 1: row partition -- vector buffers hold Lm + 2 planes (ghost, local..., ghost),
                       //    march neighbours are never wrapped; 0: periodic wrap
     int RP;           // padded vectors (partial row length)
@@ -245,7 +246,10 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             while (next_seg(g, sq, s)) {
                 const int c0 = 2 * s.lg * g.TL;
                 const int x0 = s.px * g.TX, y0 = s.py * g.TY;
-                const int xl = (x0 - 1 + g.L0) % g.L0, xr = (x0 + g.TX) % g.L0;
+                // padded x-rows (3D): the halo columns are the frame, never wrapped
+                const int xm = x0 + g.xpad;
+                const int xl = g.xpad ? xm - 1 : (x0 - 1 + g.L0) % g.L0;
+                const int xr = g.xpad ? xm + g.TX : (x0 + g.TX) % g.L0;
                 const int yt = (y0 - 1 + g.L1) % g.L1, yb = (y0 + g.TY) % g.L1;
                 const int H = s.m1 - s.m0;
                 for (int q = 0; q < H + 2; ++q) {
@@ -261,11 +265,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         tma_load(dst + SL.right_off, &mapCol, fullA + slot, c0, xr, m);
                         if (ONSITE) tma_load_2d(dst + SL.eps_off, &mapE, fullA + slot, x0, m - g.ghost);
                     } else {
-                        tma_load(dst + SL.main_off, &mapA, fullA + slot, c0, x0, y0, m);
+                        tma_load(dst + SL.main_off, &mapA, fullA + slot, c0, xm, y0, m);
                         tma_load(dst + SL.left_off, &mapCol, fullA + slot, c0, xl, y0, m);
                         tma_load(dst + SL.right_off, &mapCol, fullA + slot, c0, xr, y0, m);
-                        tma_load(dst + SL.top_off, &mapRow, fullA + slot, c0, x0, yt, m);
-                        tma_load(dst + SL.bot_off, &mapRow, fullA + slot, c0, x0, yb, m);
+                        tma_load(dst + SL.top_off, &mapRow, fullA + slot, c0, xm, yt, m);
+                        tma_load(dst + SL.bot_off, &mapRow, fullA + slot, c0, xm, yb, m);
                         if (ONSITE) tma_load(dst + SL.eps_off, &mapE, fullA + slot, x0, y0, m - g.ghost);
                     }
                     ++ia;
@@ -276,7 +280,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         if (ip >= kSP) mbar_wait(emptyP + ps, (uint32_t)(((ip / kSP) - 1) & 1));
                         mbar_expect_tx(fullP + ps, tile_bytes);
                         if (NDIM == 2) tma_load_hint(ringP + ps * tile_bytes, &mapP, fullP + ps, c0, x0, mp, pol_first);
-                        else tma_load_hint(ringP + ps * tile_bytes, &mapP, fullP + ps, c0, x0, y0, mp, pol_first);
+                        else tma_load_hint(ringP + ps * tile_bytes, &mapP, fullP + ps, c0, xm, y0, mp, pol_first);
                         ++ip;
                     }
                 }
@@ -364,9 +368,15 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     const double2 h = fma2(e, x, scale2(g.t, nb));
                     const double2 p = Pv[k * g.TL + l];
                     const double2 y = make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));  // Eq (18)
-                    const long long site = NDIM == 2 ? (long long)m * g.L0 + (x0 + lx)
-                                                     : ((long long)m * g.L1 + (y0 + ly)) * g.L0 + (x0 + lx);
-                    __stcs(g.out + site * g.RG + s.lg * g.TL + l, y);
+                    const int xs = x0 + lx;
+                    const long long site = NDIM == 2 ? (long long)m * g.L0 + xs
+                                                     : ((long long)m * g.L1 + (y0 + ly)) * (g.L0 + 2 * g.xpad) + xs + g.xpad;
+                    double2* o = g.out + site * g.RG + s.lg * g.TL + l;
+                    __stcs(o, y);
+                    if (NDIM == 3 && g.xpad) {  // periodic x images in the frame
+                        if (xs < g.xpad) __stcs(o + (long long)g.L0 * g.RG, y);
+                        if (xs >= g.L0 - g.xpad) __stcs(o - (long long)g.L0 * g.RG, y);
+                    }
                     dot_acc<PEIERLS>(acc0, x, x);
                     dot_acc<PEIERLS>(acc1, x, y);
                     if (tail) dot_acc<PEIERLS>(acc2, y, y);
