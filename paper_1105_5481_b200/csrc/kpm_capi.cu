@@ -23,6 +23,7 @@
 #include "kpm_kernels.cuh"
 #include "kpm_tma.cuh"
 #include "kpm_tma2.cuh"
+#include "kpm_tmak.cuh"
 #include "kpm_ell.cuh"
 #include "kpm_small.cuh"
 
@@ -117,6 +118,10 @@ struct Plan {
     bool use_tma2 = false, no_fused = false;
     size_t tma2_smem = 0;
     int TX2 = 0, tma2_minb = 1, tma2_grid = 0;  // two-step tile width, CTAs per SM, grid
+    // KS steps per launch (deep temporal blocking, 2D), see kpm_tmak.cuh; needs 4 vector blocks
+    bool use_tmak = false;
+    int KSK = 0, TLK = 0, TXK = 0, NPIK = 0, tmak_grid = 0;
+    size_t tmak_smem = 0;
     // whole recursion in one launch with the vector blocks in shared memory (kpm_small.cuh)
     bool use_small = false;
     size_t small_smem = 0;
@@ -135,6 +140,18 @@ bool env_on(const char* name) {
     return e && e[0] && e[0] != '0';
 }
 bool tma_disabled() { return env_on("KPM_NO_TMA"); }
+int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+
+// Shared memory of the instantiated KS-step kernels (0 = not instantiated).
+size_t stepk_smem(int ks, int tl, int npi, bool onsite, int RP) {
+    if (ks == 4 && tl == 16 && npi == 2) return kpm::stepk_smem_bytes<4, 16, 32, 2>(onsite, RP);
+    if (ks == 4 && tl == 16 && npi == 1) return kpm::stepk_smem_bytes<4, 16, 32, 1>(onsite, RP);
+    if (ks == 4 && tl == 8 && npi == 2) return kpm::stepk_smem_bytes<4, 8, 64, 2>(onsite, RP);
+    return 0;
+}
 
 // Tile choice for the TMA march: ~16 KB main tiles (TX*TY*TL = 1024 lanes), full passes
 // of the 256 consumer threads, tiles dividing the lattice, lane groups dividing RG.
@@ -197,6 +214,26 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
             p->use_tma2 = true;
         }
     }
+    // KS-step kernel: 2D lattices, row tiles of TXK * TLK = 512 lanes (kpm_tmak.cuh)
+    p->use_tmak = false;
+    const int ks = env_on("KPM_NO_TMAK") ? 0 : env_int("KPM_TMAK_KS", 4);
+    if (h->ndim == 2 && !p->no_fused && ks >= 2) {
+        const bool on = h->d_eps != nullptr;
+        const int tlk = RG % 16 == 0 ? 16 : (RG % 8 == 0 ? 8 : 0);
+        const int npi = env_int("KPM_TMAK_NPI", 2);
+        const int txk = tlk ? 512 / tlk : 0;
+        const size_t sm = tlk ? stepk_smem(ks, tlk, npi, on, p->RP) : 0;
+        if (sm && h->L[0] % txk == 0 && h->L[0] >= ks && sm <= 227 * 1024) {
+            p->KSK = ks;
+            p->TLK = tlk;
+            p->TXK = txk;
+            p->NPIK = npi;
+            p->tmak_smem = sm;
+            const long long WK = (long long)(RG / tlk) * (h->L[0] / txk) * h->L[1];
+            p->tmak_grid = (int)std::min<long long>(WK, (long long)h->num_sms);
+            p->use_tmak = true;
+        }
+    }
 }
 
 kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p,
@@ -230,8 +267,10 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
         p->gx = p->TS;  // partial-sum rows per slot = thread rows of the single CTA
     }
     if (p->use_tma2) p->gx = std::max(p->gx, p->tma2_grid);  // partial rows per slot (max over kernels)
+    if (p->use_tmak) p->gx = std::max(p->gx, p->tmak_grid);
     p->nslots = N;
-    if (h->rows) p->use_tma2 = false;  // the two-step kernel needs two-deep halos; not with slabs
+    if (h->rows) p->use_tma2 = p->use_tmak = false;  // multi-step kernels need deep halos; not with slabs
+    if (p->use_tmak && p->M - 1 < p->KSK) p->use_tmak = false;
     p->xpad = (h->kind == KIND_STENCIL && h->ndim == 3) ? 2 : 0;
     const size_t rows_of_x = (size_t)(h->D / h->L[0]);
     p->mem_sites = (size_t)h->D + 2 * (size_t)p->xpad * rows_of_x;
@@ -244,11 +283,10 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
     p->off_R = off;
     if ((flags & KPM_DIRECT) && with_r0) off = align_up(off + p->lane_bytes);
-    if (p->use_tma2 && p->M - 1 >= 2) {
+    if (p->use_tma2 && p->M - 1 < 2) p->use_tma2 = false;
+    if (p->use_tma2 || p->use_tmak) {  // out-of-place multi-step launches: two spare blocks
         p->off_X2 = off; off = align_up(off + p->lane_bytes);
         p->off_X3 = off; off = align_up(off + p->lane_bytes);
-    } else {
-        p->use_tma2 = false;
     }
     p->off_part = off; off = align_up(off + (size_t)N * p->gx * p->RP * sizeof(double));
     p->off_Sv = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
@@ -410,7 +448,8 @@ EncodeFn get_encode() {
 
 // Tensor map over the lane-layout vector block viewed as doubles [L2][L1][L0][2 RG]
 // (rank 3 in 2D, 4 in 3D) with the given box.
-kpm_status make_vec_map(const kpm_handle_s* h, const Plan& p, void* base, int bx, int by, int bz, CUtensorMap* m) {
+kpm_status make_vec_map(const kpm_handle_s* h, const Plan& p, void* base, int bx, int by, int bz, CUtensorMap* m,
+                        int tl = 0) {
     EncodeFn enc = get_encode();
     if (!enc) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const int rank = h->ndim + 1;
@@ -419,7 +458,7 @@ kpm_status make_vec_map(const kpm_handle_s* h, const Plan& p, void* base, int bx
     if (p.xpad) dims[1] += 2 * p.xpad;    // x-row frames (3D)
     cuuint64_t pitch = (cuuint64_t)h->L[0] + 2 * p.xpad;
     cuuint64_t strides[3] = {(cuuint64_t)p.RG * 16, (cuuint64_t)p.RG * 16 * pitch, (cuuint64_t)p.RG * 16 * pitch * h->L[1]};
-    cuuint32_t box[4] = {(cuuint32_t)(2 * p.TL), (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
+    cuuint32_t box[4] = {(cuuint32_t)(2 * (tl ? tl : p.TL)), (cuuint32_t)bx, (cuuint32_t)by, (cuuint32_t)bz};
     if (h->ndim == 2) box[2] = 1;
     cuuint32_t es[4] = {1, 1, 1, 1};
     CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -447,6 +486,7 @@ struct BufMaps {
     const void* base = nullptr;
     CUtensorMap A, Col, Row, P, Col2;  // main, 1-site column, row, (=main), 2-site column (2D)
     CUtensorMap A2;                    // main box of the two-step kernel (width TX2)
+    CUtensorMap AK, AKH, AKH1;         // KS-step kernel: main (TXK), KS-site and (KS-1)-site boxes, TLK lanes
 };
 
 kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMaps* bm) {
@@ -456,6 +496,11 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     KPM_TRY(make_vec_map(h, p, base, p.TX, 1, 1, &bm->Row));
     if (h->ndim == 2) KPM_TRY(make_vec_map(h, p, base, 2, 1, 1, &bm->Col2));
     if (p.use_tma2) KPM_TRY(make_vec_map(h, p, base, p.TX2, 1, 1, &bm->A2));
+    if (p.use_tmak) {
+        KPM_TRY(make_vec_map(h, p, base, p.TXK, 1, 1, &bm->AK, p.TLK));
+        KPM_TRY(make_vec_map(h, p, base, p.KSK, 1, 1, &bm->AKH, p.TLK));
+        KPM_TRY(make_vec_map(h, p, base, p.KSK - 1, 1, 1, &bm->AKH1, p.TLK));
+    }
     bm->P = bm->A;
     return KPM_OK;
 }
@@ -509,6 +554,43 @@ kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     if (p.TL == 16 && p.TX2 == 64) return launch_tma2_s<16, 64, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 8 && p.TX2 == 128) return launch_tma2_s<8, 128, 1>(h, p, A, P, E, E2, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX2);
+}
+
+template <int KS, int TL, int TX, int NPI, bool ONSITE, bool PEIERLS>
+kpm_status launch_tmak_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                         const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
+    auto kern = kpm::kpm_stepk_tma_kernel<KS, TL, TX, NPI, ONSITE, PEIERLS>;
+    static size_t configured = 0;
+    if (configured < p.tmak_smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tmak_smem));
+        configured = p.tmak_smem;
+    }
+    kern<<<p.tmak_grid, kpm::StepKThreads<KS, TL, TX, NPI>::NT, p.tmak_smem, h->stream>>>(A.AK, A.AKH, P.AK, P.AKH1, E, EH,
+                                                                                          g, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
+template <int KS, int TL, int TX, int NPI>
+kpm_status launch_tmak_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                         const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_tmak_t<KS, TL, TX, NPI, true, true>(h, p, A, P, E, EH, g, tail);
+        return launch_tmak_t<KS, TL, TX, NPI, false, true>(h, p, A, P, E, EH, g, tail);
+    }
+    if (on) return launch_tmak_t<KS, TL, TX, NPI, true, false>(h, p, A, P, E, EH, g, tail);
+    return launch_tmak_t<KS, TL, TX, NPI, false, false>(h, p, A, P, E, EH, g, tail);
+}
+
+// instantiated shapes of the KS-step kernel (see stepk_smem)
+kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                       const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
+    if (p.KSK == 4 && p.TLK == 16 && p.NPIK == 2) return launch_tmak_s<4, 16, 32, 2>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 4 && p.TLK == 16 && p.NPIK == 1) return launch_tmak_s<4, 16, 32, 1>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 4 && p.TLK == 8 && p.NPIK == 2) return launch_tmak_s<4, 8, 64, 2>(h, p, A, P, E, EH, g, tail);
+    return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d NPI=%d", p.KSK, p.TLK, p.NPIK);
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS>
@@ -630,8 +712,10 @@ struct Run {
     BufMaps maps[4];
     int nmaps = 0;
     CUtensorMap mapE, mapE2, mapEf;  // eps~: single-step box, 2-site box, two-step main box
+    CUtensorMap mapEK, mapEKH;       // eps~: KS-step main box (TXK), KS-site box
     kpm::TmaGeom tg{};
     kpm::Tma2Geom tg2{};
+    kpm::TmaKGeom tgk{};
     double2 *cur = nullptr, *prev = nullptr, *spare0 = nullptr, *spare1 = nullptr;
     int n = 1, nsteps = 0;
     double vbytes = 0, ebytes = 0, mbytes = 0;
@@ -728,15 +812,21 @@ struct Run {
         memset(&mapE, 0, sizeof mapE);
         memset(&mapE2, 0, sizeof mapE2);
         memset(&mapEf, 0, sizeof mapEf);
+        memset(&mapEK, 0, sizeof mapEK);
+        memset(&mapEKH, 0, sizeof mapEKH);
         if (p.use_tma && nsteps > 0) {
             double2* bufs[4] = {P, C, X2, X3};
-            nmaps = p.use_tma2 ? 4 : 2;
+            nmaps = (p.use_tma2 || p.use_tmak) ? 4 : 2;
             for (int i = 0; i < nmaps; ++i) KPM_TRY(make_buf_maps(h, p, base_of(bufs[i]), &maps[i]));
             if (h->d_eps) {
                 KPM_TRY(make_eps_map(h, p, &mapE));
                 if (p.use_tma2) {
                     KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
                     KPM_TRY(make_eps_map_w(h, p, p.TX2, &mapEf));
+                }
+                if (p.use_tmak) {
+                    KPM_TRY(make_eps_map_w(h, p, p.TXK, &mapEK));
+                    KPM_TRY(make_eps_map_w(h, p, p.KSK, &mapEKH));
                 }
             }
             tg.L0 = (int)h->L[0];
@@ -771,6 +861,20 @@ struct Run {
             tg2.t = tg.t;
             tg2.shift = tg.shift;
             tg2.phase = tg.phase;
+            tgk.L0 = tg.L0;
+            tgk.L1 = tg.L1;
+            tgk.TX = p.TXK;
+            tgk.TL = p.TLK;
+            tgk.RG = p.RG;
+            tgk.G_L = p.TLK ? p.RG / p.TLK : 0;
+            tgk.PX = p.TXK ? (int)(h->L[0] / p.TXK) : 0;
+            tgk.W = (long long)tgk.G_L * tgk.PX * tg.L1;
+            tgk.RP = p.RP;
+            tgk.t = tg.t;
+            tgk.shift = tg.shift;
+            tgk.phase = tg.phase;
+            tgk.slot_stride = (long long)slot;
+            tgk.rows_total = p.gx;
         }
         cur = C;
         prev = P;
@@ -797,6 +901,25 @@ struct Run {
     double2* fresh() const { return cur; }
 
     kpm_status launch_next() {
+        if (!direct && p.use_tmak && n + p.KSK - 1 <= nsteps) {
+            // steps n .. n+KS-1: slots 2n .. 2n+2KS-1 (+ odd-N tail 2(n+KS))
+            const int KS = p.KSK;
+            const bool tail = (N & 1) && n + KS - 1 == nsteps;
+            tgk.red = part + (size_t)(2 * n) * slot;
+            tgk.outB = spare0;
+            tgk.outC = spare1;
+            KPM_TRY(launch_tmak(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapEK, mapEKH, tgk, tail));
+            double2* oc = cur;
+            double2* op = prev;
+            cur = spare1;
+            prev = spare0;
+            spare0 = oc;
+            spare1 = op;
+            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->step_launches++;
+            n += KS;
+            return KPM_OK;
+        }
         const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1));
         if (pair) {
             // steps n and n+1: slots 2n .. 2n+3 (+ odd-N tail 2n+4)
@@ -1360,7 +1483,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[8] = p.use_tma2 ? p.TX2 : 0;
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;
-    info[11] = 0;
+    info[11] = p.use_tmak ? p.KSK : 0;
     return KPM_OK;
 }
 

@@ -83,7 +83,8 @@ struct LoadCursor {
     long long w, w_end;
     int lg, px, m0, H, q, nq;
     bool valid;
-    __device__ void seg(const Tma2Geom& g, int extra) {
+    template <class G>
+    __device__ void seg(const G& g, int extra) {
         valid = w < w_end;
         if (!valid) return;
         const long long col = w / g.L1;
@@ -96,12 +97,14 @@ struct LoadCursor {
         q = 0;
         nq = H + extra;
     }
-    __device__ void init(const Tma2Geom& g, long long b, long long e, int extra) {
+    template <class G>
+    __device__ void init(const G& g, long long b, long long e, int extra) {
         w = b;
         w_end = e;
         seg(g, extra);
     }
-    __device__ void next(const Tma2Geom& g, int extra) {
+    template <class G>
+    __device__ void next(const G& g, int extra) {
         if (++q >= nq) seg(g, extra);
     }
 };

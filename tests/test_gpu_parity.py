@@ -137,6 +137,47 @@ def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
     assert normwise(mu2, ref) < TOL and normwise(mu1, ref) < TOL
 
 
+KSTEP_CASES = {
+    "2d_R64": (lat_of(2, (64, 200)), 64),                        # segments cross pencil columns
+    "2d_anderson_R16": (lat_of(2, (128, 24), W=2.0), 16),        # 8 lanes per site: TL 8, TX 64
+    "2d_peierls_R32": (lat_of(2, (64, 16), flux=1 / 8), 32),
+    "2d_peierls_anderson_R16": (lat_of(2, (32, 30), flux=1 / 4, W=1.0), 16),
+    "2d_one_row_per_cta": (lat_of(2, (32, 4)), 32),              # 8 output rows -> 8 CTAs, H = 1
+    "2d_L1_2": (lat_of(2, (64, 2), W=1.0), 48),                  # rows wrap around several times
+    "2d_R96_two_groups": (lat_of(2, (96, 40)), 96),              # 3 pencils x 3 lane groups
+}
+
+
+@pytest.mark.parametrize("case", sorted(KSTEP_CASES))
+@pytest.mark.parametrize("N", [10, 11, 12, 13, 16, 19, 26])
+def test_four_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
+    """2D: the KS = 4 deep temporal-blocking kernel (kpm_tmak.cuh) mixed with two-step and
+    single-step launches for the remainder, every parity of N (odd-N tail in the last launch)."""
+    monkeypatch.setenv("KPM_NO_SMALL", "1")
+    lat, R = KSTEP_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b -= 0.02 * a
+    a *= 1.03
+    r = ki.rademacher(13, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b)
+    info = h.plan_info(N, R)
+    assert info["ks"] == 4, info
+    mu = h.moments(N, R, 13)
+    assert normwise(mu, ref) < TOL
+    pv = h.moments_ex(N, R, 13, flags=kpm.KPM_PER_VECTOR)
+    assert normwise(pv, ref_pv) < TOL
+    assert np.array_equal(h.moments(N, R, 13), mu), "not deterministic"
+    _, launches, _ = h.last_timing()
+    M = N // 2
+    rem = (M - 1) % 4
+    assert launches == (M - 1) // 4 + (rem // 2 + rem % 2 if info["two_step"] else rem), (launches, info)
+    monkeypatch.setenv("KPM_NO_TMAK", "1")
+    assert h.plan_info(N, R)["ks"] == 0
+    assert normwise(h.moments(N, R, 13), ref) < TOL
+
+
 @pytest.mark.parametrize("case", ["2d", "3d_anderson", "peierls"])
 def test_direct_mode_matches_oracle_direct(kpm, case):
     """KPM_DIRECT: the paper's own estimator, Eq (19): mu_n = <r|a_n>, N-1 products."""
