@@ -104,7 +104,8 @@ def profiled_traffic(config, plan):
         rec = json.load(open(p))[config]
     except Exception:
         return None
-    want = "step2" if plan.get("two_step") else ("step_tma" if plan["tma"] else "kpm_step_kernel")
+    want = ("stepk" if plan.get("ks") else "step2" if plan.get("two_step")
+            else ("step_tma" if plan["tma"] else "kpm_step_kernel"))
     if want not in rec.get("kernel", ""):
         return None  # the committed capture is of another kernel: no traffic claim
     return rec["dram_bytes_per_launch"]
@@ -295,7 +296,9 @@ def main():
     plan = h.plan_info(N, R)
     kname = ("kpm_step_kernel<EllOp> (ELL SpMM over the vector block + recursion + reductions)"
              if args.format == "csr" else
-             "kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
+             f"kpm_stepk_tma_kernel ({plan['ks']} recursion steps per HBM pass, TMA-fed march; remainder steps "
+             "by the two-/single-step kernels, included)" if plan.get("ks")
+             else "kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
              else "kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan["tma"]
              else "kpm_step_kernel (fused stencil SpMM + recursion + reductions)")
     avg_step_ms = steps_ms / max(step_launches, 1)

@@ -148,7 +148,7 @@ int env_int(const char* name, int dflt) {
 // Shared memory of the instantiated KS-step kernels (0 = not instantiated).
 size_t stepk_smem(int ks, int tl, int npi, bool onsite, int RP) {
     if (ks == 4 && tl == 16 && npi == 2) return kpm::stepk_smem_bytes<4, 16, 32, 2>(onsite, RP);
-    if (ks == 4 && tl == 16 && npi == 1) return kpm::stepk_smem_bytes<4, 16, 32, 1>(onsite, RP);
+    if (ks == 2 && tl == 16 && npi == 2) return kpm::stepk_smem_bytes<2, 16, 32, 2>(onsite, RP);
     if (ks == 4 && tl == 8 && npi == 2) return kpm::stepk_smem_bytes<4, 8, 64, 2>(onsite, RP);
     return 0;
 }
@@ -588,7 +588,7 @@ kpm_status launch_tmak_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const
 kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                        const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
     if (p.KSK == 4 && p.TLK == 16 && p.NPIK == 2) return launch_tmak_s<4, 16, 32, 2>(h, p, A, P, E, EH, g, tail);
-    if (p.KSK == 4 && p.TLK == 16 && p.NPIK == 1) return launch_tmak_s<4, 16, 32, 1>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 2 && p.TLK == 16 && p.NPIK == 2) return launch_tmak_s<2, 16, 32, 2>(h, p, A, P, E, EH, g, tail);
     if (p.KSK == 4 && p.TLK == 8 && p.NPIK == 2) return launch_tmak_s<4, 8, 64, 2>(h, p, A, P, E, EH, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d NPI=%d", p.KSK, p.TLK, p.NPIK);
 }
@@ -858,6 +858,7 @@ struct Run {
             tg2.PX = p.TX2 ? (int)(h->L[0] / p.TX2) : 0;
             tg2.W = (long long)tg.G_L * tg2.PX * tg.L1;
             tg2.RP = p.RP;
+            tg2.rows_total = p.gx;
             tg2.t = tg.t;
             tg2.shift = tg.shift;
             tg2.phase = tg.phase;

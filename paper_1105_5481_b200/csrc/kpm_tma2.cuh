@@ -39,6 +39,7 @@ struct Tma2Geom {
     int TX, TL, RG, G_L, PX;
     long long W;         // output rows = G_L * PX * L1
     int RP;
+    int rows_total;      // partial-sum rows per slot (>= gridDim.x; extra rows are zeroed)
     double t, shift;
     const double2* phase;
     double* red[5];      // slots 2n, 2n+1, 2n+2, 2n+3, (tail) 2n+4; red[4] nullable
@@ -358,6 +359,8 @@ __global__ void __launch_bounds__(kThreads2, MINB)
         double* rowk = g.red[k];
         if (rowk == nullptr || (k == 4 && !tail)) continue;
         for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + v] = sacc[k * g.RP + v];
+        for (int rr = blockIdx.x + gridDim.x; rr < g.rows_total; rr += gridDim.x)
+            for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)rr * g.RP + v] = 0.0;
     }
 }
 

@@ -21,9 +21,10 @@
 // after that barrier (the barrier is the "slot empty" signal, an mbarrier transaction
 // count the "slot full" one).
 //
-// Threads: NI = TX*TL/NPI interior threads own NPI interior columns each (they also store
-// the outputs and accumulate the inner products); NH = 2(KS-1)*TL halo threads own the
-// 2(KS-1) halo columns (column at distance d outside the tile computes levels 1..KS-d).
+// Threads: NI = TX*TL/2 interior threads own two interior columns each (they also store
+// the outputs and accumulate the inner products); NH = (KS-1)*TL halo threads own one left
+// and one right halo column each (a column at distance d outside the tile computes levels
+// 1..KS-d).
 //
 // Reductions (doubling identities, north_star): level j contributes <a_{n+j-1}|a_{n+j-1}>
 // (moment slot 2(n+j-1)) and <a_{n+j-1}|a_{n+j}> (slot 2(n+j-1)+1) over owned sites; the
@@ -73,8 +74,9 @@ struct SlotKLayout {
 
 template <int KS, int TL, int TX, int NPI>
 struct StepKThreads {
+    static_assert(NPI == 2, "two columns per thread (the halo threads own a left and a right column)");
     static constexpr int NI = TX * TL / NPI;
-    static constexpr int NH = 2 * (KS - 1) * TL;
+    static constexpr int NH = (KS - 1) * TL;
     static constexpr int NT = NI + NH;
 };
 
@@ -175,25 +177,26 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
     for (int i = t; i < NACC * g.RP; i += blockDim.x) sacc[i] = 0.0;
     __syncthreads();
 
-    // ---- this thread's columns
+    // ---- this thread's columns: interior threads own columns t/TL and t/TL + KSTEP; halo thread
+    // hc owns the left column -(KS-1)+hc and the right column TX+hc, which compute levels
+    // 1..top (top = KS - distance outside the tile).  All levels are evaluated every row
+    // (straight-line code; the two columns are independent chains the scheduler interleaves);
+    // results outside a column's range or before a level's first row are never stored.
     const bool interior = t < NI;
-    const int l = interior ? t % TL : (t - NI) % TL;
+    const int l = (interior ? t : t - NI) % TL;
     const int lo = l * 16;
-    int lxs[NPI];  // tile x of each owned column
-    int depth;     // halo columns: distance outside the tile (1..KS-1); interior: 0
+    int lxs[2], top[2];
     if (interior) {
-#pragma unroll
-        for (int p = 0; p < NPI; ++p) lxs[p] = t / TL + p * KSTEP;
-        depth = 0;
+        lxs[0] = t / TL;
+        lxs[1] = t / TL + KSTEP;
+        top[0] = top[1] = KS;
     } else {
-        const int hc = (t - NI) / TL;  // 0 .. 2(KS-1)-1
-        const int lx = hc < KS - 1 ? hc - (KS - 1) : TX + (hc - (KS - 1));
-#pragma unroll
-        for (int p = 0; p < NPI; ++p) lxs[p] = lx;
-        depth = lx < 0 ? -lx : lx - TX + 1;
+        const int hc = (t - NI) / TL;
+        lxs[0] = hc - (KS - 1);
+        lxs[1] = TX + hc;
+        top[0] = hc + 1;
+        top[1] = KS - 1 - hc;
     }
-    const int npc = interior ? NPI : 1;  // columns this thread computes
-    const int top = KS - depth;          // highest level this thread computes
 
     double2 acc[NACC];
 #pragma unroll
@@ -236,15 +239,18 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
         const int lg = cs.lg, m0 = cs.m0, H = cs.H, x0 = cs.px * TX;
         if (cur_lg != -1 && lg != cur_lg) flush(cur_lg);
         cur_lg = lg;
-        const long long growstep = (long long)g.L0 * g.RG;
-        const long long colbase = (long long)lg * TL + l;
-        // per column: levels 0..KS-1 at three rows (m2 = two rows back, m1, c = this row), eps~
-        double2 vm2[NPI][KS], vm1[NPI][KS], vc[NPI][KS];
-        double es[NPI][KS];
-        double2 ph[NPI];
+        // per column: levels 0..KS-1 at three rows (m2 = two rows back, m1 = one row back,
+        // c = this row), eps~ of the rows of levels 2..KS, Peierls phase, output pointer
+        double2 vm2[2][KS], vm1[2][KS], vc[2][KS];
+        double es[2][KS];
+        double2 ph[2];
+        long long ocol[2];
 #pragma unroll
-        for (int p = 0; p < NPI; ++p)
+        for (int p = 0; p < 2; ++p) {
             ph[p] = PEIERLS ? __ldg(g.phase + (x0 + lxs[p] + g.L0) % g.L0) : make_double2(0.0, 0.0);
+            ocol[p] = (long long)(x0 + lxs[p]) * g.RG + (long long)lg * TL + l;
+        }
+        const long long growstep = (long long)g.L0 * g.RG;
         const int ia_seg = ia;
         const int NQ = H + 2 * KS - 2;
         int s1 = (ia_seg + 1) % kSAK;  // slot of a_n row r
@@ -255,6 +261,13 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
             if (q == 0) {
                 mbar_wait(fullA + ia_seg % kSAK, (uint32_t)((ia_seg / kSAK) & 1));
                 mbar_wait(fullA + s1, (uint32_t)(((ia_seg + 1) / kSAK) & 1));
+                const unsigned char* A0 = ringA + (ia_seg % kSAK) * A_BYTES;
+                const unsigned char* A1 = ringA + s1 * A_BYTES;
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    vm2[p][0] = ld(A0 + (lxs[p] + KS) * SITE + lo);
+                    vm1[p][0] = ld(A1 + (lxs[p] + KS) * SITE + lo);
+                }
             }
             mbar_wait(fullA + s2, (uint32_t)(((ia_seg + q + 2) / kSAK) & 1));
             mbar_wait(fullP + ps, (uint32_t)((ip / kSPK) & 1));
@@ -262,55 +275,55 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
             const unsigned char* A2 = ringA + s2 * A_BYTES;  // a_n row r+1
             const unsigned char* Pq = ringP + ps * SL::P_BYTES;
             const int wslot = q & 1, rslot = wslot ^ 1;
+            double e1[2];
 #pragma unroll
-            for (int p = 0; p < NPI; ++p) {
-                if (p >= npc) break;
+            for (int p = 0; p < 2; ++p) {
                 const int lx = lxs[p];
-                if (q == 0) {
-                    const unsigned char* A0 = ringA + (ia_seg % kSAK) * A_BYTES;
-                    vm2[p][0] = ld(A0 + (lx + KS) * SITE + lo);
-                    vm1[p][0] = ld(A1 + (lx + KS) * SITE + lo);
-                }
                 vc[p][0] = ld(A2 + (lx + KS) * SITE + lo);
-                double e1 = g.shift;
-                if (ONSITE) {
-                    const double* eb = reinterpret_cast<const double*>(
+                e1[p] = g.shift;
+                if (ONSITE)
+                    e1[p] = *reinterpret_cast<const double*>(
                         A1 + (lx < 0 ? SL::EPS_L + (lx + KS) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8)));
-                    e1 = *eb;
-                }
+            }
 #pragma unroll
-                for (int j = 1; j <= KS; ++j) {
-                    if (j > top || q < 2 * (j - 1)) break;
-                    const int row = r - (j - 1);
-                    double2 xm, xp;
+            for (int j = 1; j <= KS; ++j) {
+                const int row = r - (j - 1);
+                const bool owned = interior && row >= m0 && row < m0 + H;
+#pragma unroll
+                for (int p = 0; p < 2; ++p) {
+                    const int lx = lxs[p];
+                    double2 xm, xp, minus;
                     if (j == 1) {
                         xm = ld(A1 + (lx + KS - 1) * SITE + lo);
                         xp = ld(A1 + (lx + KS + 1) * SITE + lo);
+                        minus = ld(Pq + (lx + KS - 1) * SITE + lo);
                     } else {
                         const unsigned char* Lr = ringL + SL::lev_off(j - 1) + rslot * SL::lev_row(j - 1);
-                        xm = ld(Lr + (lx + KS - (j - 1) - 1) * SITE + lo);
-                        xp = ld(Lr + (lx + KS - (j - 1) + 1) * SITE + lo);
+                        xm = ld(Lr + (lx + KS - j) * SITE + lo);
+                        xp = ld(Lr + (lx + KS - j + 2) * SITE + lo);
+                        minus = vm2[p][j >= 2 ? j - 2 : 0];
                     }
-                    const double2 minus = j == 1 ? ld(Pq + (lx + KS - 1) * SITE + lo) : vm2[p][j - 2 < 0 ? 0 : j - 2];
-                    const double e = ONSITE ? (j == 1 ? e1 : es[p][j - 2 < 0 ? 0 : j - 2]) : g.shift;
+                    const double e = ONSITE ? (j == 1 ? e1[p] : es[p][j >= 2 ? j - 2 : 0]) : g.shift;
                     const double2 x = vm1[p][j - 1];
                     const double2 y = step_val(x, xm, xp, vm2[p][j - 1], vc[p][j - 1], e, ph[p], minus);
                     if (j < KS) {
-                        unsigned char* Lw = ringL + SL::lev_off(j) + wslot * SL::lev_row(j);
-                        *reinterpret_cast<double2*>(Lw + (lx + KS - j) * SITE + lo) = y;
+                        if (j <= top[p]) {
+                            unsigned char* Lw = ringL + SL::lev_off(j) + wslot * SL::lev_row(j);
+                            *reinterpret_cast<double2*>(Lw + (lx + KS - j) * SITE + lo) = y;
+                        }
                         vc[p][j] = y;
                     }
-                    if (interior && row >= m0 && row < m0 + H) {
-                        if (j >= KS - 1) {
-                            double2* o = (j == KS ? g.outC : g.outB) + row * growstep + (long long)(x0 + lx) * g.RG + colbase;
-                            __stcs(o, y);
-                        }
+                    if (owned) {
+                        if (j >= KS - 1) __stcs((j == KS ? g.outC : g.outB) + ocol[p] + row * growstep, y);
                         dot_acc<PEIERLS>(acc[2 * (j - 1)], x, x);
                         dot_acc<PEIERLS>(acc[2 * (j - 1) + 1], x, y);
                         if (j == KS && tail) dot_acc<PEIERLS>(acc[2 * KS], y, y);
                     }
                 }
-                // roll one row down
+            }
+            // roll one row down
+#pragma unroll
+            for (int p = 0; p < 2; ++p) {
 #pragma unroll
                 for (int j = 0; j < KS; ++j) {
                     vm2[p][j] = vm1[p][j];
@@ -319,7 +332,7 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
                 if (ONSITE) {
 #pragma unroll
                     for (int j = KS - 1; j > 0; --j) es[p][j] = es[p][j - 1];
-                    es[p][0] = e1;
+                    es[p][0] = e1[p];
                 }
             }
             __syncthreads();  // row done: a_n row r (and at q == 0 row r-1) and a_{n-1} row r are free
