@@ -120,7 +120,7 @@ struct Plan {
     int TX2 = 0, tma2_minb = 1, tma2_grid = 0;  // two-step tile width, CTAs per SM, grid
     // KS steps per launch (deep temporal blocking, 2D), see kpm_tmak.cuh; needs 4 vector blocks
     bool use_tmak = false;
-    int KSK = 0, TLK = 0, TXK = 0, NPIK = 0, tmak_grid = 0;
+    int KSK = 0, TLK = 0, TXK = 0, tmak_grid = 0;
     size_t tmak_smem = 0;
     // whole recursion in one launch with the vector blocks in shared memory (kpm_small.cuh)
     bool use_small = false;
@@ -146,10 +146,11 @@ int env_int(const char* name, int dflt) {
 }
 
 // Shared memory of the instantiated KS-step kernels (0 = not instantiated).
-size_t stepk_smem(int ks, int tl, int npi, bool onsite, int RP) {
-    if (ks == 4 && tl == 16 && npi == 2) return kpm::stepk_smem_bytes<4, 16, 32, 2>(onsite, RP);
-    if (ks == 2 && tl == 16 && npi == 2) return kpm::stepk_smem_bytes<2, 16, 32, 2>(onsite, RP);
-    if (ks == 4 && tl == 8 && npi == 2) return kpm::stepk_smem_bytes<4, 8, 64, 2>(onsite, RP);
+size_t stepk_smem(int ks, int tl, bool onsite, int RP) {
+    using namespace kpm;
+    if (ks == 4 && tl == 16) return onsite ? stepk_smem_bytes<4, 16, 32, true>(RP) : stepk_smem_bytes<4, 16, 32, false>(RP);
+    if (ks == 4 && tl == 8) return onsite ? stepk_smem_bytes<4, 8, 64, true>(RP) : stepk_smem_bytes<4, 8, 64, false>(RP);
+    if (ks == 2 && tl == 16) return onsite ? stepk_smem_bytes<2, 16, 32, true>(RP) : stepk_smem_bytes<2, 16, 32, false>(RP);
     return 0;
 }
 
@@ -220,14 +221,12 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     if (h->ndim == 2 && !p->no_fused && ks >= 2) {
         const bool on = h->d_eps != nullptr;
         const int tlk = RG % 16 == 0 ? 16 : (RG % 8 == 0 ? 8 : 0);
-        const int npi = env_int("KPM_TMAK_NPI", 2);
         const int txk = tlk ? 512 / tlk : 0;
-        const size_t sm = tlk ? stepk_smem(ks, tlk, npi, on, p->RP) : 0;
+        const size_t sm = tlk ? stepk_smem(ks, tlk, on, p->RP) : 0;
         if (sm && h->L[0] % txk == 0 && h->L[0] >= ks && sm <= 227 * 1024) {
             p->KSK = ks;
             p->TLK = tlk;
             p->TXK = txk;
-            p->NPIK = npi;
             p->tmak_smem = sm;
             const long long WK = (long long)(RG / tlk) * (h->L[0] / txk) * h->L[1];
             p->tmak_grid = (int)std::min<long long>(WK, (long long)h->num_sms);
@@ -556,41 +555,41 @@ kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX2);
 }
 
-template <int KS, int TL, int TX, int NPI, bool ONSITE, bool PEIERLS>
+template <int KS, int TL, int TX, bool ONSITE, bool PEIERLS>
 kpm_status launch_tmak_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
-    auto kern = kpm::kpm_stepk_tma_kernel<KS, TL, TX, NPI, ONSITE, PEIERLS>;
+    auto kern = kpm::kpm_stepk_tma_kernel<KS, TL, TX, ONSITE, PEIERLS>;
     static size_t configured = 0;
     if (configured < p.tmak_smem) {
         KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tmak_smem));
         configured = p.tmak_smem;
     }
-    kern<<<p.tmak_grid, kpm::StepKThreads<KS, TL, TX, NPI>::NT, p.tmak_smem, h->stream>>>(A.AK, A.AKH, P.AK, P.AKH1, E, EH,
-                                                                                          g, tail);
+    kern<<<p.tmak_grid, kpm::StepKThreads<KS, TL, TX>::NT, p.tmak_smem, h->stream>>>(A.AK, A.AKH, P.AK, P.AKH1, E, EH, g,
+                                                                                     tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
     return KPM_OK;
 }
 
-template <int KS, int TL, int TX, int NPI>
+template <int KS, int TL, int TX>
 kpm_status launch_tmak_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
     const bool on = h->d_eps != nullptr;
     if (is_cplx(h)) {
-        if (on) return launch_tmak_t<KS, TL, TX, NPI, true, true>(h, p, A, P, E, EH, g, tail);
-        return launch_tmak_t<KS, TL, TX, NPI, false, true>(h, p, A, P, E, EH, g, tail);
+        if (on) return launch_tmak_t<KS, TL, TX, true, true>(h, p, A, P, E, EH, g, tail);
+        return launch_tmak_t<KS, TL, TX, false, true>(h, p, A, P, E, EH, g, tail);
     }
-    if (on) return launch_tmak_t<KS, TL, TX, NPI, true, false>(h, p, A, P, E, EH, g, tail);
-    return launch_tmak_t<KS, TL, TX, NPI, false, false>(h, p, A, P, E, EH, g, tail);
+    if (on) return launch_tmak_t<KS, TL, TX, true, false>(h, p, A, P, E, EH, g, tail);
+    return launch_tmak_t<KS, TL, TX, false, false>(h, p, A, P, E, EH, g, tail);
 }
 
 // instantiated shapes of the KS-step kernel (see stepk_smem)
 kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                        const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
-    if (p.KSK == 4 && p.TLK == 16 && p.NPIK == 2) return launch_tmak_s<4, 16, 32, 2>(h, p, A, P, E, EH, g, tail);
-    if (p.KSK == 2 && p.TLK == 16 && p.NPIK == 2) return launch_tmak_s<2, 16, 32, 2>(h, p, A, P, E, EH, g, tail);
-    if (p.KSK == 4 && p.TLK == 8 && p.NPIK == 2) return launch_tmak_s<4, 8, 64, 2>(h, p, A, P, E, EH, g, tail);
-    return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d NPI=%d", p.KSK, p.TLK, p.NPIK);
+    if (p.KSK == 4 && p.TLK == 16) return launch_tmak_s<4, 16, 32>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 4 && p.TLK == 8) return launch_tmak_s<4, 8, 64>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 2 && p.TLK == 16) return launch_tmak_s<2, 16, 32>(h, p, A, P, E, EH, g, tail);
+    return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d", p.KSK, p.TLK);
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS>

@@ -3,28 +3,27 @@
 // One launch advances the recursion (Eq 18) by KS steps,
 //     a_{n+j} = 2 H~ a_{n+j-1} - a_{n+j-2},   j = 1 .. KS,
 // reading a_n and a_{n-1} from HBM once and writing only a_{n+KS-1} and a_{n+KS}:
-// 4 D R s bytes per KS steps (KS = 2 is kpm_tma2.cuh's case).
+// 4 D R s bytes per KS steps (kpm_tma2.cuh is the KS = 2 case).
 // The intermediate blocks a_{n+1} .. a_{n+KS-2} never leave the SM.
 //
 // Geometry.  A CTA marches a pencil of TX sites x TL lanes over y (rows).  "Level" j is
-// the block a_{n+j}: level 0 = a_n and level -1 = a_{n-1} come from TMA, levels 1..KS are
-// computed.  In the iteration for row r, level j is computed at row r - (j-1) (one row
-// behind the level below it), on the tile x range widened by KS - j halo sites per side
-// (halo sites are recomputed, not exchanged):
-//     level j at row r-j+1 needs level j-1 at rows r-j, r-j+1, r-j+2 (x) and at row r-j+1
-//     (x-1, x+1), and level j-2 at row r-j+1 (x).
-// Every tile column (x, all TL lanes) is owned by ONE thread for all levels, so the rows a
-// column needs of its own x come from registers (three rows per level, rolled), and only
-// the x-neighbours (row r-j+1 of level j-1, computed in the previous iteration) come from
-// shared memory: each level 1..KS-1 writes its row into a 2-slot ring.  One CTA barrier
-// per row; the TMA refills of the slots a row released are issued by one thread right
-// after that barrier (the barrier is the "slot empty" signal, an mbarrier transaction
-// count the "slot full" one).
+// the block a_{n+j}: level 0 = a_n and level -1 = a_{n-1} arrive by TMA, levels 1..KS are
+// computed, each on the tile widened by KS - j halo sites per side (halo sites are
+// recomputed, not exchanged).  In iteration q a new a_n row enters and level j computes
+// the row two rows behind the newest row of level j-1:
+//     level j at row y needs level j-1 at rows y-1, y, y+1 (own x), at row y (x-1, x+1),
+//     and level j-2 at row y (own x)
+// -- all produced in EARLIER iterations, so the KS levels of an iteration are independent
+// (KS x 2 columns of instruction-level parallelism per thread; a one-row lag would chain
+// them).  Every tile column (x, TL lanes) is owned by one thread for all levels: the rows
+// of its own x come from registers (rolled), the x-neighbours and the level j-2 term come
+// from per-level shared-memory row rings.  One CTA barrier per iteration; right after it
+// one thread refills the released TMA slots (the barrier is the "slot empty" signal, an
+// mbarrier transaction count the "slot full" one).
 //
-// Threads: NI = TX*TL/2 interior threads own two interior columns each (they also store
-// the outputs and accumulate the inner products); NH = (KS-1)*TL halo threads own one left
-// and one right halo column each (a column at distance d outside the tile computes levels
-// 1..KS-d).
+// Threads: NI = TX*TL/2 interior threads own two interior columns each (they also store the
+// outputs and accumulate the inner products); NH = (KS-1)*TL halo threads own one left and
+// one right halo column (a column at distance d outside the tile computes levels 1..KS-d).
 //
 // Reductions (doubling identities, north_star): level j contributes <a_{n+j-1}|a_{n+j-1}>
 // (moment slot 2(n+j-1)) and <a_{n+j-1}|a_{n+j}> (slot 2(n+j-1)+1) over owned sites; the
@@ -48,10 +47,10 @@ struct TmaKGeom {
     double2* outC;       // a_{n+KS}
 };
 
-constexpr int kSAK = 5;  // a_n ring (rows r, r+1 in use, three in flight)
+constexpr int kSAK = 5;  // a_n ring: rows of loads q-2, q-1, q in use, two in flight
 constexpr int kSPK = 3;  // a_{n-1} ring
 
-template <int KS, int TL, int TX>
+template <int KS, int TL, int TX, bool ONSITE>
 struct SlotKLayout {
     static constexpr int SITE = TL * 16;
     __host__ __device__ static constexpr int round128(int b) { return (b + 127) / 128 * 128; }
@@ -60,36 +59,40 @@ struct SlotKLayout {
     static constexpr int EPS_L = A_VEC;
     static constexpr int EPS_M = EPS_L + 128;
     static constexpr int EPS_R = EPS_M + round128(TX * 8);
-    static constexpr int A_ON = EPS_R + 128;
+    static constexpr int A_BYTES = ONSITE ? EPS_R + 128 : A_VEC;
     static constexpr int P_BYTES = round128((TX + 2 * (KS - 1)) * SITE);
-    // ring of level j (1..KS-1): sites [-(KS-j), TX+KS-j), 2 slots
-    __host__ __device__ static constexpr int lev_row(int j) { return round128((TX + 2 * (KS - j)) * SITE); }
-    __host__ __device__ static constexpr int lev_off(int j) {  // offset of level j's ring from the first ring
+    // level j (1..KS-1) ring: sites [-(KS-j), TX+KS-j) (+ their eps~), lev_slots(j) rows
+    __host__ __device__ static constexpr int lev_sites(int j) { return TX + 2 * (KS - j); }
+    __host__ __device__ static constexpr int lev_eps(int j) { return lev_sites(j) * SITE; }
+    __host__ __device__ static constexpr int lev_row(int j) {
+        return round128(lev_sites(j) * SITE + (ONSITE ? lev_sites(j) * 8 : 0));
+    }
+    // read back 2 iterations later (x-neighbours of level j+1) and 4 later (level j+2's term)
+    __host__ __device__ static constexpr int lev_slots(int j) { return j <= KS - 2 ? 5 : 3; }
+    __host__ __device__ static constexpr int lev_off(int j) {
         int o = 0;
-        for (int i = 1; i < j; ++i) o += 2 * lev_row(i);
+        for (int i = 1; i < j; ++i) o += lev_slots(i) * lev_row(i);
         return o;
     }
     static constexpr int LEV_BYTES = lev_off(KS);
 };
 
-template <int KS, int TL, int TX, int NPI>
+template <int KS, int TL, int TX>
 struct StepKThreads {
-    static_assert(NPI == 2, "two columns per thread (the halo threads own a left and a right column)");
-    static constexpr int NI = TX * TL / NPI;
+    static constexpr int NI = TX * TL / 2;
     static constexpr int NH = (KS - 1) * TL;
     static constexpr int NT = NI + NH;
 };
 
-template <int KS, int TL, int TX, int NPI>
-__host__ __device__ inline size_t stepk_smem_bytes(bool onsite, int RP) {
-    using SL = SlotKLayout<KS, TL, TX>;
-    const size_t a = onsite ? SL::A_ON : SL::A_VEC;
-    return (size_t)kSAK * a + (size_t)kSPK * SL::P_BYTES + (size_t)SL::LEV_BYTES + (2 * KS + 1) * (size_t)RP * 8 +
-           (size_t)StepKThreads<KS, TL, TX, NPI>::NI * 16 + (kSAK + kSPK) * 8 + 64;
+template <int KS, int TL, int TX, bool ONSITE>
+__host__ __device__ inline size_t stepk_smem_bytes(int RP) {
+    using SL = SlotKLayout<KS, TL, TX, ONSITE>;
+    return (size_t)kSAK * SL::A_BYTES + (size_t)kSPK * SL::P_BYTES + (size_t)SL::LEV_BYTES +
+           (2 * KS + 1) * (size_t)RP * 8 + (size_t)StepKThreads<KS, TL, TX>::NI * 16 + (kSAK + kSPK) * 8 + 64;
 }
 
-template <int KS, int TL, int TX, int NPI, bool ONSITE, bool PEIERLS>
-__global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
+template <int KS, int TL, int TX, bool ONSITE, bool PEIERLS>
+__global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
     kpm_stepk_tma_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
                          const __grid_constant__ CUtensorMap mapAH,   // a_n halo box {2TL, KS, 1}
                          const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
@@ -97,16 +100,16 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
                          const __grid_constant__ CUtensorMap mapE,    // eps~ box {TX, 1}
                          const __grid_constant__ CUtensorMap mapEH,   // eps~ box {KS, 1}
                          const TmaKGeom g, const int tail) {
-    using SL = SlotKLayout<KS, TL, TX>;
-    using TH = StepKThreads<KS, TL, TX, NPI>;
+    using SL = SlotKLayout<KS, TL, TX, ONSITE>;
+    using TH = StepKThreads<KS, TL, TX>;
     constexpr int NI = TH::NI;
     constexpr int SITE = SL::SITE;
-    constexpr int KSTEP = NI / TL;  // interior columns per pass
+    constexpr int KSTEP = NI / TL;  // = TX / 2: the second column of an interior thread
     constexpr int NACC = 2 * KS + 1;
-    constexpr int A_BYTES = ONSITE ? SL::A_ON : SL::A_VEC;
+    constexpr int A_BYTES = SL::A_BYTES;
     static_assert(KS >= 2 && KS <= 4, "KS in 2..4");
     static_assert(NI % 32 == 0, "interior threads fill whole warps");
-    static_assert(TX % KSTEP == 0, "interior columns must fill whole passes");
+    static_assert(!ONSITE || KS % 2 == 0, "eps~ halo box: KS * 8 bytes must be a multiple of 16");
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ringA = smem;
     unsigned char* ringP = ringA + kSAK * A_BYTES;
@@ -120,7 +123,7 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
     const long long w_begin = g.W * blockIdx.x / gridDim.x;
     const long long w_end = g.W * (blockIdx.x + 1) / gridDim.x;
 
-    // ---- in-band producer (thread PRODUCER: the first halo thread, whose column computes one level)
+    // ---- in-band producer (thread PRODUCER: the first halo thread)
     constexpr int PRODUCER = NI;
     __shared__ LoadCursor cur_smem[2];
     __shared__ uint64_t pol_smem;
@@ -177,11 +180,11 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
     for (int i = t; i < NACC * g.RP; i += blockDim.x) sacc[i] = 0.0;
     __syncthreads();
 
-    // ---- this thread's columns: interior threads own columns t/TL and t/TL + KSTEP; halo thread
-    // hc owns the left column -(KS-1)+hc and the right column TX+hc, which compute levels
-    // 1..top (top = KS - distance outside the tile).  All levels are evaluated every row
-    // (straight-line code; the two columns are independent chains the scheduler interleaves);
-    // results outside a column's range or before a level's first row are never stored.
+    // ---- this thread's columns: interior threads own columns t/TL and t/TL + TX/2; halo
+    // thread hc owns the left column -(KS-1)+hc and the right column TX+hc, which compute
+    // levels 1..top (top = KS - distance outside the tile).  All levels are evaluated in
+    // every iteration (straight-line code); a level's values before its first row, after its
+    // last row or outside its column range are never stored nor read back.
     const bool interior = t < NI;
     const int l = (interior ? t : t - NI) % TL;
     const int lo = l * 16;
@@ -231,6 +234,10 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
         const double2 h = fma2(e, x, scale2(g.t, nb));
         return make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));
     };
+    auto lev_slot = [&](int j, int qq) {  // ring row of level j written in iteration qq (qq may be < 0)
+        const int S = SL::lev_slots(j);
+        return ringL + SL::lev_off(j) + (((qq % S) + S) % S) * SL::lev_row(j);
+    };
 
     LoadCursor cs;
     cs.init(g, w_begin, w_end, 0);
@@ -239,10 +246,9 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
         const int lg = cs.lg, m0 = cs.m0, H = cs.H, x0 = cs.px * TX;
         if (cur_lg != -1 && lg != cur_lg) flush(cur_lg);
         cur_lg = lg;
-        // per column: levels 0..KS-1 at three rows (m2 = two rows back, m1 = one row back,
-        // c = this row), eps~ of the rows of levels 2..KS, Peierls phase, output pointer
-        double2 vm2[2][KS], vm1[2][KS], vc[2][KS];
-        double es[2][KS];
+        // Registers per column: a_n at the last four rows (a0[0] = newest), levels 1..KS-1 at
+        // their last three rows (v[j][0] = newest); Peierls phase; output offset.
+        double2 a0[2][4], v[2][KS][3];
         double2 ph[2];
         long long ocol[2];
 #pragma unroll
@@ -252,102 +258,95 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
         }
         const long long growstep = (long long)g.L0 * g.RG;
         const int ia_seg = ia;
-        const int NQ = H + 2 * KS - 2;
-        int s1 = (ia_seg + 1) % kSAK;  // slot of a_n row r
-        int ps = ip % kSPK;
+        const int NA = H + 2 * KS;  // a_n rows of the segment (loads 0 .. NA-1)
+        const int NQ = H + 3 * KS;  // iterations
+        const int yb = m0 - KS - 1; // level j computes row yb + q - 2j + 1 in iteration q
         for (int q = 0; q < NQ; ++q) {
-            const int s2 = s1 + 1 == kSAK ? 0 : s1 + 1;  // a_n row r+1
-            const int r = m0 - KS + 1 + q;                // level-1 row (unwrapped)
-            if (q == 0) {
-                mbar_wait(fullA + ia_seg % kSAK, (uint32_t)((ia_seg / kSAK) & 1));
-                mbar_wait(fullA + s1, (uint32_t)(((ia_seg + 1) / kSAK) & 1));
-                const unsigned char* A0 = ringA + (ia_seg % kSAK) * A_BYTES;
-                const unsigned char* A1 = ringA + s1 * A_BYTES;
-#pragma unroll
-                for (int p = 0; p < 2; ++p) {
-                    vm2[p][0] = ld(A0 + (lxs[p] + KS) * SITE + lo);
-                    vm1[p][0] = ld(A1 + (lxs[p] + KS) * SITE + lo);
-                }
-            }
-            mbar_wait(fullA + s2, (uint32_t)(((ia_seg + q + 2) / kSAK) & 1));
-            mbar_wait(fullP + ps, (uint32_t)((ip / kSPK) & 1));
-            const unsigned char* A1 = ringA + s1 * A_BYTES;  // a_n row r
-            const unsigned char* A2 = ringA + s2 * A_BYTES;  // a_n row r+1
-            const unsigned char* Pq = ringP + ps * SL::P_BYTES;
-            const int wslot = q & 1, rslot = wslot ^ 1;
+            const bool newA = q < NA;             // a_n load q enters
+            const bool useP = q >= 3 && q <= NA;  // level 1 consumes a_{n-1} load q-3
+            if (newA) mbar_wait(fullA + (ia_seg + q) % kSAK, (uint32_t)(((ia_seg + q) / kSAK) & 1));
+            if (useP) mbar_wait(fullP + ip % kSPK, (uint32_t)((ip / kSPK) & 1));
+            const unsigned char* An = ringA + ((ia_seg + q) % kSAK) * A_BYTES;            // newest a_n row
+            const unsigned char* Ax = ringA + ((ia_seg + q - 2 + kSAK) % kSAK) * A_BYTES;  // level-1 row
+            const unsigned char* Pq = ringP + (ip % kSPK) * SL::P_BYTES;
+            double2 anew[2], y[2][KS + 1];
             double e1[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
                 const int lx = lxs[p];
-                vc[p][0] = ld(A2 + (lx + KS) * SITE + lo);
+                anew[p] = ld(An + (lx + KS) * SITE + lo);
                 e1[p] = g.shift;
                 if (ONSITE)
                     e1[p] = *reinterpret_cast<const double*>(
-                        A1 + (lx < 0 ? SL::EPS_L + (lx + KS) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8)));
+                        Ax + (lx < 0 ? SL::EPS_L + (lx + KS) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8)));
             }
 #pragma unroll
             for (int j = 1; j <= KS; ++j) {
-                const int row = r - (j - 1);
+                const int row = yb + q - 2 * j + 1;
                 const bool owned = interior && row >= m0 && row < m0 + H;
+                const unsigned char* Lx = j >= 2 ? lev_slot(j - 1, q - 2) : nullptr;  // level j-1 at this row
+                const unsigned char* Lm = j >= 3 ? lev_slot(j - 2, q - 4) : nullptr;  // level j-2 at this row
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
                     const int lx = lxs[p];
-                    double2 xm, xp, minus;
+                    double2 xm, xp, x, ym, yp, minus;
+                    double e;
                     if (j == 1) {
-                        xm = ld(A1 + (lx + KS - 1) * SITE + lo);
-                        xp = ld(A1 + (lx + KS + 1) * SITE + lo);
+                        xm = ld(Ax + (lx + KS - 1) * SITE + lo);
+                        xp = ld(Ax + (lx + KS + 1) * SITE + lo);
+                        ym = a0[p][2];
+                        x = a0[p][1];
+                        yp = a0[p][0];
                         minus = ld(Pq + (lx + KS - 1) * SITE + lo);
+                        e = e1[p];
                     } else {
-                        const unsigned char* Lr = ringL + SL::lev_off(j - 1) + rslot * SL::lev_row(j - 1);
-                        xm = ld(Lr + (lx + KS - j) * SITE + lo);
-                        xp = ld(Lr + (lx + KS - j + 2) * SITE + lo);
-                        minus = vm2[p][j >= 2 ? j - 2 : 0];
+                        const int ix = lx + KS - (j - 1);  // index in level j-1's row
+                        xm = ld(Lx + (ix - 1) * SITE + lo);
+                        xp = ld(Lx + (ix + 1) * SITE + lo);
+                        ym = v[p][j - 1][2];
+                        x = v[p][j - 1][1];
+                        yp = v[p][j - 1][0];
+                        minus = j == 2 ? a0[p][3] : ld(Lm + (lx + KS - (j - 2)) * SITE + lo);
+                        e = ONSITE ? *reinterpret_cast<const double*>(Lx + SL::lev_eps(j - 1) + ix * 8) : g.shift;
                     }
-                    const double e = ONSITE ? (j == 1 ? e1[p] : es[p][j >= 2 ? j - 2 : 0]) : g.shift;
-                    const double2 x = vm1[p][j - 1];
-                    const double2 y = step_val(x, xm, xp, vm2[p][j - 1], vc[p][j - 1], e, ph[p], minus);
-                    if (j < KS) {
-                        if (j <= top[p]) {
-                            unsigned char* Lw = ringL + SL::lev_off(j) + wslot * SL::lev_row(j);
-                            *reinterpret_cast<double2*>(Lw + (lx + KS - j) * SITE + lo) = y;
-                        }
-                        vc[p][j] = y;
+                    y[p][j] = step_val(x, xm, xp, ym, yp, e, ph[p], minus);
+                    if (j < KS && j <= top[p]) {
+                        unsigned char* Lw = lev_slot(j, q);
+                        const int iw = lx + KS - j;
+                        *reinterpret_cast<double2*>(Lw + iw * SITE + lo) = y[p][j];
+                        if (ONSITE && l == 0) *reinterpret_cast<double*>(Lw + SL::lev_eps(j) + iw * 8) = e;
                     }
                     if (owned) {
-                        if (j >= KS - 1) __stcs((j == KS ? g.outC : g.outB) + ocol[p] + row * growstep, y);
+                        if (j >= KS - 1) __stcs((j == KS ? g.outC : g.outB) + ocol[p] + row * growstep, y[p][j]);
                         dot_acc<PEIERLS>(acc[2 * (j - 1)], x, x);
-                        dot_acc<PEIERLS>(acc[2 * (j - 1) + 1], x, y);
-                        if (j == KS && tail) dot_acc<PEIERLS>(acc[2 * KS], y, y);
+                        dot_acc<PEIERLS>(acc[2 * (j - 1) + 1], x, y[p][j]);
+                        if (j == KS && tail) dot_acc<PEIERLS>(acc[2 * KS], y[p][j], y[p][j]);
                     }
                 }
             }
-            // roll one row down
+            // roll: this iteration's values become the newest rows
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
+                a0[p][3] = a0[p][2];
+                a0[p][2] = a0[p][1];
+                a0[p][1] = a0[p][0];
+                a0[p][0] = anew[p];
 #pragma unroll
-                for (int j = 0; j < KS; ++j) {
-                    vm2[p][j] = vm1[p][j];
-                    vm1[p][j] = vc[p][j];
-                }
-                if (ONSITE) {
-#pragma unroll
-                    for (int j = KS - 1; j > 0; --j) es[p][j] = es[p][j - 1];
-                    es[p][0] = e1[p];
+                for (int j = 1; j < KS; ++j) {
+                    v[p][j][2] = v[p][j][1];
+                    v[p][j][1] = v[p][j][0];
+                    v[p][j][0] = y[p][j];
                 }
             }
-            __syncthreads();  // row done: a_n row r (and at q == 0 row r-1) and a_{n-1} row r are free
+            __syncthreads();  // iteration done: a_n load q-2 and a_{n-1} load q-3 are free
             if (t == PRODUCER) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (q == 0) issueA(ia_seg % kSAK);
-                issueA(s1);
-                issueP(ps);
+                if (q >= 2 && q - 2 < NA) issueA((ia_seg + q - 2) % kSAK);
+                if (useP) issueP(ip % kSPK);
             }
-            ++ip;
-            s1 = s2;
-            ps = ps + 1 == kSPK ? 0 : ps + 1;
+            if (useP) ++ip;
         }
-        if (t == PRODUCER) issueA(s1);  // the segment's last a_n row
-        ia = ia_seg + H + 2 * KS;
+        ia = ia_seg + NA;
         cs.seg(g, 0);
     }
     if (cur_lg != -1) flush(cur_lg);
@@ -355,9 +354,9 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX, NPI>::NT, 1)
     for (int k = 0; k < NACC; ++k) {
         if (k == 2 * KS && !tail) continue;
         double* rowk = g.red + (size_t)k * g.slot_stride;
-        for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + v] = sacc[k * g.RP + v];
+        for (int vv = t; vv < g.RP; vv += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + vv] = sacc[k * g.RP + vv];
         for (int rr = blockIdx.x + gridDim.x; rr < g.rows_total; rr += gridDim.x)
-            for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)rr * g.RP + v] = 0.0;
+            for (int vv = t; vv < g.RP; vv += blockDim.x) rowk[(size_t)rr * g.RP + vv] = 0.0;
     }
 }
 
