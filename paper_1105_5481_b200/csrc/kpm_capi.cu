@@ -150,7 +150,8 @@ size_t stepk_smem(int ks, int tl, bool onsite, int RP) {
     using namespace kpm;
     if (ks == 4 && tl == 16) return onsite ? stepk_smem_bytes<4, 16, 32, true>(RP) : stepk_smem_bytes<4, 16, 32, false>(RP);
     if (ks == 4 && tl == 8) return onsite ? stepk_smem_bytes<4, 8, 64, true>(RP) : stepk_smem_bytes<4, 8, 64, false>(RP);
-    if (ks == 2 && tl == 16) return onsite ? stepk_smem_bytes<2, 16, 32, true>(RP) : stepk_smem_bytes<2, 16, 32, false>(RP);
+    if (ks == 3 && tl == 16) return onsite ? stepk_smem_bytes<3, 16, 32, true>(RP) : stepk_smem_bytes<3, 16, 32, false>(RP);
+    if (ks == 3 && tl == 8) return onsite ? stepk_smem_bytes<3, 8, 64, true>(RP) : stepk_smem_bytes<3, 8, 64, false>(RP);
     return 0;
 }
 
@@ -217,13 +218,13 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     }
     // KS-step kernel: 2D lattices, row tiles of TXK * TLK = 512 lanes (kpm_tmak.cuh)
     p->use_tmak = false;
-    const int ks = env_on("KPM_NO_TMAK") ? 0 : env_int("KPM_TMAK_KS", 4);
+    const int ks = env_on("KPM_NO_TMAK") ? 0 : env_int("KPM_TMAK_KS", 3);
     if (h->ndim == 2 && !p->no_fused && ks >= 2) {
         const bool on = h->d_eps != nullptr;
         const int tlk = RG % 16 == 0 ? 16 : (RG % 8 == 0 ? 8 : 0);
         const int txk = tlk ? 512 / tlk : 0;
         const size_t sm = tlk ? stepk_smem(ks, tlk, on, p->RP) : 0;
-        if (sm && h->L[0] % txk == 0 && h->L[0] >= ks && sm <= 227 * 1024) {
+        if (sm && h->L[0] % txk == 0 && h->L[0] >= 4 && sm <= 227 * 1024) {
             p->KSK = ks;
             p->TLK = tlk;
             p->TXK = txk;
@@ -588,7 +589,8 @@ kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
                        const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
     if (p.KSK == 4 && p.TLK == 16) return launch_tmak_s<4, 16, 32>(h, p, A, P, E, EH, g, tail);
     if (p.KSK == 4 && p.TLK == 8) return launch_tmak_s<4, 8, 64>(h, p, A, P, E, EH, g, tail);
-    if (p.KSK == 2 && p.TLK == 16) return launch_tmak_s<2, 16, 32>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 3 && p.TLK == 16) return launch_tmak_s<3, 16, 32>(h, p, A, P, E, EH, g, tail);
+    if (p.KSK == 3 && p.TLK == 8) return launch_tmak_s<3, 8, 64>(h, p, A, P, E, EH, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d", p.KSK, p.TLK);
 }
 
@@ -825,7 +827,7 @@ struct Run {
                 }
                 if (p.use_tmak) {
                     KPM_TRY(make_eps_map_w(h, p, p.TXK, &mapEK));
-                    KPM_TRY(make_eps_map_w(h, p, p.KSK, &mapEKH));
+                    KPM_TRY(make_eps_map_w(h, p, (p.KSK + 1) / 2 * 2, &mapEKH));
                 }
             }
             tg.L0 = (int)h->L[0];

@@ -54,7 +54,9 @@ template <int KS, int TL, int TX, bool ONSITE>
 struct SlotKLayout {
     static constexpr int SITE = TL * 16;
     __host__ __device__ static constexpr int round128(int b) { return (b + 127) / 128 * 128; }
-    // a_n slot: sites [-KS, TX+KS), then eps~ in three 128-byte aligned pieces [KS][TX][KS]
+    // a_n slot: sites [-KS, TX+KS), then eps~ in three 128-byte aligned pieces [KSE][TX][KSE]
+    // (KSE = KS rounded up to even: a TMA box row must be a multiple of 16 bytes)
+    static constexpr int KSE = (KS + 1) / 2 * 2;
     static constexpr int A_VEC = (TX + 2 * KS) * SITE;
     static constexpr int EPS_L = A_VEC;
     static constexpr int EPS_M = EPS_L + 128;
@@ -98,7 +100,7 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
                          const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
                          const __grid_constant__ CUtensorMap mapPH,   // a_{n-1} halo box {2TL, KS-1, 1}
                          const __grid_constant__ CUtensorMap mapE,    // eps~ box {TX, 1}
-                         const __grid_constant__ CUtensorMap mapEH,   // eps~ box {KS, 1}
+                         const __grid_constant__ CUtensorMap mapEH,   // eps~ box {KSE, 1}
                          const TmaKGeom g, const int tail) {
     using SL = SlotKLayout<KS, TL, TX, ONSITE>;
     using TH = StepKThreads<KS, TL, TX>;
@@ -109,7 +111,6 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
     constexpr int A_BYTES = SL::A_BYTES;
     static_assert(KS >= 2 && KS <= 4, "KS in 2..4");
     static_assert(NI % 32 == 0, "interior threads fill whole warps");
-    static_assert(!ONSITE || KS % 2 == 0, "eps~ halo box: KS * 8 bytes must be a multiple of 16");
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ringA = smem;
     unsigned char* ringP = ringA + kSAK * A_BYTES;
@@ -135,12 +136,12 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
         const int c0 = 2 * ca.lg * TL, x0 = ca.px * TX;
         const int xl = (x0 - KS + g.L0) % g.L0, xr = (x0 + TX) % g.L0;
         unsigned char* dst = ringA + slot * A_BYTES;
-        mbar_expect_tx(fullA + slot, (TX + 2 * KS) * SITE + (ONSITE ? (TX + 2 * KS) * 8 : 0));
+        mbar_expect_tx(fullA + slot, (TX + 2 * KS) * SITE + (ONSITE ? (TX + 2 * SL::KSE) * 8 : 0));
         tma_load(dst, &mapAH, fullA + slot, c0, xl, row);
         tma_load(dst + KS * SITE, &mapA, fullA + slot, c0, x0, row);
         tma_load(dst + (TX + KS) * SITE, &mapAH, fullA + slot, c0, xr, row);
         if (ONSITE) {
-            tma_load_2d(dst + SL::EPS_L, &mapEH, fullA + slot, xl, row);
+            tma_load_2d(dst + SL::EPS_L, &mapEH, fullA + slot, (x0 - SL::KSE + g.L0) % g.L0, row);
             tma_load_2d(dst + SL::EPS_M, &mapE, fullA + slot, x0, row);
             tma_load_2d(dst + SL::EPS_R, &mapEH, fullA + slot, xr, row);
         }
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
                 e1[p] = g.shift;
                 if (ONSITE)
                     e1[p] = *reinterpret_cast<const double*>(
-                        Ax + (lx < 0 ? SL::EPS_L + (lx + KS) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8)));
+                        Ax + (lx < 0 ? SL::EPS_L + (lx + SL::KSE) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8)));
             }
 #pragma unroll
             for (int j = 1; j <= KS; ++j) {
