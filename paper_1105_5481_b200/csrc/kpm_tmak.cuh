@@ -205,7 +205,6 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
     double2 acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = make_double2(0.0, 0.0);
-    auto ld = [](const unsigned char* p) { return *reinterpret_cast<const double2*>(p); };
     auto flush = [&](int lgf) {
 #pragma unroll
         for (int k = 0; k < NACC; ++k) {
@@ -235,9 +234,27 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
         const double2 h = fma2(e, x, scale2(g.t, nb));
         return make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));
     };
-    auto lev_slot = [&](int j, int qq) {  // ring row of level j written in iteration qq (qq may be < 0)
+    // Shared-memory addressing: 32-bit offsets from smem.  Per column one invariant offset
+    // colA (site lx of an a_n slot); level j-1's row is shifted by j-1 sites, the a_{n-1} row
+    // by one.  Slot bases are uniform per iteration and advanced incrementally.
+    auto ld = [&](uint32_t off) { return *reinterpret_cast<const double2*>(smem + off); };
+    auto ldd = [&](uint32_t off) { return *reinterpret_cast<const double*>(smem + off); };
+    const uint32_t offA = 0, offP = kSAK * A_BYTES, offL = offP + kSPK * SL::P_BYTES;
+    uint32_t colA[2], colE[2], epsA[2];
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+        const int lx = lxs[p];
+        colA[p] = (uint32_t)((lx + KS) * SITE + lo);
+        colE[p] = (uint32_t)((lx + KS) * 8);
+        epsA[p] = (uint32_t)(lx < 0 ? SL::EPS_L + (lx + SL::KSE) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8));
+    }
+    // ring slot of level j for iteration q - back (back = 0, 2, 4), from the counters q mod 5, q mod 3
+    auto lev_base = [&](int j, int c5, int c3, int back) -> uint32_t {
         const int S = SL::lev_slots(j);
-        return ringL + SL::lev_off(j) + (((qq % S) + S) % S) * SL::lev_row(j);
+        int sl;
+        if (S == 5) sl = back == 0 ? c5 : (back == 2 ? (c5 >= 2 ? c5 - 2 : c5 + 3) : (c5 >= 4 ? c5 - 4 : c5 + 1));
+        else sl = back == 0 ? c3 : (back == 2 ? (c3 >= 2 ? c3 - 2 : c3 + 1) : (c3 >= 1 ? c3 - 1 : c3 + 2));
+        return offL + (uint32_t)SL::lev_off(j) + (uint32_t)sl * (uint32_t)SL::lev_row(j);
     };
 
     LoadCursor cs;
@@ -262,63 +279,63 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
         const int NA = H + 2 * KS;  // a_n rows of the segment (loads 0 .. NA-1)
         const int NQ = H + 3 * KS;  // iterations
         const int yb = m0 - KS - 1; // level j computes row yb + q - 2j + 1 in iteration q
+        int sN = ia_seg % kSAK;                 // slot of a_n load q
+        int sX = (ia_seg + kSAK - 2) % kSAK;    // slot of a_n load q-2
+        int c5 = 0, c3 = 0;                     // q mod 5, q mod 3
         for (int q = 0; q < NQ; ++q) {
             const bool newA = q < NA;             // a_n load q enters
             const bool useP = q >= 3 && q <= NA;  // level 1 consumes a_{n-1} load q-3
-            if (newA) mbar_wait(fullA + (ia_seg + q) % kSAK, (uint32_t)(((ia_seg + q) / kSAK) & 1));
-            if (useP) mbar_wait(fullP + ip % kSPK, (uint32_t)((ip / kSPK) & 1));
-            const unsigned char* An = ringA + ((ia_seg + q) % kSAK) * A_BYTES;            // newest a_n row
-            const unsigned char* Ax = ringA + ((ia_seg + q - 2 + kSAK) % kSAK) * A_BYTES;  // level-1 row
-            const unsigned char* Pq = ringP + (ip % kSPK) * SL::P_BYTES;
+            const int sP = ip % kSPK;
+            if (newA) mbar_wait(fullA + sN, (uint32_t)(((ia_seg + q) / kSAK) & 1));
+            if (useP) mbar_wait(fullP + sP, (uint32_t)((ip / kSPK) & 1));
+            const uint32_t An = offA + (uint32_t)sN * A_BYTES;   // newest a_n row
+            const uint32_t Ax = offA + (uint32_t)sX * A_BYTES;   // a_n at level 1's row
+            const uint32_t Pq = offP + (uint32_t)sP * SL::P_BYTES;
             double2 anew[2], y[2][KS + 1];
             double e1[2];
 #pragma unroll
             for (int p = 0; p < 2; ++p) {
-                const int lx = lxs[p];
-                anew[p] = ld(An + (lx + KS) * SITE + lo);
-                e1[p] = g.shift;
-                if (ONSITE)
-                    e1[p] = *reinterpret_cast<const double*>(
-                        Ax + (lx < 0 ? SL::EPS_L + (lx + SL::KSE) * 8 : (lx < TX ? SL::EPS_M + lx * 8 : SL::EPS_R + (lx - TX) * 8)));
+                anew[p] = ld(An + colA[p]);
+                e1[p] = ONSITE ? ldd(Ax + epsA[p]) : g.shift;
             }
 #pragma unroll
             for (int j = 1; j <= KS; ++j) {
                 const int row = yb + q - 2 * j + 1;
                 const bool owned = interior && row >= m0 && row < m0 + H;
-                const unsigned char* Lx = j >= 2 ? lev_slot(j - 1, q - 2) : nullptr;  // level j-1 at this row
-                const unsigned char* Lm = j >= 3 ? lev_slot(j - 2, q - 4) : nullptr;  // level j-2 at this row
+                const long long rowoff = (long long)row * growstep;
+                const uint32_t Lx = j >= 2 ? lev_base(j - 1, c5, c3, 2) : 0u;  // level j-1 at this row
+                const uint32_t Lm = j >= 3 ? lev_base(j - 2, c5, c3, 4) : 0u;  // level j-2 at this row
+                const uint32_t Lw = j < KS ? lev_base(j, c5, c3, 0) : 0u;      // level j, written now
 #pragma unroll
                 for (int p = 0; p < 2; ++p) {
-                    const int lx = lxs[p];
                     double2 xm, xp, x, ym, yp, minus;
                     double e;
                     if (j == 1) {
-                        xm = ld(Ax + (lx + KS - 1) * SITE + lo);
-                        xp = ld(Ax + (lx + KS + 1) * SITE + lo);
+                        const uint32_t c = Ax + colA[p];
+                        xm = ld(c - SITE);
+                        xp = ld(c + SITE);
                         ym = a0[p][2];
                         x = a0[p][1];
                         yp = a0[p][0];
-                        minus = ld(Pq + (lx + KS - 1) * SITE + lo);
+                        minus = ld(Pq + colA[p] - SITE);
                         e = e1[p];
                     } else {
-                        const int ix = lx + KS - (j - 1);  // index in level j-1's row
-                        xm = ld(Lx + (ix - 1) * SITE + lo);
-                        xp = ld(Lx + (ix + 1) * SITE + lo);
+                        const uint32_t c = Lx + colA[p] - (j - 1) * SITE;  // site lx of level j-1's row
+                        xm = ld(c - SITE);
+                        xp = ld(c + SITE);
                         ym = v[p][j - 1][2];
                         x = v[p][j - 1][1];
                         yp = v[p][j - 1][0];
-                        minus = j == 2 ? a0[p][3] : ld(Lm + (lx + KS - (j - 2)) * SITE + lo);
-                        e = ONSITE ? *reinterpret_cast<const double*>(Lx + SL::lev_eps(j - 1) + ix * 8) : g.shift;
+                        minus = j == 2 ? a0[p][3] : ld(Lm + colA[p] - (j - 2) * SITE);
+                        e = ONSITE ? ldd(Lx + SL::lev_eps(j - 1) + colE[p] - (j - 1) * 8) : g.shift;
                     }
                     y[p][j] = step_val(x, xm, xp, ym, yp, e, ph[p], minus);
                     if (j < KS && j <= top[p]) {
-                        unsigned char* Lw = lev_slot(j, q);
-                        const int iw = lx + KS - j;
-                        *reinterpret_cast<double2*>(Lw + iw * SITE + lo) = y[p][j];
-                        if (ONSITE && l == 0) *reinterpret_cast<double*>(Lw + SL::lev_eps(j) + iw * 8) = e;
+                        *reinterpret_cast<double2*>(smem + Lw + colA[p] - j * SITE) = y[p][j];
+                        if (ONSITE && l == 0) *reinterpret_cast<double*>(smem + Lw + SL::lev_eps(j) + colE[p] - j * 8) = e;
                     }
                     if (owned) {
-                        if (j >= KS - 1) __stcs((j == KS ? g.outC : g.outB) + ocol[p] + row * growstep, y[p][j]);
+                        if (j >= KS - 1) __stcs((j == KS ? g.outC : g.outB) + (rowoff + ocol[p]), y[p][j]);
                         dot_acc<PEIERLS>(acc[2 * (j - 1)], x, x);
                         dot_acc<PEIERLS>(acc[2 * (j - 1) + 1], x, y[p][j]);
                         if (j == KS && tail) dot_acc<PEIERLS>(acc[2 * KS], y[p][j], y[p][j]);
@@ -342,10 +359,14 @@ __global__ void __launch_bounds__(StepKThreads<KS, TL, TX>::NT, 1)
             __syncthreads();  // iteration done: a_n load q-2 and a_{n-1} load q-3 are free
             if (t == PRODUCER) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                if (q >= 2 && q - 2 < NA) issueA((ia_seg + q - 2) % kSAK);
-                if (useP) issueP(ip % kSPK);
+                if (q >= 2 && q - 2 < NA) issueA(sX);
+                if (useP) issueP(sP);
             }
             if (useP) ++ip;
+            sN = sN + 1 == kSAK ? 0 : sN + 1;
+            sX = sX + 1 == kSAK ? 0 : sX + 1;
+            c5 = c5 + 1 == 5 ? 0 : c5 + 1;
+            c3 = c3 + 1 == 3 ? 0 : c3 + 1;
         }
         ia = ia_seg + NA;
         cs.seg(g, 0);

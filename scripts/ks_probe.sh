@@ -5,7 +5,7 @@ cd "${GRAFT_REPO_ROOT:-/root/repo}"
 OUT=gpurun_out/$1
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()"
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -k "four_step or tma_march or two_step" > $OUT/pytest.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -m gpu -k "multi_step or tma_march or two_step" > $OUT/pytest.log 2>&1
 tail -3 $OUT/pytest.log
 B="python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e"
 for c in c2 c4; do

@@ -150,8 +150,8 @@ KSTEP_CASES = {
 
 @pytest.mark.parametrize("case", sorted(KSTEP_CASES))
 @pytest.mark.parametrize("N", [10, 11, 12, 13, 16, 19, 26])
-def test_four_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
-    """2D: the KS = 4 deep temporal-blocking kernel (kpm_tmak.cuh) mixed with two-step and
+def test_multi_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
+    """2D: the KS-step (default KS = 3) deep temporal-blocking kernel (kpm_tmak.cuh) mixed with two-step and
     single-step launches for the remainder, every parity of N (odd-N tail in the last launch)."""
     monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat, R = KSTEP_CASES[case]
@@ -163,7 +163,8 @@ def test_four_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
     h = make(kpm, lat, a, b)
     info = h.plan_info(N, R)
-    assert info["ks"] == 4, info
+    ks = info["ks"]
+    assert ks >= 3, info
     mu = h.moments(N, R, 13)
     assert normwise(mu, ref) < TOL
     pv = h.moments_ex(N, R, 13, flags=kpm.KPM_PER_VECTOR)
@@ -171,8 +172,8 @@ def test_four_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
     assert np.array_equal(h.moments(N, R, 13), mu), "not deterministic"
     _, launches, _ = h.last_timing()
     M = N // 2
-    rem = (M - 1) % 4
-    assert launches == (M - 1) // 4 + (rem // 2 + rem % 2 if info["two_step"] else rem), (launches, info)
+    rem = (M - 1) % ks
+    assert launches == (M - 1) // ks + (rem // 2 + rem % 2 if info["two_step"] else rem), (launches, info)
     monkeypatch.setenv("KPM_NO_TMAK", "1")
     assert h.plan_info(N, R)["ks"] == 0
     assert normwise(h.moments(N, R, 13), ref) < TOL
