@@ -218,7 +218,9 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     }
     // KS-step kernel: 2D lattices, row tiles of TXK * TLK = 512 lanes (kpm_tmak.cuh)
     p->use_tmak = false;
-    const int ks = env_on("KPM_NO_TMAK") ? 0 : env_int("KPM_TMAK_KS", 3);
+    // Opt-in (KPM_TMAK_KS = 3 or 4): measured slower than the two-step kernel on c2 and c4
+    // ("deeper temporal blocking"), so the default plan does not use it.
+    const int ks = env_on("KPM_NO_TMAK") ? 0 : env_int("KPM_TMAK_KS", 0);
     if (h->ndim == 2 && !p->no_fused && ks >= 2) {
         const bool on = h->d_eps != nullptr;
         const int tlk = RG % 16 == 0 ? 16 : (RG % 8 == 0 ? 8 : 0);

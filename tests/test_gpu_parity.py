@@ -148,12 +148,14 @@ KSTEP_CASES = {
 }
 
 
+@pytest.mark.parametrize("ks", [3, 4])
 @pytest.mark.parametrize("case", sorted(KSTEP_CASES))
 @pytest.mark.parametrize("N", [10, 11, 12, 13, 16, 19, 26])
-def test_multi_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
+def test_multi_step_kernel_matches_oracle(kpm, case, N, ks, monkeypatch):
     """2D: the KS-step (default KS = 3) deep temporal-blocking kernel (kpm_tmak.cuh) mixed with two-step and
     single-step launches for the remainder, every parity of N (odd-N tail in the last launch)."""
     monkeypatch.setenv("KPM_NO_SMALL", "1")
+    monkeypatch.setenv("KPM_TMAK_KS", str(ks))  # opt-in kernel
     lat, R = KSTEP_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -163,8 +165,7 @@ def test_multi_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
     h = make(kpm, lat, a, b)
     info = h.plan_info(N, R)
-    ks = info["ks"]
-    assert ks >= 3, info
+    assert info["ks"] == ks, info
     mu = h.moments(N, R, 13)
     assert normwise(mu, ref) < TOL
     pv = h.moments_ex(N, R, 13, flags=kpm.KPM_PER_VECTOR)
@@ -174,7 +175,7 @@ def test_multi_step_kernel_matches_oracle(kpm, case, N, monkeypatch):
     M = N // 2
     rem = (M - 1) % ks
     assert launches == (M - 1) // ks + (rem // 2 + rem % 2 if info["two_step"] else rem), (launches, info)
-    monkeypatch.setenv("KPM_NO_TMAK", "1")
+    monkeypatch.delenv("KPM_TMAK_KS")
     assert h.plan_info(N, R)["ks"] == 0
     assert normwise(h.moments(N, R, 13), ref) < TOL
 
