@@ -159,6 +159,17 @@ def moments_doubling(H: CSR, a, b, r, N, per_vector=False):
     return _moments(_load().oracle_moments_doubling, H, a, b, r, N, per_vector)
 
 
+def local_moments(H: CSR, a, b, sites, N):
+    """Local moments mu_n^(i) = <i|T_n(H~)|i> (the local DoS of site i; SURVEY.md 8(f)
+    NEXT-1): O3 with the unit start vectors e_i, whose per-vector moments are
+    (1/D) <i|T_n(H~)|i>, times D.  Returns (len(sites), N)."""
+    sites = np.asarray(sites, dtype=np.int64)
+    r = np.zeros((len(sites), H.D))
+    r[np.arange(len(sites)), sites] = 1.0
+    _, pv = moments_doubling(H, a, b, r, N, per_vector=True)
+    return pv * H.D
+
+
 from .exact import (chebyshev_nodes, dos, dos_closed_1d, dos_closed_2d,  # noqa: E402,F401
-                    exact_moments_dense, exact_moments_from_eigs, harper_spectrum, jackson,
-                    lattice_spectrum)
+                    exact_moments_dense, exact_moments_from_eigs, green, green_closed_1d,
+                    harper_spectrum, jackson, kernel_coeffs, lattice_spectrum)

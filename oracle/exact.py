@@ -77,18 +77,77 @@ def jackson(N: int) -> np.ndarray:
     return ((N - n + 1) * np.cos(q * n) + np.sin(q * n) / np.tan(q)) / (N + 1)
 
 
+def kernel_coeffs(N: int, kind: str = "jackson", lam: float = 4.0) -> np.ndarray:
+    """Damping factors g_n, n = 0..N-1, of Eq (6) ("a kernel which satisfies the
+    limit" Eq 7).  The paper names the Jackson kernel; the others
+    are the standard ones of its ref [10] (Weisse et al., RMP 78, 275):
+      jackson  reading X8 (jackson() above)
+      lorentz  g_n = sinh(lam (1 - n/N)) / sinh(lam)      (for Green's functions; lam ~ 3-5)
+      fejer    g_n = 1 - n/N                               (Cesaro mean of the partial sums)
+      none     g_n = 1                                     (Dirichlet: truncated series, Eq 1)"""
+    n = np.arange(N, dtype=np.float64)
+    if kind == "jackson":
+        return jackson(N)
+    if kind == "lorentz":
+        return np.sinh(lam * (1.0 - n / N)) / np.sinh(lam)
+    if kind == "fejer":
+        return 1.0 - n / N
+    if kind == "none":
+        return np.ones(N)
+    raise ValueError(kind)
+
+
+def green(mu, a: float, b: float, omega, kernel: str = "jackson", lam: float = 4.0) -> np.ndarray:
+    """Retarded Green's function G(omega) = (1/D) Tr 1/(omega + i0 - H) from the damped
+    moments (the paper's "Green's functions"; expansion of ref [10]), reading
+    X24: with x = (omega - b)/a, c_0 = g_0 mu_0, c_n = 2 g_n mu_n and
+      |x| < 1:  G~(x) = -i sum_n c_n e^{-i n theta} / sin(theta),  theta = arccos x
+      |x| > 1:  G~(x) = sum_n c_n t^n / (sgn(x) sqrt(x^2 - 1)),     t = x - sgn(x) sqrt(x^2 - 1)
+    (both from 1/(z - y) = sum_n (2 - delta_n0) T_n(y) t^n / sqrt(z^2 - 1), t = z - sqrt(z^2-1));
+    G(omega) = G~(x) / a.  |x| = 1 is singular: NaN."""
+    mu = np.asarray(mu, dtype=np.float64)
+    N = len(mu)
+    c = kernel_coeffs(N, kernel, lam) * mu
+    c[1:] *= 2.0
+    x = (np.asarray(omega, dtype=np.float64) - b) / a
+    out = np.full(x.shape, np.nan + 1j * np.nan, dtype=np.complex128)
+    n = np.arange(N, dtype=np.float64)
+    ins = np.abs(x) < 1.0
+    th = np.arccos(x[ins])
+    out[ins] = -1j * (np.exp(-1j * np.outer(th, n)) @ c) / np.sin(th)
+    outs = np.abs(x) > 1.0
+    xo = x[outs]
+    sg = np.sign(xo)
+    sq = np.sqrt(xo * xo - 1.0)
+    t = xo - sg * sq
+    out[outs] = (np.power.outer(t, n) @ c) / (sg * sq)
+    return out / a
+
+
+def green_closed_1d(E, t: float = -1.0) -> np.ndarray:
+    """O7: Green's function of the infinite 1D chain, G(E + i0) = 1/sqrt((E+i0)^2 - 4t^2):
+    -i/sqrt(4t^2 - E^2) inside the band, 1/(sgn(E) sqrt(E^2 - 4t^2)) outside."""
+    E = np.asarray(E, dtype=np.float64)
+    w = 2 * abs(t)
+    out = np.empty(E.shape, dtype=np.complex128)
+    ins = np.abs(E) < w
+    out[ins] = -1j / np.sqrt(w * w - E[ins] ** 2)
+    out[~ins] = 1.0 / (np.sign(E[~ins]) * np.sqrt(E[~ins] ** 2 - w * w))
+    return out
+
+
 def chebyshev_nodes(K: int) -> np.ndarray:
     """x_k = cos(pi (k + 1/2) / K), k = 0..K-1 (reading X7)."""
     return np.cos(np.pi * (np.arange(K) + 0.5) / K)
 
 
-def dos(mu, a: float, b: float, omega, kernel: str = "jackson") -> np.ndarray:
+def dos(mu, a: float, b: float, omega, kernel: str = "jackson", lam: float = 4.0) -> np.ndarray:
     """Eq (6), mapped back to omega (Eq 11-12; reading X9):
     rho(omega) = [g_0 mu_0 + 2 sum_{n=1}^{N-1} g_n mu_n T_n(x)] / (pi sqrt(1-x^2)) / a,
     x = (omega - b)/a; rho = 0 for |x| >= 1 (reading X7)."""
     mu = np.asarray(mu, dtype=np.float64)
     N = len(mu)
-    g = jackson(N) if kernel == "jackson" else np.ones(N)
+    g = kernel_coeffs(N, kernel, lam)
     x = (np.asarray(omega, dtype=np.float64) - b) / a
     out = np.zeros_like(x)
     inside = np.abs(x) < 1.0

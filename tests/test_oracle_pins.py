@@ -330,3 +330,85 @@ def test_2d_kpm_dos_converges_to_elliptic_closed_form():
         mu = oracle.exact_moments_from_eigs(lam, 4.0, 0.0, N)
         err[N] = np.abs(oracle.dos(mu, 4.0, 0.0, E) - oracle.dos_closed_2d(E)).max()
     assert err[256] < err[128] / 3 < err[64] / 9 < 0.001
+
+
+# ---------------------------------------------------------------- NEXT-1: kernels, G, LDoS
+def test_fejer_kernel_is_cesaro_mean_of_partial_sums():
+    """kernel_coeffs('fejer') pinned by its construction: the Fejer-damped series equals the
+    arithmetic mean of the truncated (Dirichlet, g = 1) series with 1..N terms."""
+    H = oracle.lattice_csr(lat(2, (12, 10)))
+    mu = oracle.moments_doubling(H, 4.0, 0.0, ki.rademacher(4, 3, 120), 24)
+    E = np.linspace(-3.9, 3.9, 41)
+    mean = np.mean([oracle.dos(mu[:m], 4.0, 0.0, E, kernel="none") for m in range(1, 25)], axis=0)
+    assert np.abs(oracle.dos(mu, 4.0, 0.0, E, kernel="fejer") - mean).max() < 1e-13
+
+
+def test_lorentz_kernel_limits():
+    """kernel_coeffs('lorentz'): g_0 = 1, decreasing to g_N = 0 (beyond the last moment), and
+    the lam -> 0 limit is the Fejer kernel (sinh(lam u)/sinh(lam) -> u)."""
+    N = 50
+    g = oracle.kernel_coeffs(N, "lorentz", 4.0)
+    assert g[0] == 1.0 and np.all(np.diff(g) < 0) and 0 < g[-1] < 0.1
+    assert np.abs(oracle.kernel_coeffs(N, "lorentz", 1e-5) - oracle.kernel_coeffs(N, "fejer")).max() < 1e-9
+    assert np.array_equal(oracle.kernel_coeffs(N, "none"), np.ones(N))
+    assert np.array_equal(oracle.kernel_coeffs(N, "jackson"), oracle.jackson(N))
+
+
+def test_green_1d_exact_moments_equal_closed_form():
+    """green() with the exact infinite-chain moments (mu_n = delta_n0, a = 2) is the textbook
+    chain Green's function 1/sqrt((E + i0)^2 - 4t^2) inside and outside the band, for every
+    kernel (g_0 = 1)."""
+    mu = oracle.exact_moments_from_eigs(oracle.lattice_spectrum(1, (1024, 1, 1), -1.0), 2.0, 0.0, 64)
+    E = np.concatenate([np.linspace(-1.9, 1.9, 39), [-3.0, -2.2, 2.1, 2.7, 5.0]])
+    ref = oracle.green_closed_1d(E)
+    for k in ("jackson", "lorentz", "none"):
+        G = oracle.green(mu, 2.0, 0.0, E, kernel=k)
+        assert np.abs(G / ref - 1).max() < 1e-10, k
+
+
+def test_green_outside_spectrum_equals_resolvent_trace():
+    """Outside [b-a, b+a] the undamped expansion converges geometrically (|t| < 1) to the exact
+    resolvent (1/D) sum_k 1/(omega - E_k) of a random Hermitian H (dense eigvalsh)."""
+    rng = np.random.default_rng(3)
+    D = 40
+    A = rng.standard_normal((D, D)) + 1j * rng.standard_normal((D, D))
+    Hd = (A + A.conj().T) / 2
+    ev = np.linalg.eigvalsh(Hd)
+    b = 0.3
+    a = 1.02 * max(ev.max() - b, b - ev.min())
+    mu = oracle.exact_moments_from_eigs(ev, a, b, 400)
+    w = np.array([b - 1.6 * a, b - 1.1 * a, b + 1.05 * a, b + 2.0 * a])
+    ref = (1.0 / (w[:, None] - ev[None, :])).mean(axis=1)
+    G = oracle.green(mu, a, b, w, kernel="none")
+    assert np.abs(G.imag).max() == 0.0
+    assert np.abs(G.real - ref).max() < 1e-12 * np.abs(ref).max()
+
+
+def test_green_imaginary_part_is_minus_pi_dos():
+    """Inside the band -Im G / pi is the KPM DoS of Eq (6) (same kernel), and Re G is an odd
+    function of omega for a symmetric spectrum (b = 0, bipartite 2D lattice)."""
+    H = oracle.lattice_csr(lat(2, (16, 16)))
+    mu = oracle.moments_doubling(H, 4.0, 0.0, ki.rademacher(8, 5, 256), 64)
+    mu[1::2] = 0.0  # exact odd moments of the bipartite lattice (Q8)
+    E = np.linspace(-3.9, 3.9, 53)
+    for k in ("jackson", "lorentz"):
+        G = oracle.green(mu, 4.0, 0.0, E, kernel=k)
+        assert np.abs(-G.imag / np.pi - oracle.dos(mu, 4.0, 0.0, E, kernel=k)).max() < 1e-13
+        assert np.abs(G.real + G.real[::-1]).max() < 1e-12
+
+
+def test_local_moments_average_to_trace_and_are_uniform_on_clean_lattices():
+    """local_moments: (i) the average over all sites is the exact trace (dense eigvalsh, with
+    Anderson disorder so sites differ); (ii) on a clean periodic lattice every site has the
+    same local moments, equal to the exact DoS moments (translation invariance)."""
+    onsite = ki.anderson_onsite(9, 60, 2.0)
+    H = oracle.lattice_csr(lat(2, (10, 6), onsite=onsite))
+    a, b = oracle.gershgorin(H)
+    lm = oracle.local_moments(H, a, b, np.arange(60), 40)
+    ex = oracle.exact_moments_dense(H, a, b, 40)
+    assert np.abs(lm.mean(axis=0) - ex).max() < 1e-13
+    assert np.abs(lm - lm[0]).max() > 1e-3  # disorder: sites differ
+    H2 = oracle.lattice_csr(lat(3, (6, 5, 4)))
+    lm2 = oracle.local_moments(H2, 6.0, 0.0, [0, 7, 33, 119], 30)
+    ex2 = oracle.exact_moments_from_eigs(oracle.lattice_spectrum(3, (6, 5, 4), -1.0), 6.0, 0.0, 30)
+    assert np.abs(lm2 - ex2[None, :]).max() < 1e-13
