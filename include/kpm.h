@@ -62,12 +62,17 @@ enum {
 /* Element type of H and of the vector block. */
 enum { KPM_REAL64 = 0, KPM_COMPLEX128 = 1 };
 
-/* Damping kernel g_n of Eq (6). */
+/* Damping kernel g_n of Eq (6) ("a kernel which satisfies the limit" Eq 7, PAPER.md:65-68;
+ * formulas from the paper's ref [10]; X8, X26). */
 enum {
     KPM_KERNEL_JACKSON = 0, /* g_n = [(N-n+1)cos(pi n/(N+1)) + sin(pi n/(N+1))cot(pi/(N+1))]/(N+1)
-                               (formula from its ref [10]; X8) */
-    KPM_KERNEL_NONE = 1     /* g_n = 1 (truncated series, Eq 1) */
+                                */
+    KPM_KERNEL_NONE = 1,    /* g_n = 1 (truncated series, Eq 1) */
+    KPM_KERNEL_LORENTZ = 2, /* g_n = sinh(lambda (1 - n/N)) / sinh(lambda), lambda > 0 (Green's
+                               functions; kpm_dos uses lambda = KPM_LORENTZ_DEFAULT_LAMBDA) */
+    KPM_KERNEL_FEJER = 3    /* g_n = 1 - n/N (Cesaro mean of the partial sums) */
 };
+#define KPM_LORENTZ_DEFAULT_LAMBDA 4.0
 
 /* kpm_moments_ex flags. */
 enum {
@@ -76,7 +81,11 @@ enum {
     KPM_DEVICE_OUT = 4u, /* out is a device pointer */
     KPM_RAW_SUMS = 8u,   /* out = raw sums S[N] over this rank's vectors, before normalisation and
                             the doubling transform (for a cross-rank all-reduce; see kpm_assemble) */
-    KPM_DEVICE_IN = 16u  /* r0 is a device pointer */
+    KPM_DEVICE_IN = 16u, /* r0 is a device pointer */
+    KPM_LOCAL = 32u      /* local moments: r0 is a HOST int64 list of R global site indices; the start
+                            vectors are the unit vectors e_site (no randomness, seed ignored) and
+                            out[R_local][N] = <site|T_n(H~)|site> (implies KPM_PER_VECTOR; no 1/D).
+                            Not combinable with KPM_RAW_SUMS or KPM_DEVICE_IN. */
 };
 
 /* Nearest-neighbour lattice Hamiltonian (the paper's model, PAPER.md:229:
@@ -194,6 +203,30 @@ kpm_status kpm_vector_range(int64_t R, int32_t rank, int32_t world, int64_t* beg
  * Host mu[N], omega[K] -> host rho[K]; computed on `device`. */
 kpm_status kpm_dos(const double* mu, int32_t N, int32_t kernel, double a, double b,
                    const double* omega, int64_t K, double* rho, int32_t device);
+
+/* Eq (6) with any kernel: as kpm_dos, with the Lorentz parameter lambda (> 0; ignored by the
+ * other kernels). */
+kpm_status kpm_dos_ex(const double* mu, int32_t N, int32_t kernel, double lambda, double a, double b,
+                      const double* omega, int64_t K, double* rho, int32_t device);
+
+/* Retarded Green's function from the damped moments (the paper's "Green's functions",
+ * PAPER.md:23; expansion of ref [10]; X24): G(omega) = (1/D) Tr 1/(omega + i0 - H)
+ * for DoS moments (or <i|1/(omega + i0 - H)|i> for local moments), with x = (omega - b)/a,
+ * c_0 = g_0 mu_0, c_n = 2 g_n mu_n:
+ *   |x| < 1: G = -i sum_n c_n e^{-i n arccos x} / (a sqrt(1 - x^2))   (Im G = -pi rho)
+ *   |x| > 1: G = sum_n c_n t^n / (a sgn(x) sqrt(x^2 - 1)), t = x - sgn(x) sqrt(x^2 - 1)  (real)
+ *   |x| = 1: NaN.
+ * Host mu[N], omega[K] -> host G[K][2] = (Re, Im); computed on `device`. */
+kpm_status kpm_green(const double* mu, int32_t N, int32_t kernel, double lambda, double a, double b,
+                     const double* omega, int64_t K, double* G, int32_t device);
+
+/* Damping factors g[0..N-1] of `kernel` (host output; computed on `device`). */
+kpm_status kpm_damping(int32_t N, int32_t kernel, double lambda, double* g, int32_t device);
+
+/* Local moments mu_n^(i) = <i|T_n(H~)|i> of the global sites i = sites[0..nsites-1] (local DoS;
+ * SURVEY.md 8(f) NEXT-1): kpm_moments_ex(h, N, nsites, 0, sites, KPM_LOCAL, out), out host
+ * [nsites_local][N].  With KPM_PART_VECTORS the sites are split like vectors. */
+kpm_status kpm_moments_local(kpm_handle h, int32_t N, const int64_t* sites, int64_t nsites, double* out);
 
 /* ---- introspection ---------------------------------------------------------------- */
 

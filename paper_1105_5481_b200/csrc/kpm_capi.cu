@@ -130,7 +130,7 @@ struct Plan {
     int xpad = 0;            // 3D stencils: x-row frame of periodic images (row pitch L0 + 2 xpad)
     size_t mem_sites = 0;    // memory sites of the local block (with frames, without ghost planes)
     size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
-           total = 0;
+           off_sites = 0, total = 0;
 };
 
 bool is_cplx(const kpm_handle_s* h) { return h->dtype == KPM_COMPLEX128; }
@@ -294,6 +294,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_Sv = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
     p->off_S = off; off = align_up(off + (size_t)N * sizeof(double));
     p->off_out = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
+    p->off_sites = off; off = align_up(off + ((flags & KPM_LOCAL) ? (size_t)R * sizeof(long long) : 0));
     p->total = off;
     if (h->D * (long long)p->RG > (1LL << 40)) return fail(KPM_ERR_INVALID_ARG, "problem too large");
     return KPM_OK;
@@ -707,6 +708,8 @@ struct Run {
     int64_t R = 0;
     uint32_t flags = 0;
     const void* r0 = nullptr;
+    const int64_t* local_sites = nullptr;  // KPM_LOCAL: host list of R global sites
+    long long* d_sites = nullptr;
     bool cplx = false, direct = false;
     double2 *P = nullptr, *C = nullptr, *Rb = nullptr, *X2 = nullptr, *X3 = nullptr;  // interiors
     double *part = nullptr, *Sv = nullptr, *S = nullptr, *dout = nullptr;
@@ -736,6 +739,20 @@ struct Run {
         R = R_;
         flags = flags_;
         r0 = r0_;
+        if (flags & KPM_LOCAL) {
+            // unit start vectors e_site: r0 is the host list of R global sites (not a vector block)
+            if (!r0) return fail(KPM_ERR_INVALID_ARG, "KPM_LOCAL needs the site list in r0");
+            if (flags & (KPM_RAW_SUMS | KPM_DEVICE_IN))
+                return fail(KPM_ERR_INVALID_ARG, "KPM_LOCAL: per-site host list only (no raw sums, no device r0)");
+            const int64_t* st = static_cast<const int64_t*>(r0);
+            for (int64_t i = 0; i < R_; ++i)
+                if (st[i] < 0 || st[i] >= h->D_total)
+                    return fail(KPM_ERR_INVALID_ARG, "KPM_LOCAL: site %lld out of range [0, %lld)", (long long)st[i],
+                                (long long)h->D_total);
+            local_sites = st;
+            r0 = nullptr;
+            flags |= KPM_PER_VECTOR;
+        }
         if ((flags & KPM_PER_VECTOR) && (flags & KPM_RAW_SUMS))
             return fail(KPM_ERR_INVALID_ARG, "KPM_PER_VECTOR and KPM_RAW_SUMS are exclusive");
         KPM_CUDA(cudaSetDevice(h->device));
@@ -745,6 +762,12 @@ struct Run {
             // four vector blocks do not fit: fall back to in-place single steps (two blocks)
             KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p, true));
             KPM_TRY(ensure_workspace(h, p.total));
+        }
+        v.sites = nullptr;
+        if (local_sites) {
+            d_sites = reinterpret_cast<long long*>(h->ws + p.off_sites);
+            KPM_CUDA(cudaMemcpyAsync(d_sites, local_sites, (size_t)R * sizeof(long long), cudaMemcpyHostToDevice, h->stream));
+            v.sites = d_sites;
         }
         cplx = is_cplx(h);
         direct = (flags & KPM_DIRECT) != 0;
@@ -992,7 +1015,7 @@ struct Run {
         } else if (flags & KPM_PER_VECTOR) {
             const long long ne = (long long)N * p.R_loc;
             kpm::assemble_pervec_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, h->stream>>>(
-                Sv, N, p.R_loc, 1.0 / (double)h->D_total, direct, dout);
+                Sv, N, p.R_loc, local_sites ? 1.0 : 1.0 / (double)h->D_total, direct, dout);
             KPM_CUDA(cudaGetLastError());
             h->total_launches++;
             src = dout;
@@ -1434,28 +1457,76 @@ kpm_status kpm_vector_range(int64_t R, int32_t rank, int32_t world, int64_t* beg
     return KPM_OK;
 }
 
-kpm_status kpm_dos(const double* mu, int32_t N, int32_t kernel, double a, double b, const double* omega, int64_t K,
-                   double* rho, int32_t device) {
-    if (!mu || !omega || !rho || N < 1 || K < 0) return fail(KPM_ERR_INVALID_ARG, "bad kpm_dos arguments");
-    if (kernel != KPM_KERNEL_JACKSON && kernel != KPM_KERNEL_NONE) return fail(KPM_ERR_INVALID_ARG, "bad kernel %d", kernel);
+}  // extern "C"
+
+namespace {
+// Eq (6) on the device: c_n from mu and the kernel, then rho (what = 0) or G (what = 1) at the
+// K energies.  Host in/out; scratch from cudaMalloc (not on the hot path).
+kpm_status expand(const char* fn, int what, const double* mu, int32_t N, int32_t kernel, double lam, double a,
+                  double b, const double* omega, int64_t K, double* out, int32_t device) {
+    if (!mu || !omega || !out || N < 1 || K < 0) return fail(KPM_ERR_INVALID_ARG, "%s: bad arguments", fn);
+    if (kernel < KPM_KERNEL_JACKSON || kernel > KPM_KERNEL_FEJER) return fail(KPM_ERR_INVALID_ARG, "%s: bad kernel %d", fn, kernel);
+    if (kernel == KPM_KERNEL_LORENTZ && !(lam > 0.0 && std::isfinite(lam)))
+        return fail(KPM_ERR_INVALID_ARG, "%s: Lorentz kernel needs lambda > 0 (got %g)", fn, lam);
     KPM_TRY(check_ab(a, b));
     if (K == 0) return KPM_OK;
     KPM_CUDA(cudaSetDevice(device));
+    const size_t outw = what == 1 ? 2 : 1;
     double* buf = nullptr;
-    const size_t bytes = (2 * (size_t)N + 2 * (size_t)K) * sizeof(double);
+    const size_t bytes = (2 * (size_t)N + (1 + outw) * (size_t)K) * sizeof(double);
     KPM_CUDA(cudaMalloc(&buf, bytes));
-    double *dmu = buf, *dc = buf + N, *dom = buf + 2 * N, *drho = buf + 2 * N + K;
+    double *dmu = buf, *dc = buf + N, *dom = buf + 2 * N, *dout = buf + 2 * N + K;
     cudaError_t e = cudaMemcpy(dmu, mu, N * sizeof(double), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(dom, omega, K * sizeof(double), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) {
-        kpm::dos_coeff_kernel<<<(N + 255) / 256, 256>>>(dmu, N, kernel == KPM_KERNEL_JACKSON, dc);
-        kpm::dos_kernel<<<(unsigned)((K + 255) / 256), 256>>>(dc, N, a, b, dom, K, drho);
+        kpm::dos_coeff_kernel<<<(N + 255) / 256, 256>>>(dmu, N, kernel, lam, dc);
+        if (what == 1) kpm::green_kernel<<<(unsigned)((K + 255) / 256), 256>>>(dc, N, a, b, dom, K, dout);
+        else kpm::dos_kernel<<<(unsigned)((K + 255) / 256), 256>>>(dc, N, a, b, dom, K, dout);
         e = cudaGetLastError();
     }
-    if (e == cudaSuccess) e = cudaMemcpy(rho, drho, K * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(out, dout, outw * K * sizeof(double), cudaMemcpyDeviceToHost);
     cudaFree(buf);
-    if (e != cudaSuccess) return fail(KPM_ERR_CUDA, "kpm_dos: %s", cudaGetErrorString(e));
+    if (e != cudaSuccess) return fail(KPM_ERR_CUDA, "%s: %s", fn, cudaGetErrorString(e));
     return KPM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+kpm_status kpm_dos(const double* mu, int32_t N, int32_t kernel, double a, double b, const double* omega, int64_t K,
+                   double* rho, int32_t device) {
+    return expand("kpm_dos", 0, mu, N, kernel, KPM_LORENTZ_DEFAULT_LAMBDA, a, b, omega, K, rho, device);
+}
+
+kpm_status kpm_dos_ex(const double* mu, int32_t N, int32_t kernel, double lambda, double a, double b,
+                      const double* omega, int64_t K, double* rho, int32_t device) {
+    return expand("kpm_dos_ex", 0, mu, N, kernel, lambda, a, b, omega, K, rho, device);
+}
+
+kpm_status kpm_green(const double* mu, int32_t N, int32_t kernel, double lambda, double a, double b,
+                     const double* omega, int64_t K, double* G, int32_t device) {
+    return expand("kpm_green", 1, mu, N, kernel, lambda, a, b, omega, K, G, device);
+}
+
+kpm_status kpm_damping(int32_t N, int32_t kernel, double lambda, double* g, int32_t device) {
+    if (!g || N < 1) return fail(KPM_ERR_INVALID_ARG, "kpm_damping: bad arguments");
+    if (kernel < KPM_KERNEL_JACKSON || kernel > KPM_KERNEL_FEJER) return fail(KPM_ERR_INVALID_ARG, "bad kernel %d", kernel);
+    if (kernel == KPM_KERNEL_LORENTZ && !(lambda > 0.0 && std::isfinite(lambda)))
+        return fail(KPM_ERR_INVALID_ARG, "Lorentz kernel needs lambda > 0");
+    KPM_CUDA(cudaSetDevice(device));
+    double* d = nullptr;
+    KPM_CUDA(cudaMalloc(&d, N * sizeof(double)));
+    kpm::dos_coeff_kernel<<<(N + 255) / 256, 256>>>(nullptr, N, kernel, lambda, d);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaMemcpy(g, d, N * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(KPM_ERR_CUDA, "kpm_damping: %s", cudaGetErrorString(e));
+    return KPM_OK;
+}
+
+kpm_status kpm_moments_local(kpm_handle h, int32_t N, const int64_t* sites, int64_t nsites, double* out) {
+    if (!sites) return fail(KPM_ERR_INVALID_ARG, "kpm_moments_local: NULL sites");
+    return kpm_moments_ex(h, N, nsites, 0, sites, KPM_LOCAL, out);
 }
 
 kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launches, int32_t* total_launches) {

@@ -148,6 +148,7 @@ struct VecArgs {
     long long r_off;       // global index of this GPU's first vector
     long long D_total;     // global number of sites (RNG counter stride)
     long long i_off;       // global index of this GPU's site 0
+    const long long* sites;// KPM_LOCAL: global site of each global vector (unit start vectors e_site), else nullptr
     int ghost;             // row partition: site indices j < 0 or >= D are ghost sites (wrap globally)
     int L0;                // x extent
     int xpad;              // 3D lattices: 2 -- vector blocks store each x-row with a 2-site frame of
@@ -184,6 +185,10 @@ template <bool CPLX>
 __device__ __forceinline__ double2 gen_lane(const VecArgs& v, int j, int rg) {
     long long ig = v.i_off + j;
     if (v.ghost) ig = (ig % v.D_total + v.D_total) % v.D_total;  // ghost plane of a neighbouring slab
+    if (v.sites) {  // unit start vectors |r> = e_{site(r)} (local DoS)
+        auto unit = [&](long long r) { return (r < v.R_loc && __ldg(v.sites + v.r_off + r) == ig) ? 1.0 : 0.0; };
+        return CPLX ? make_double2(unit(rg), 0.0) : make_double2(unit(2LL * rg), unit(2LL * rg + 1));
+    }
     const uint64_t i = (uint64_t)ig;
     if (CPLX) {
         const long long r = rg;
@@ -340,19 +345,27 @@ __global__ void assemble_pervec_kernel(const double* __restrict__ Sv, int N, lon
     pv[e] = assemble_one(Sv + v, R_loc, n, c, direct);
 }
 
-// ------------------------------------------------------------ DoS (Eq 6)
-// c_n = g_n mu_n (n = 0), 2 g_n mu_n (n >= 1); Jackson g_n (X8).
-__global__ void dos_coeff_kernel(const double* __restrict__ mu, int N, int jackson, double* __restrict__ c) {
-    const int n = blockIdx.x * blockDim.x + threadIdx.x;
-    if (n >= N) return;
-    double g = 1.0;
-    if (jackson) {
+// ------------------------------------------------------------ DoS (Eq 6), Green's function
+// Damping factors g_n of Eq (6) (X8, X26):
+//   0 Jackson, 1 none (g = 1), 2 Lorentz sinh(lam (1 - n/N)) / sinh(lam), 3 Fejer 1 - n/N.
+__device__ __forceinline__ double damping(int n, int N, int kernel, double lam) {
+    if (kernel == 0) {
         const double q = CUDART_PI / (N + 1);
         double sn, cn;
         sincospi((double)n / (N + 1), &sn, &cn);
-        g = ((N - n + 1) * cn + sn * (cos(q) / sin(q))) / (N + 1);
+        return ((N - n + 1) * cn + sn * (cos(q) / sin(q))) / (N + 1);
     }
-    c[n] = (n == 0 ? 1.0 : 2.0) * g * mu[n];
+    if (kernel == 2) return sinh(lam * (1.0 - (double)n / N)) / sinh(lam);
+    if (kernel == 3) return 1.0 - (double)n / N;
+    return 1.0;
+}
+
+// c_n = g_n mu_n (n = 0), 2 g_n mu_n (n >= 1); mu == nullptr gives g_n itself.
+__global__ void dos_coeff_kernel(const double* __restrict__ mu, int N, int kernel, double lam, double* __restrict__ c) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    const double g = damping(n, N, kernel, lam);
+    c[n] = mu ? (n == 0 ? 1.0 : 2.0) * g * mu[n] : g;
 }
 
 // rho(omega) = sum_n c_n T_n(x) / (pi a sqrt(1 - x^2)), x = (omega - b)/a; T_n by Eq (4)-(5).
@@ -375,6 +388,51 @@ __global__ void dos_kernel(const double* __restrict__ c, int N, double a, double
         t1 = t2;
     }
     rho[k] = s / (CUDART_PI * a * sqrt(1.0 - x * x));
+}
+
+// Retarded G(omega) = G~(x)/a (X24).  Inside (|x| < 1), with
+// e^{-i n theta} = T_n(x) - i sin(theta) U_{n-1}(x):
+//   Re G~ = -sum_{n>=1} c_n U_{n-1}(x),   Im G~ = -sum_n c_n T_n(x) / sqrt(1 - x^2)
+// (T and U by the three-term recurrence, Eq 5).  Outside: G~ = sum_n c_n t^n / (sgn(x)
+// sqrt(x^2 - 1)), t = x - sgn(x) sqrt(x^2 - 1) (Horner).  |x| = 1: NaN.  G is [K][2] (re, im).
+__global__ void green_kernel(const double* __restrict__ c, int N, double a, double b, const double* __restrict__ omega,
+                             long long K, double* __restrict__ G) {
+    const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (k >= K) return;
+    const double x = (omega[k] - b) / a;
+    double re, im;
+    if (fabs(x) < 1.0) {
+        double t0 = 1.0, t1 = x, u0 = 1.0, u1 = 2.0 * x;  // T_0, T_1, U_0, U_1
+        double st = c[0], su = 0.0;
+        if (N > 1) {
+            st = fma(c[1], t1, st);
+            su = c[1] * u0;
+        }
+        for (int n = 2; n < N; ++n) {
+            const double t2 = fma(2.0 * x, t1, -t0);
+            st = fma(c[n], t2, st);
+            su = fma(c[n], u1, su);  // U_{n-1}
+            const double u2 = fma(2.0 * x, u1, -u0);
+            t0 = t1;
+            t1 = t2;
+            u0 = u1;
+            u1 = u2;
+        }
+        re = -su;
+        im = -st / sqrt(1.0 - x * x);
+    } else if (fabs(x) > 1.0) {
+        const double sg = x > 0 ? 1.0 : -1.0;
+        const double sq = sqrt(x * x - 1.0);
+        const double t = x - sg * sq;
+        double s = 0.0;
+        for (int n = N - 1; n >= 0; --n) s = fma(s, t, c[n]);
+        re = s / (sg * sq);
+        im = 0.0;
+    } else {
+        re = im = CUDART_NAN;
+    }
+    G[2 * k] = re / a;
+    G[2 * k + 1] = im / a;
 }
 
 }  // namespace kpm

@@ -4,7 +4,8 @@ Every step of the method runs in the CUDA kernels behind the C ABI; nothing
 here computes moments.  If libkpm.so is missing this module raises on import
 (there is no CPU fallback).  Names follow the C ABI: kpm_create_stencil,
 kpm_create_csr, kpm_create_ell, kpm_gershgorin_stencil, kpm_gershgorin_csr,
-kpm_moments, kpm_moments_ex, kpm_assemble, kpm_dos, kpm_workspace_size,
+kpm_moments, kpm_moments_ex, kpm_moments_local, kpm_assemble, kpm_dos, kpm_dos_ex,
+kpm_green, kpm_damping, kpm_workspace_size,
 kpm_set_workspace, kpm_set_stream, kpm_last_timing, kpm_step_bytes,
 kpm_destroy, kpm_last_error, kpm_version.
 """
@@ -24,8 +25,9 @@ _lib = ctypes.CDLL(LIB_PATH)
 
 KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM_ERR_SPECTRUM = range(6)
 KPM_REAL64, KPM_COMPLEX128 = 0, 1
-KPM_KERNEL_JACKSON, KPM_KERNEL_NONE = 0, 1
-KPM_PER_VECTOR, KPM_DIRECT, KPM_DEVICE_OUT, KPM_RAW_SUMS, KPM_DEVICE_IN = 1, 2, 4, 8, 16
+KPM_KERNEL_JACKSON, KPM_KERNEL_NONE, KPM_KERNEL_LORENTZ, KPM_KERNEL_FEJER = 0, 1, 2, 3
+KPM_LORENTZ_DEFAULT_LAMBDA = 4.0
+KPM_PER_VECTOR, KPM_DIRECT, KPM_DEVICE_OUT, KPM_RAW_SUMS, KPM_DEVICE_IN, KPM_LOCAL = 1, 2, 4, 8, 16, 32
 KPM_PART_NONE, KPM_PART_VECTORS, KPM_PART_ROWS = 0, 1, 2
 KPM_COMM_SELF, KPM_COMM_NCCL, KPM_COMM_LOCAL = 0, 1, 2
 
@@ -33,7 +35,8 @@ EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershg
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
-           "kpm_moments_group", "kpm_destroy", "kpm_last_error", "kpm_version"]
+           "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moments_local", "kpm_destroy",
+           "kpm_last_error", "kpm_version"]
 
 
 class kpm_stencil_desc(ctypes.Structure):
@@ -62,6 +65,10 @@ _SIG = {
     "kpm_assemble": [_P, _P, _i32, _i64, _i64, _u32, _P],
     "kpm_vector_range": [_i64, _i32, _i32, _P, _P],
     "kpm_dos": [_P, _i32, _i32, _f64, _f64, _P, _i64, _P, _i32],
+    "kpm_dos_ex": [_P, _i32, _i32, _f64, _f64, _f64, _P, _i64, _P, _i32],
+    "kpm_green": [_P, _i32, _i32, _f64, _f64, _f64, _P, _i64, _P, _i32],
+    "kpm_damping": [_i32, _i32, _f64, _P, _i32],
+    "kpm_moments_local": [_P, _i32, _P, _i64, _P],
     "kpm_last_timing": [_P, _P, _P, _P],
     "kpm_step_bytes": [_P, _P],
     "kpm_plan_info": [_P, _i32, _i64, _u32, _P],
@@ -213,6 +220,13 @@ class Handle:
         _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags), _ptr(res)))
         return res
 
+    def moments_local(self, N, sites):
+        sites = np.ascontiguousarray(sites, dtype=np.int64)
+        _, n_loc = self.r_local(len(sites))
+        res = np.zeros((n_loc, int(N)), dtype=np.float64)
+        _check(_lib.kpm_moments_local(self._h, int(N), _ptr(sites), len(sites), _ptr(res)))
+        return res
+
     def assemble(self, S, N, R, flags=0, out=None):
         """Raw sums -> moments (kpm_assemble); S: host array, or int device pointer with out."""
         if isinstance(S, (int, np.integer)):
@@ -350,6 +364,36 @@ def kpm_dos(mu, a, b, omega, kernel=KPM_KERNEL_JACKSON, device=0):
     _check(_lib.kpm_dos(_ptr(mu), len(mu), int(kernel), float(a), float(b), _ptr(om), len(om), _ptr(rho),
                         int(device)))
     return rho
+
+
+def kpm_dos_ex(mu, a, b, omega, kernel=KPM_KERNEL_JACKSON, lam=KPM_LORENTZ_DEFAULT_LAMBDA, device=0):
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    om = np.ascontiguousarray(omega, dtype=np.float64)
+    rho = np.zeros(len(om), dtype=np.float64)
+    _check(_lib.kpm_dos_ex(_ptr(mu), len(mu), int(kernel), float(lam), float(a), float(b), _ptr(om), len(om),
+                           _ptr(rho), int(device)))
+    return rho
+
+
+def kpm_green(mu, a, b, omega, kernel=KPM_KERNEL_JACKSON, lam=KPM_LORENTZ_DEFAULT_LAMBDA, device=0):
+    """Retarded Green's function G(omega) (complex128[K]) from the damped moments."""
+    mu = np.ascontiguousarray(mu, dtype=np.float64)
+    om = np.ascontiguousarray(omega, dtype=np.float64)
+    G = np.zeros(2 * len(om), dtype=np.float64)
+    _check(_lib.kpm_green(_ptr(mu), len(mu), int(kernel), float(lam), float(a), float(b), _ptr(om), len(om),
+                          _ptr(G), int(device)))
+    return G[0::2] + 1j * G[1::2]
+
+
+def kpm_damping(N, kernel=KPM_KERNEL_JACKSON, lam=KPM_LORENTZ_DEFAULT_LAMBDA, device=0):
+    g = np.zeros(int(N), dtype=np.float64)
+    _check(_lib.kpm_damping(int(N), int(kernel), float(lam), _ptr(g), int(device)))
+    return g
+
+
+def kpm_moments_local(h: Handle, N, sites):
+    """<i|T_n(H~)|i> for the global sites i (this rank's share under KPM_PART_VECTORS)."""
+    return h.moments_local(N, sites)
 
 
 def kpm_destroy(h: Handle):
