@@ -207,6 +207,11 @@ class Handle:
             r0p = None
         elif isinstance(r0, (int, np.integer)):
             r0p = ctypes.c_void_p(int(r0))
+        elif flags & KPM_LOCAL:  # host list of R global sites
+            keep = np.ascontiguousarray(r0, dtype=np.int64)
+            assert keep.shape == (int(R),), keep.shape
+            r0p = _ptr(keep)
+            R_loc = self.r_local(R)[1]
         else:
             keep = np.ascontiguousarray(r0, dtype=np.float64)
             assert keep.shape == (R_loc, self.D_local), (keep.shape, (R_loc, self.D_local))
@@ -215,7 +220,7 @@ class Handle:
             _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags),
                                        ctypes.c_void_p(int(out))))
             return None
-        shape = (R_loc, int(N)) if flags & KPM_PER_VECTOR else (int(N),)
+        shape = (R_loc, int(N)) if flags & (KPM_PER_VECTOR | KPM_LOCAL) else (int(N),)
         res = np.zeros(shape, dtype=np.float64)
         _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags), _ptr(res)))
         return res

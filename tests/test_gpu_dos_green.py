@@ -1,8 +1,10 @@
 """GPU parity of SURVEY.md 8(f) NEXT-1 (through the C ABI) against the CPU oracle:
 damping kernels (Eq 6-7 with the kernels of ref [10]), the DoS with every kernel, the
 retarded Green's function (reading X24), and local moments <i|T_n(H~)|i> from unit start
-vectors (KPM_LOCAL).  Tolerances: reading X17 (normwise 1e-10) for moments; the
-expansions are O(N) fp64 sums per energy, compared at 1e-12 relative to max |value|."""
+vectors (KPM_LOCAL).  Tolerances: reading X17 (normwise 1e-10) for moments.  The expansions
+evaluate T_n (and U_n) by the three-term recurrence (Eq 5) on the GPU and by cos(n arccos x)
+in the oracle; the recurrence's rounding error grows like n^2 eps near x = +-1, so the bar is
+N^2 eps sum|c_n| / max|value| <~ 1e-10 for N <= 1000 (X27), written as 1e-10."""
 import numpy as np
 import pytest
 
@@ -47,7 +49,7 @@ def test_dos_every_kernel_matches_oracle(kpm, name):
     mu = oracle.moments_doubling(H, a, b, ki.rademacher(3, 6, lat["D"]), 200)
     om = np.concatenate([np.linspace(b - 1.2 * a, b + 1.2 * a, 301), [b - a, b + a]])
     rho = kpm.kpm_dos_ex(mu, a, b, om, kernel=KERNELS[name], lam=3.0)
-    assert rel(rho, oracle.dos(mu, a, b, om, kernel=name, lam=3.0)) < 1e-12
+    assert rel(rho, oracle.dos(mu, a, b, om, kernel=name, lam=3.0)) < 1e-10
     if name == "jackson":
         assert np.array_equal(rho, kpm.kpm_dos(mu, a, b, om))
 
@@ -62,12 +64,12 @@ def test_green_matches_oracle_inside_and_outside(kpm, name):
                          b + a * np.array([-3.0, -1.5, -1.001, 1.001, 1.2, 4.0])])
     G = kpm.kpm_green(mu, a, b, om, kernel=KERNELS[name], lam=4.0)
     ref = oracle.green(mu, a, b, om, kernel=name, lam=4.0)
-    assert rel(G.real, ref.real) < 1e-11 and rel(G.imag, ref.imag) < 1e-12
+    assert rel(G.real, ref.real) < 1e-10 and rel(G.imag, ref.imag) < 1e-10
     assert np.all(np.isnan(kpm.kpm_green(mu, a, b, [b - a, b + a], kernel=KERNELS[name])))
     # Im G = -pi rho (same kernel)
     ins = np.abs(om - b) < a
     rho = kpm.kpm_dos_ex(mu, a, b, om[ins], kernel=KERNELS[name], lam=4.0)
-    assert rel(-G.imag[ins] / np.pi, rho) < 1e-12
+    assert rel(-G.imag[ins] / np.pi, rho) < 1e-12  # same recurrence on both
 
 
 LOCAL_CASES = {
