@@ -150,11 +150,22 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
                           double a, double b, int32_t device, const kpm_dist* dist,
                           kpm_handle* out);
 
+/* H given DENSE (the paper's own variant: "when H is considered as a dense matrix,
+ * the complexity of the part becomes O(D^2)"; H_SIZE experiments PAPER.md:241-253): row-major
+ * D x D doubles (KPM_REAL64 only; complex -> KPM_ERR_UNSUPPORTED), Hermitian (not checked),
+ * D <= 131072.  Stored on the device pre-scaled by 1/a and zero padded to a multiple of 64;
+ * each recursion step is a DMMA (fp64 tensor-core) GEMM with the recursion and the moment sums
+ * fused into its epilogue (kpm_dense.cuh).  Partitions: none or KPM_PART_VECTORS.
+ * KPM_DIRECT is not implemented for dense H (KPM_ERR_UNSUPPORTED). */
+kpm_status kpm_create_dense(int64_t D, const void* H, int32_t dtype, double a, double b, int32_t device,
+                            const kpm_dist* dist, kpm_handle* out);
+
 /* Gerschgorin bounds: E_upper = max_i (Re H_ii + sum_{j!=i} |H_ij|),
  * E_lower = min_i (...); eps pads both (0 = none); returns a = (Eu-El)/2, b = (Eu+El)/2. */
 kpm_status kpm_gershgorin_stencil(const kpm_stencil_desc* desc, double eps, double* a, double* b);
 kpm_status kpm_gershgorin_csr(int64_t D, const int64_t* rowptr, const int32_t* col,
                               const void* val, int32_t dtype, double eps, double* a, double* b);
+kpm_status kpm_gershgorin_dense(int64_t D, const void* H, int32_t dtype, double eps, double* a, double* b);
 
 /* ---- execution ------------------------------------------------------------------- */
 

@@ -92,7 +92,23 @@ CONFIGS = {
                disorder_seed=0, flux=0.125, N=4096, R=256, seed=4),
     "c5": dict(name="3D Anderson 512^3 W=2", ndim=3, L=(512, 512, 512), t=-1.0, W=2.0,
                disorder_seed=105, flux=0.0, N=1024, R=32, seed=5),
+    # the paper's own dense-H experiment (Exp IV.C largest point: H_SIZE = 4096,
+    # R*S = 14*128 = 1792, N = 128) on its model lattice (3D cubic, t = -1, periodic; 16^3 = 4096)
+    "pd": dict(name="paper Exp IV.C: dense H_SIZE=4096 (3D 16^3), RS=1792, N=128", ndim=3, L=(16, 16, 16),
+               t=-1.0, W=0.0, disorder_seed=0, flux=0.0, N=128, R=1792, seed=6, format="dense"),
 }
+
+
+def lattice_dense(lat: dict) -> np.ndarray:
+    """The lattice Hamiltonian as a dense row-major D x D array (input construction for
+    kpm_create_dense; real lattices only)."""
+    rowptr, col, val = lattice_csr(lat)
+    assert not np.iscomplexobj(val), "dense input: real H only"
+    D = len(rowptr) - 1
+    H = np.zeros((D, D))
+    rows = np.repeat(np.arange(D), np.diff(rowptr))
+    np.add.at(H, (rows, col), val)
+    return H
 
 
 def num_sites(L) -> int:

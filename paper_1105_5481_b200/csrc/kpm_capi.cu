@@ -26,6 +26,7 @@
 #include "kpm_tmak.cuh"
 #include "kpm_ell.cuh"
 #include "kpm_small.cuh"
+#include "kpm_dense.cuh"
 
 namespace {
 
@@ -55,7 +56,7 @@ kpm_status fail(kpm_status st, const char* fmt, ...) {
         if (s_ != KPM_OK) return s_;         \
     } while (0)
 
-enum Kind { KIND_STENCIL = 0, KIND_ELL = 1 };
+enum Kind { KIND_STENCIL = 0, KIND_ELL = 1, KIND_DENSE = 2 };
 constexpr int kThreads = 512;     // threads per CTA of the step kernels
 constexpr size_t kAlign = 256;
 
@@ -81,6 +82,9 @@ struct kpm_handle_s {
     int K = 0;
     int32_t* d_col = nullptr;
     double* d_val = nullptr;
+    // dense H~ (the paper's variant): Dp x Dp row-major, H / a, zero padded (kpm_dense.cuh)
+    double* d_dense = nullptr;
+    int64_t Dp = 0;
     // partition
     kpm_dist dist{KPM_PART_NONE, 0, 1, KPM_COMM_SELF, nullptr};
     // row partition (KPM_PART_ROWS): slab [z0, z0 + nloc) of the slowest dimension `slow`;
@@ -252,6 +256,10 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->R_loc < 1) return fail(KPM_ERR_INVALID_ARG, "rank %d of %d owns no vectors (R=%lld)", rank, world, (long long)R);
     p->RG = is_cplx(h) ? (int)p->R_loc : (int)((p->R_loc + 1) / 2);
     p->RP = is_cplx(h) ? p->RG : 2 * p->RG;
+    if (h->kind == KIND_DENSE) {  // GEMM tiles: vectors padded to 64 (zero columns)
+        p->RP = (int)((p->R_loc + kpm::kDBN - 1) / kpm::kDBN * kpm::kDBN);
+        p->RG = p->RP / 2;
+    }
     int tr = 1;
     while (tr < p->RG && tr < 32) tr <<= 1;
     p->TR = tr;
@@ -261,8 +269,10 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->gx = (int)std::min<long long>(site_ctas, 2LL * h->num_sms);
     plan_tma(h, flags, p);
     if (p->use_tma) p->gx = p->tma_grid;
+    if (h->kind == KIND_DENSE) p->gx = (int)(h->Dp / kpm::kDBM);  // partial rows = M tiles
     p->small_smem = 2 * (size_t)h->D * p->TR * sizeof(double2);
-    p->use_small = !h->rows && !(flags & KPM_DIRECT) && p->small_smem <= kpm::kSmallSmemMax && !env_on("KPM_NO_SMALL");
+    p->use_small = !h->rows && !(flags & KPM_DIRECT) && p->small_smem <= kpm::kSmallSmemMax && !env_on("KPM_NO_SMALL") &&
+                   h->kind != KIND_DENSE;
     if (p->use_small) {
         p->use_tma = p->use_tma2 = false;
         p->TS = kpm::kSmallThreads / p->TR;
@@ -276,6 +286,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->xpad = (h->kind == KIND_STENCIL && h->ndim == 3) ? 2 : 0;
     const size_t rows_of_x = (size_t)(h->D / h->L[0]);
     p->mem_sites = (size_t)h->D + 2 * (size_t)p->xpad * rows_of_x;
+    if (h->kind == KIND_DENSE) p->mem_sites = (size_t)h->Dp;
     const size_t plane_mem = !h->rows ? 0
                              : p->xpad ? (size_t)(h->plane / h->L[0]) * (h->L[0] + 2 * p->xpad) : (size_t)h->plane;
     p->ghost_lanes = plane_mem * p->RG;
@@ -290,7 +301,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
         p->off_X2 = off; off = align_up(off + p->lane_bytes);
         p->off_X3 = off; off = align_up(off + p->lane_bytes);
     }
-    p->off_part = off; off = align_up(off + (size_t)N * p->gx * p->RP * sizeof(double));
+    p->off_part = off; off = align_up(off + (size_t)std::max(N, 3) * p->gx * p->RP * sizeof(double));
     p->off_Sv = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
     p->off_S = off; off = align_up(off + (size_t)N * sizeof(double));
     p->off_out = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
@@ -805,6 +816,7 @@ struct Run {
         if (r0) {
             const size_t rbytes = (size_t)p.R_loc * h->D * sizeof(double);
             double* stage = reinterpret_cast<double*>(base_of(C));
+            if (h->kind == KIND_DENSE) KPM_CUDA(cudaMemsetAsync(P, 0, p.lane_bytes, h->stream));
             KPM_CUDA(cudaMemcpyAsync(stage, r0, rbytes,
                                      (flags & KPM_DEVICE_IN) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
             const long long ne = h->D * (long long)p.RG;
@@ -817,6 +829,7 @@ struct Run {
             first_mode = kpm::FIRST_BUF;
         }
         if (first_mode == kpm::FIRST_BUF && h->rows) KPM_TRY(need_exchange(P));
+        if (h->kind == KIND_DENSE) return begin_dense(first_mode);
         if (p.use_small) {  // the whole recursion in one launch (kpm_small.cuh)
             KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
             KPM_TRY(launch_small(h, p, v, first_mode == kpm::FIRST_BUF, N, part));
@@ -916,6 +929,58 @@ struct Run {
         return KPM_OK;
     }
 
+    // Dense H~ (kpm_dense.cuh): a_0 materialised (generated here, or the caller's block already
+    // loaded into P), then a_1 = H~ a_0 by the GEMM kernel with the fused sums S_0, S_1.
+    kpm_status begin_dense(int first_mode) {
+        if (direct) return fail(KPM_ERR_UNSUPPORTED, "KPM_DIRECT is not implemented for dense H");
+        if (first_mode != kpm::FIRST_BUF) {
+            const long long ne = h->Dp * (long long)p.RG;
+            const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
+            kpm::dense_gen_kernel<false><<<blocks, 256, 0, h->stream>>>(v, (int)h->Dp, P);
+            KPM_CUDA(cudaGetLastError());
+            h->total_launches++;
+        }
+        v.red0 = part;
+        v.red1 = part + slot;  // the partial buffer has >= 3 slots (slot 1 unused when N = 1)
+        v.red2 = (N == 3) ? part + 2 * slot : nullptr;
+        KPM_TRY(launch_dense(true, P, C, v.red0, v.red1, v.red2, v.red2 != nullptr));
+        nsteps = std::max(0, p.M - 1);
+        cur = C;
+        prev = P;
+        n = 1;
+        vbytes = (double)h->Dp * (double)p.RP * 8.0;
+        ebytes = 0.0;
+        mbytes = 8.0 * (double)h->Dp * (double)h->Dp;
+        KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
+        return KPM_OK;
+    }
+    kpm_status launch_dense(bool first, double2* A, double2* out, double* r0_, double* r1_, double* r2_, int tail) {
+        kpm::DenseArgs g;
+        g.H = h->d_dense;
+        g.A = reinterpret_cast<const double*>(A);
+        g.P = reinterpret_cast<double*>(out);
+        g.Dp = (int)h->Dp;
+        g.RP = p.RP;
+        g.shift = -h->b / h->a;
+        g.red0 = r0_;
+        g.red1 = r1_;
+        g.red2 = r2_;
+        dim3 grid(p.RP / kpm::kDBN, (unsigned)(h->Dp / kpm::kDBM));
+        static bool configured = false;
+        if (!configured) {
+            KPM_CUDA(cudaFuncSetAttribute(kpm::kpm_dense_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kpm::kDenseSmem));
+            KPM_CUDA(cudaFuncSetAttribute(kpm::kpm_dense_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)kpm::kDenseSmem));
+            configured = true;
+        }
+        if (first) kpm::kpm_dense_step_kernel<true><<<grid, kpm::kDThreads, kpm::kDenseSmem, h->stream>>>(g, tail);
+        else kpm::kpm_dense_step_kernel<false><<<grid, kpm::kDThreads, kpm::kDenseSmem, h->stream>>>(g, tail);
+        KPM_CUDA(cudaGetLastError());
+        h->total_launches++;
+        return KPM_OK;
+    }
+
     // ghost planes of `X` must be refreshed before the next launch (recorded; done by the caller)
     double2* pending = nullptr;
     kpm_status need_exchange(double2* X) {
@@ -928,6 +993,16 @@ struct Run {
     double2* fresh() const { return cur; }
 
     kpm_status launch_next() {
+        if (h->kind == KIND_DENSE) {  // Eq (18) as a GEMM with the fused epilogue, in place over a_{n-1}
+            const bool tail = (N & 1) && n == nsteps;
+            KPM_TRY(launch_dense(false, cur, prev, part + (size_t)(2 * n) * slot, part + (size_t)(2 * n + 1) * slot,
+                                 tail ? part + (size_t)(2 * n + 2) * slot : nullptr, tail));
+            h->steps_bytes += 3.0 * vbytes + mbytes;
+            h->step_launches++;
+            std::swap(cur, prev);
+            ++n;
+            return KPM_OK;
+        }
         if (!direct && p.use_tmak && n + p.KSK - 1 <= nsteps) {
             // steps n .. n+KS-1: slots 2n .. 2n+2KS-1 (+ odd-N tail 2(n+KS))
             const int KS = p.KSK;
@@ -1126,6 +1201,7 @@ void kpm_destroy(kpm_handle h) {
     cudaFree(h->d_phase);
     cudaFree(h->d_col);
     cudaFree(h->d_val);
+    cudaFree(h->d_dense);
     if (h->nccl) ncclCommDestroy(h->nccl);
     if (h->ev_begin) cudaEventDestroy(h->ev_begin);
     if (h->ev_end) cudaEventDestroy(h->ev_end);
@@ -1277,6 +1353,56 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
     if (st != KPM_OK) {
         kpm_destroy(h);
         return st;
+    }
+    *out = h;
+    return KPM_OK;
+}
+
+kpm_status kpm_gershgorin_dense(int64_t D, const void* H, int32_t dtype, double eps, double* a, double* b) {
+    if (D < 1 || !H || !a || !b) return fail(KPM_ERR_INVALID_ARG, "bad dense arguments");
+    if (dtype != KPM_REAL64) return fail(KPM_ERR_UNSUPPORTED, "dense H: KPM_REAL64 only");
+    const double* m = static_cast<const double*>(H);
+    double Eu = -INFINITY, El = INFINITY;
+    for (int64_t i = 0; i < D; ++i) {
+        double rad = 0.0;
+        for (int64_t j = 0; j < D; ++j)
+            if (j != i) rad += std::fabs(m[i * D + j]);
+        Eu = std::max(Eu, m[i * D + i] + rad);
+        El = std::min(El, m[i * D + i] - rad);
+    }
+    Eu += eps;
+    El -= eps;
+    *a = (Eu - El) / 2.0;
+    *b = (Eu + El) / 2.0;
+    return KPM_OK;
+}
+
+kpm_status kpm_create_dense(int64_t D, const void* H, int32_t dtype, double a, double b, int32_t device,
+                            const kpm_dist* dist, kpm_handle* out) {
+    if (D < 1 || D > (1LL << 17) || !H) return fail(KPM_ERR_INVALID_ARG, "bad dense arguments (D=%lld)", (long long)D);
+    if (dtype != KPM_REAL64) return fail(KPM_ERR_UNSUPPORTED, "dense H: KPM_REAL64 only");
+    KPM_TRY(check_ab(a, b));
+    if (dist && dist->partition == KPM_PART_ROWS)
+        return fail(KPM_ERR_UNSUPPORTED, "row partition is implemented for lattice stencils only");
+    const int64_t Dp = (D + kpm::kDBM - 1) / kpm::kDBM * kpm::kDBM;
+    std::vector<double> hp((size_t)Dp * Dp, 0.0);
+    const double* m = static_cast<const double*>(H);
+    for (int64_t i = 0; i < D; ++i)
+        for (int64_t j = 0; j < D; ++j) hp[(size_t)i * Dp + j] = m[i * D + j] / a;
+    kpm_handle_s* h = nullptr;
+    KPM_TRY(new_handle(device, dist, &h));
+    h->kind = KIND_DENSE;
+    h->D_total = D;
+    h->D = D;
+    h->Dp = Dp;
+    h->dtype = dtype;
+    h->a = a;
+    h->b = b;
+    cudaError_t ce = cudaMalloc(&h->d_dense, hp.size() * sizeof(double));
+    if (ce == cudaSuccess) ce = cudaMemcpy(h->d_dense, hp.data(), hp.size() * sizeof(double), cudaMemcpyHostToDevice);
+    if (ce != cudaSuccess) {
+        kpm_destroy(h);
+        return fail(KPM_ERR_CUDA, "dense upload: %s", cudaGetErrorString(ce));
     }
     *out = h;
     return KPM_OK;

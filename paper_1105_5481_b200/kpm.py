@@ -35,7 +35,8 @@ EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershg
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
-           "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moments_local", "kpm_destroy",
+           "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moments_local", "kpm_create_dense",
+           "kpm_gershgorin_dense", "kpm_destroy",
            "kpm_last_error", "kpm_version"]
 
 
@@ -68,6 +69,8 @@ _SIG = {
     "kpm_dos_ex": [_P, _i32, _i32, _f64, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_green": [_P, _i32, _i32, _f64, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_damping": [_i32, _i32, _f64, _P, _i32],
+    "kpm_create_dense": [_i64, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
+    "kpm_gershgorin_dense": [_i64, _P, _i32, _f64, _P, _P],
     "kpm_moments_local": [_P, _i32, _P, _i64, _P],
     "kpm_last_timing": [_P, _P, _P, _P],
     "kpm_step_bytes": [_P, _P],
@@ -283,6 +286,24 @@ def kpm_create_csr(D, rowptr, col, val, a, b, device=0, dist=None) -> Handle:
     _check(_lib.kpm_create_csr(int(D), _ptr(rowptr), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
                                dp, ctypes.byref(h)))
     return Handle(h.value, D, dist=dist)
+
+
+def kpm_create_dense(H, a, b, device=0, dist=None) -> Handle:
+    """Dense real H (row-major D x D): the paper's own variant (DMMA GEMM per step)."""
+    Hd = np.ascontiguousarray(H, dtype=np.float64)
+    D = Hd.shape[0]
+    assert Hd.shape == (D, D)
+    dp, keep = _dist(dist)
+    h = ctypes.c_void_p()
+    _check(_lib.kpm_create_dense(D, _ptr(Hd), KPM_REAL64, float(a), float(b), int(device), dp, ctypes.byref(h)))
+    return Handle(h.value, D, dist=dist)
+
+
+def kpm_gershgorin_dense(H, eps=0.0):
+    Hd = np.ascontiguousarray(H, dtype=np.float64)
+    a, b = ctypes.c_double(), ctypes.c_double()
+    _check(_lib.kpm_gershgorin_dense(Hd.shape[0], _ptr(Hd), KPM_REAL64, float(eps), ctypes.byref(a), ctypes.byref(b)))
+    return a.value, b.value
 
 
 def kpm_create_ell(D, K, col, val, a, b, device=0, dist=None) -> Handle:
