@@ -111,12 +111,30 @@ def profiled_traffic(config, plan):
     return rec["dram_bytes_per_launch"]
 
 
-def oracle_sample(cfg, lat, a, b, target_s=15.0):
+def measure_dgemm_tflops(dev, D, R, reps=10):
+    """fp64 tensor-core reference: cuBLAS DGEMM (torch.matmul on float64) of the dense step's
+    shape (D x D) x (D x R), CUDA events, after warm-up."""
+    import torch
+    A = torch.randn(D, D, dtype=torch.float64, device=dev)
+    B = torch.randn(D, R, dtype=torch.float64, device=dev)
+    C = torch.matmul(A, B)
+    torch.cuda.synchronize(dev)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        torch.matmul(A, B, out=C)
+    e1.record()
+    torch.cuda.synchronize(dev)
+    return 2.0 * D * D * R * reps / (e0.elapsed_time(e1) / 1000.0) / 1e12
+
+
+def oracle_sample(cfg, lat, a, b, target_s=15.0, dense=False):
     """The oracle as it stands, on a bounded sample of the workload: full D, R' vectors
     (one per host thread, fewer for huge D), and the first N' <= N moments chosen from a
-    short calibration run so the sample takes ~target_s.  Returns D*N'*R'/s."""
+    short calibration run so the sample takes ~target_s.  Returns D*N'*R'/s.  dense: H is
+    handed to the oracle with all D^2 entries (the dense variant's arithmetic)."""
     import oracle
-    H = oracle.lattice_csr(lat)
+    H = oracle.csr_from_dense(ki.lattice_dense(lat), keep_zeros=True) if dense else oracle.lattice_csr(lat)
     threads = oracle.num_threads()
     D = lat["D"]
     Rs = threads if D <= (1 << 24) else max(1, min(threads, 4))
@@ -158,7 +176,9 @@ def run_reference(args, cfg, lat, a, b, rank, world):
 
 def config_obj(args, cfg, lat, world):
     rows = getattr(args, "partition", "vectors") == "rows"
-    return {"workload": f"BASELINE.json configs[{int(args.config[1]) - 1}]: {cfg['name']}", "config": args.config,
+    wl = (f"BASELINE.json configs[{int(args.config[1]) - 1}]: {cfg['name']}" if args.config.startswith("c")
+          else cfg["name"])
+    return {"workload": wl, "config": args.config,
             "D": lat["D"], "N": cfg["N"], "R_per_gpu": cfg["R"] if not rows else None,
             "R_total": cfg["R"] * (1 if rows else world), "ndim": lat["ndim"],
             "L": list(lat["L"]), "t": lat["t"], "anderson_W": cfg["W"], "flux": lat["flux"],
@@ -177,9 +197,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--format", default="stencil", choices=["stencil", "csr"],
-                    help="how H reaches the library: lattice-stencil descriptor, or the same H as CSR "
-                         "(kpm_create_csr -> ELL; general sparse path)")
+    ap.add_argument("--format", default=None, choices=["stencil", "csr", "dense"],
+                    help="how H reaches the library: lattice-stencil descriptor, the same H as CSR "
+                         "(kpm_create_csr -> ELL; general sparse path), or dense (the paper's own variant; "
+                         "default for config pd)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: all-reduce through host memory; lets several "
                          "ranks share one GPU to test the multi-rank path)")
@@ -194,6 +215,8 @@ def main():
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = ki.CONFIGS[args.config]
     lat = ki.lattice(cfg)
+    if args.format is None:
+        args.format = cfg.get("format", "stencil")
 
     if args.impl == "reference":
         import oracle
@@ -217,7 +240,7 @@ def main():
     N, R_loc = cfg["N"], cfg["R"]
     rows = args.partition == "rows"
     if rows or args.format == "csr":
-        args.no_e2e = True  # (e2e below re-creates a plain stencil handle)
+        args.no_e2e = True  # (e2e below re-creates a stencil or dense handle)
     if rows:
         if world == 1:
             dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % (29500 + os.getpid() % 1000),
@@ -227,11 +250,17 @@ def main():
     else:
         R = R_loc * world
         part = (kpm.KPM_PART_VECTORS, rank, world)
+    Hd = None
     if args.format == "csr":
         assert not rows, "the row partition is implemented for stencils"
         rowptr, col, val = ki.lattice_csr(lat)
         a, b = kpm.kpm_gershgorin_csr(lat["D"], rowptr, col, val)
         h = kpm.kpm_create_csr(lat["D"], rowptr, col, val, a, b, device=local_rank, dist=part)
+    elif args.format == "dense":
+        assert not rows, "the row partition is implemented for stencils"
+        Hd = ki.lattice_dense(lat)
+        a, b = kpm.kpm_gershgorin_dense(Hd)
+        h = kpm.kpm_create_dense(Hd, a, b, device=local_rank, dist=part)
     else:
         h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
                                    device=local_rank, dist=part)
@@ -293,9 +322,11 @@ def main():
 
     # roofline of the dominant kernel: the fused recursion step
     peak, peak_kind = peak_hbm()
-    plan = h.plan_info(N, R)
+    plan = h.plan_info(N, R) if args.format != "dense" else {"dense": 1, "tile": "64x64x32 DMMA m8n8k4"}
     kname = ("kpm_step_kernel<EllOp> (ELL SpMM over the vector block + recursion + reductions)"
              if args.format == "csr" else
+             "kpm_dense_step_kernel (DMMA fp64 GEMM H~ a_n + fused recursion and moment sums)"
+             if args.format == "dense" else
              f"kpm_stepk_tma_kernel ({plan['ks']} recursion steps per HBM pass, TMA-fed march; remainder steps "
              "by the two-/single-step kernels, included)" if plan.get("ks")
              else "kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
@@ -316,9 +347,16 @@ def main():
         if lat["onsite"] is not None:
             pinned_onsite = torch.from_numpy(lat["onsite"]).pin_memory().numpy()
 
+        if Hd is not None:
+            Hd_pinned = torch.from_numpy(Hd).pin_memory().numpy()
+            onsite_bytes, phase_bytes = Hd.nbytes, 0
+
         def e2e_step():
-            h2 = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=pinned_onsite,
-                                        flux=lat["flux"], device=local_rank, dist=part)
+            if Hd is not None:
+                h2 = kpm.kpm_create_dense(Hd_pinned, a, b, device=local_rank, dist=part)
+            else:
+                h2 = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=pinned_onsite,
+                                            flux=lat["flux"], device=local_rank, dist=part)
             if world > 1:
                 out = kpm.moments_distributed(h2, N, R, cfg["seed"],
                                               device=None if args.dist_backend == "nccl" else torch.device("cpu"))
@@ -341,13 +379,31 @@ def main():
         assert np.array_equal(e2e_out, mu_host), "e2e result differs from the device-resident run"
         e2e = {"value": D * N * R / (e2e_ms / 1000.0), "unit": UNIT, "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": int(onsite_bytes + phase_bytes + 64), "d2h_bytes_per_step": 8 * N,
-               "path": "kpm_create_stencil + kpm_moments (host mu) + kpm_destroy per step"}
+               "path": ("kpm_create_dense" if Hd is not None else "kpm_create_stencil") +
+                       " + kpm_moments (host mu) + kpm_destroy per step"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, threads, sample, _ = oracle_sample(cfg, lat, a, b)
+        v, threads, sample, _ = oracle_sample(cfg, lat, a, b, dense=Hd is not None)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample}
 
+    if Hd is None:
+        roofline = {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
+                    "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                    "traffic": profiled_traffic(args.config, plan),
+                    "alg_bytes_per_launch": step_bytes, "avg_launch_ms": avg_step_ms,
+                    "frac_of_8TBs_spec": achieved / 8000.0, "plan": plan}
+    else:
+        # a dense fp64 contraction: algorithmic flops 2 D^2 R per recursion step (unpadded) over the
+        # step launches' device time, against cuBLAS DGEMM measured here on the same shape
+        flops = 2.0 * lat["D"] ** 2 * R_loc * step_launches
+        achieved_tf = flops / (steps_ms / 1000.0) / 1e12
+        peak_tf = measure_dgemm_tflops(dev, lat["D"], R_loc)
+        roofline = {"bound": "tensor", "kernel": kname, "achieved": achieved_tf, "peak": peak_tf,
+                    "peak_kind": "measured (torch.matmul float64 = cuBLAS DGEMM, same M, N, K, in this run)",
+                    "unit": "TFLOP/s", "frac": achieved_tf / peak_tf, "traffic": None,
+                    "alg_flops_per_launch": 2.0 * lat["D"] ** 2 * R_loc, "avg_launch_ms": avg_step_ms,
+                    "frac_of_40TF_spec": achieved_tf / 40.0, "plan": plan}
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -355,11 +411,7 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Rademacher vectors, lattice H)",
                 "config": config_obj(args, cfg, lat, world),
                 "hbm_gbs_alg": steps_bytes / args.steps / (ms_per_step / 1000.0) / 1e9 * world,
-                "roofline": {"bound": "hbm", "kernel": kname, "achieved": achieved, "peak": peak,
-                             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-                             "traffic": profiled_traffic(args.config, plan),
-                             "alg_bytes_per_launch": step_bytes, "avg_launch_ms": avg_step_ms,
-                             "frac_of_8TBs_spec": achieved / 8000.0, "plan": plan},
+                "roofline": roofline,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
                                                         "max_abs_mu": float(np.abs(mu_host).max())}}

@@ -113,10 +113,11 @@ def lattice_csr(lat: dict) -> CSR:
     return CSR(D, rowptr, col, vre, vim, lat.get("flux", 0.0) != 0.0)
 
 
-def csr_from_dense(H: np.ndarray) -> CSR:
-    """CSR of an arbitrary dense Hermitian H (test-only helper)."""
+def csr_from_dense(H: np.ndarray, keep_zeros: bool = False) -> CSR:
+    """CSR of an arbitrary dense Hermitian H (test-only helper); keep_zeros stores all D^2
+    entries (the dense variant's arithmetic, for the CPU baseline of the dense config)."""
     D = H.shape[0]
-    rows, cols = np.nonzero(H)
+    rows, cols = np.nonzero(np.ones_like(H, dtype=bool) if keep_zeros else H)
     order = np.lexsort((cols, rows))
     rows, cols = rows[order], cols[order]
     rowptr = np.zeros(D + 1, dtype=np.int64)
