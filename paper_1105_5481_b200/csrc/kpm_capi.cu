@@ -102,6 +102,9 @@ struct kpm_handle_s {
     int num_sms = 148;
     // timing of the last call
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+    // row partition, overlapped halo exchange: a second stream and two events (created on demand)
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
     int step_launches = 0, total_launches = 0;
     double steps_bytes = 0.0;  // algorithmic HBM bytes of the recursion-step launches of the last call
 };
@@ -117,6 +120,9 @@ struct Plan {
     // TMA-pipelined step kernel (2D/3D stencils), see kpm_tma.cuh
     bool use_tma = false;
     int TL = 0, TX = 0, TY = 0, tma_grid = 0, tma_rr = 0;
+    // row partition: boundary planes first, halo exchange on a comm stream while the interior
+    // planes compute; partial rows [0, G) interior, [G, 2G) and [2G, 3G) boundary
+    bool overlap = false;
     size_t tma_smem = 0;
     // two steps per launch (temporal blocking, 2D), see kpm_tma2.cuh; needs 4 vector blocks
     bool use_tma2 = false, no_fused = false;
@@ -282,6 +288,9 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->use_tmak) p->gx = std::max(p->gx, p->tmak_grid);
     p->nslots = N;
     if (h->rows) p->use_tma2 = p->use_tmak = false;  // multi-step kernels need deep halos; not with slabs
+    p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL && !(flags & KPM_DIRECT) &&
+                 !env_on("KPM_NO_OVERLAP");
+    if (p->overlap) p->gx = 3 * p->tma_grid;
     if (p->use_tmak && p->M - 1 < p->KSK) p->use_tmak = false;
     p->xpad = (h->kind == KIND_STENCIL && h->ndim == 3) ? 2 : 0;
     const size_t rows_of_x = (size_t)(h->D / h->L[0]);
@@ -610,32 +619,33 @@ kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
 
 template <int NDIM, bool ONSITE, bool PEIERLS>
 kpm_status launch_tma_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
-                        const kpm::TmaGeom& g, int tail) {
+                        const kpm::TmaGeom& g, int tail, int grid) {
     auto kern = kpm::kpm_step_tma_kernel<NDIM, ONSITE, PEIERLS>;
     static size_t configured = 0;
     if (configured < p.tma_smem) {
         KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma_smem));
         configured = p.tma_smem;
     }
-    kern<<<p.tma_grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.A, cur.Col, cur.Row, prev.P, E, g, tail);
+    kern<<<grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.A, cur.Col, cur.Row, prev.P, E, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
     return KPM_OK;
 }
 
 kpm_status launch_tma(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
-                      const kpm::TmaGeom& g, int tail) {
+                      const kpm::TmaGeom& g, int tail, int grid = 0) {
     const bool on = h->d_eps != nullptr;
+    if (!grid) grid = p.tma_grid;
     if (h->ndim == 2) {
         if (is_cplx(h)) {
-            if (on) return launch_tma_t<2, true, true>(h, p, cur, prev, E, g, tail);
-            return launch_tma_t<2, false, true>(h, p, cur, prev, E, g, tail);
+            if (on) return launch_tma_t<2, true, true>(h, p, cur, prev, E, g, tail, grid);
+            return launch_tma_t<2, false, true>(h, p, cur, prev, E, g, tail, grid);
         }
-        if (on) return launch_tma_t<2, true, false>(h, p, cur, prev, E, g, tail);
-        return launch_tma_t<2, false, false>(h, p, cur, prev, E, g, tail);
+        if (on) return launch_tma_t<2, true, false>(h, p, cur, prev, E, g, tail, grid);
+        return launch_tma_t<2, false, false>(h, p, cur, prev, E, g, tail, grid);
     }
-    if (on) return launch_tma_t<3, true, false>(h, p, cur, prev, E, g, tail);
-    return launch_tma_t<3, false, false>(h, p, cur, prev, E, g, tail);
+    if (on) return launch_tma_t<3, true, false>(h, p, cur, prev, E, g, tail, grid);
+    return launch_tma_t<3, false, false>(h, p, cur, prev, E, g, tail, grid);
 }
 
 kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) {
@@ -884,6 +894,8 @@ struct Run {
             tg.ghost = h->rows ? 1 : 0;
             tg.RP = p.RP;
             tg.rows_total = p.gx;
+            tg.row_off = 0;
+            tg.zoff = 0;
             tg.xpad = p.xpad;
             tg.t = h->t_scaled;
             tg.shift = -h->b / h->a;
@@ -981,12 +993,62 @@ struct Run {
         return KPM_OK;
     }
 
+    // Row partition, one recursion step with the halo exchange overlapped:
+    // (1) the two boundary planes of a_{n+1} (slab planes 0 and nloc-1), (2) their send/recv
+    // into the neighbours' ghost planes on the comm stream, concurrently with (3) the interior
+    // planes 1..nloc-2; the next step's launches wait for (2) (event join).  The three launches
+    // write disjoint partial-sum row ranges, summed by finish_kernel in a fixed order.
+    bool comm_pending = false, exchanged_inline = false;
+    kpm_status launch_overlapped(int tail) {
+        if (!h->comm_stream) {
+            KPM_CUDA(cudaStreamCreateWithFlags(&h->comm_stream, cudaStreamNonBlocking));
+            KPM_CUDA(cudaEventCreateWithFlags(&h->ev_bnd, cudaEventDisableTiming));
+            KPM_CUDA(cudaEventCreateWithFlags(&h->ev_comm, cudaEventDisableTiming));
+        }
+        if (comm_pending) KPM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_comm, 0));  // ghosts of a_n arrived
+        const long long cols = tg.W / tg.Lm;
+        const int Lm_full = tg.Lm, G = p.tma_grid;
+        const BufMaps& mc = maps_of(base_of(cur));
+        const BufMaps& mp = maps_of(base_of(prev));
+        auto sub = [&](int z0, int nz, int row_off) -> kpm_status {
+            kpm::TmaGeom g2 = tg;
+            g2.zoff = z0;
+            g2.Lm = nz;
+            g2.W = cols * nz;
+            const int grid = (int)std::min<long long>(g2.W, (long long)h->num_sms);
+            g2.rr = (h->ndim == 3 && cols >= 4LL * grid) ? 1 : 0;
+            g2.row_off = row_off;
+            g2.rows_total = G;
+            return launch_tma(h, p, mc, mp, mapE, g2, tail, grid);
+        };
+        KPM_TRY(sub(0, 1, G));
+        KPM_TRY(sub(Lm_full - 1, 1, 2 * G));
+        KPM_CUDA(cudaEventRecord(h->ev_bnd, h->stream));
+        KPM_CUDA(cudaStreamWaitEvent(h->comm_stream, h->ev_bnd, 0));
+        KPM_TRY(exchange_on(prev, h->comm_stream));
+        KPM_CUDA(cudaEventRecord(h->ev_comm, h->comm_stream));
+        comm_pending = true;
+        exchanged_inline = true;
+        return sub(1, Lm_full - 2, 0);
+    }
+    // join the comm stream before the partial sums are read
+    kpm_status join_comm() {
+        if (comm_pending) KPM_CUDA(cudaStreamWaitEvent(h->stream, h->ev_comm, 0));
+        comm_pending = false;
+        return KPM_OK;
+    }
+
     // ghost planes of `X` must be refreshed before the next launch (recorded; done by the caller)
     double2* pending = nullptr;
     kpm_status need_exchange(double2* X) {
         pending = X;
+        if (exchanged_inline) {  // the overlapped step already sent them
+            exchanged_inline = false;
+            return KPM_OK;
+        }
         return exchange_hook ? exchange_hook(this) : KPM_OK;
     }
+    kpm_status exchange_on(double2* X, cudaStream_t st);
     kpm_status (*exchange_hook)(Run*) = nullptr;
 
     bool more() const { return n <= nsteps; }
@@ -1054,7 +1116,13 @@ struct Run {
             v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
             const bool tail = (N & 1) && n == nsteps;    // odd N: <a_M|a_M> -> mu_{N-1}
             v.red2 = tail ? part + (size_t)(2 * n + 2) * slot : nullptr;
-            if (p.use_tma) {
+            if (p.use_tma && p.overlap) {
+                tg.red0 = v.red0;
+                tg.red1 = v.red1;
+                tg.red2 = v.red2;
+                tg.out = base_of(prev);
+                KPM_TRY(launch_overlapped(tail));
+            } else if (p.use_tma) {
                 tg.red0 = v.red0;
                 tg.red1 = v.red1;
                 tg.red2 = v.red2;
@@ -1073,6 +1141,7 @@ struct Run {
 
     // Fixed-order finish of the CTA partials: Sv[m][v] and S[m] on the device.
     kpm_status collect() {
+        KPM_TRY(join_comm());
         KPM_CUDA(cudaEventRecord(h->ev_end, h->stream));
         kpm::finish_kernel<<<N, 256, 0, h->stream>>>(part, p.gx, p.RP, p.R_loc, Sv, S);
         KPM_CUDA(cudaGetLastError());
@@ -1137,28 +1206,30 @@ struct Run {
 
 // Halo exchange of a single row-partitioned handle: world 1 (periodic wrap inside the
 // slab) or NCCL send/recv with the two neighbouring ranks, on the handle's stream.
-kpm_status exchange_single(Run* r) {
-    kpm_handle_s* h = r->h;
-    double2* X = r->pending;
-    const size_t pb = r->plane_bytes();
+kpm_status Run::exchange_on(double2* X, cudaStream_t st) {
+    const size_t pb = plane_bytes();
     if (h->dist.comm == KPM_COMM_SELF) {
-        KPM_CUDA(cudaMemcpyAsync(r->ghost_lo(X), r->last_plane(X), pb, cudaMemcpyDeviceToDevice, h->stream));
-        KPM_CUDA(cudaMemcpyAsync(r->ghost_hi(X), r->first_plane(X), pb, cudaMemcpyDeviceToDevice, h->stream));
+        KPM_CUDA(cudaMemcpyAsync(ghost_lo(X), last_plane(X), pb, cudaMemcpyDeviceToDevice, st));
+        KPM_CUDA(cudaMemcpyAsync(ghost_hi(X), first_plane(X), pb, cudaMemcpyDeviceToDevice, st));
         return KPM_OK;
     }
     if (h->dist.comm != KPM_COMM_NCCL || !h->nccl) return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL handles need kpm_moments_group");
     const int W = h->dist.world, rk = h->dist.rank;
     const int lo = (rk - 1 + W) % W, hi = (rk + 1) % W;
     ncclResult_t e = ncclGroupStart();
-    if (e == ncclSuccess) e = ncclSend(r->first_plane(X), pb, ncclUint8, lo, h->nccl, h->stream);
-    if (e == ncclSuccess) e = ncclRecv(r->ghost_hi(X), pb, ncclUint8, hi, h->nccl, h->stream);
-    if (e == ncclSuccess) e = ncclSend(r->last_plane(X), pb, ncclUint8, hi, h->nccl, h->stream);
-    if (e == ncclSuccess) e = ncclRecv(r->ghost_lo(X), pb, ncclUint8, lo, h->nccl, h->stream);
+    if (e == ncclSuccess) e = ncclSend(first_plane(X), pb, ncclUint8, lo, h->nccl, st);
+    if (e == ncclSuccess) e = ncclRecv(ghost_hi(X), pb, ncclUint8, hi, h->nccl, st);
+    if (e == ncclSuccess) e = ncclSend(last_plane(X), pb, ncclUint8, hi, h->nccl, st);
+    if (e == ncclSuccess) e = ncclRecv(ghost_lo(X), pb, ncclUint8, lo, h->nccl, st);
     ncclResult_t e2 = ncclGroupEnd();
     if (e != ncclSuccess || e2 != ncclSuccess)
         return fail(KPM_ERR_UNSUPPORTED, "NCCL halo exchange: %s", ncclGetErrorString(e != ncclSuccess ? e : e2));
     return KPM_OK;
 }
+
+// Halo exchange of a single row-partitioned handle (world 1: a local wrap copy; NCCL:
+// send/recv with the two neighbouring ranks), on the handle's stream.
+kpm_status exchange_single(Run* r) { return r->exchange_on(r->pending, r->h->stream); }
 
 // Halo exchange between the in-process slab handles of a KPM_COMM_LOCAL group: every
 // rank pulls its two ghost planes from its neighbours' freshly written blocks once both
@@ -1205,6 +1276,9 @@ void kpm_destroy(kpm_handle h) {
     if (h->nccl) ncclCommDestroy(h->nccl);
     if (h->ev_begin) cudaEventDestroy(h->ev_begin);
     if (h->ev_end) cudaEventDestroy(h->ev_end);
+    if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
+    if (h->ev_comm) cudaEventDestroy(h->ev_comm);
+    if (h->comm_stream) cudaStreamDestroy(h->comm_stream);
     if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     delete h;
 }
@@ -1680,7 +1754,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[4] = p.gx;
     info[5] = (int64_t)p.tma_smem;
     info[6] = p.RG;
-    info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0);
+    info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0) | (p.overlap ? 4 : 0);
     info[8] = p.use_tma2 ? p.TX2 : 0;
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;

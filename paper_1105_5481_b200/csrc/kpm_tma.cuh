@@ -110,7 +110,9 @@ struct TmaGeom {
     int Lm;           // march extent (L1 in 2D, L2 in 3D)
     long long W;      // total output planes = G_L * PX * PY * Lm
     int rr;           // 1: round-robin whole columns over CTAs; 0: contiguous plane ranges
-    int rows_total;   // partial-sum rows per moment slot (>= gridDim.x; extra rows are zeroed)
+    int rows_total;   // partial-sum rows of this launch (>= gridDim.x; extra rows are zeroed)
+    int row_off;      // first partial-sum row of this launch (row partition: boundary/interior launches)
+    int zoff;         // ghost mode: first slab plane of this launch (planes [zoff, zoff + Lm))
     int xpad;         // 3D: x-rows of the vector blocks carry a frame of xpad periodic images per side
     int ghost;        // 1: row partition -- vector buffers hold Lm + 2 planes (ghost, local..., ghost),
                       //    march neighbours are never wrapped; 0: periodic wrap
@@ -254,7 +256,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 const int H = s.m1 - s.m0;
                 for (int q = 0; q < H + 2; ++q) {
                     // buffer plane of march coordinate m0-1+q
-                    const int m = g.ghost ? s.m0 + q : (s.m0 - 1 + q + g.Lm) % g.Lm;
+                    const int m = g.ghost ? g.zoff + s.m0 + q : (s.m0 - 1 + q + g.Lm) % g.Lm;
                     const int slot = (int)(ia % kSA);
                     if (ia >= kSA) mbar_wait(emptyA + slot, (uint32_t)(((ia / kSA) - 1) & 1));
                     unsigned char* dst = ringA + slot * SL.bytes;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     ++ia;
                     // a_{n-1} for output plane q-1, issued right behind the a_n plane it pairs with
                     if (q >= 1 && q - 1 < H) {
-                        const int mp = s.m0 + q - 1 + g.ghost;
+                        const int mp = g.zoff + s.m0 + q - 1 + g.ghost;
                         const int ps = (int)(ip % kSP);
                         if (ip >= kSP) mbar_wait(emptyP + ps, (uint32_t)(((ip / kSP) - 1) & 1));
                         mbar_expect_tx(fullP + ps, tile_bytes);
@@ -337,7 +339,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                 const unsigned char* S1 = ringA + (int)(i1 % kSA) * SL.bytes;  // plane m
                 const unsigned char* S2 = ringA + (int)(i2 % kSA) * SL.bytes;  // plane m+1
                 const double2* Pv = reinterpret_cast<const double2*>(ringP + ps * tile_bytes);
-                const int m = s.m0 + j + g.ghost;  // buffer plane of the output
+                const int m = g.zoff + s.m0 + j + g.ghost;  // buffer plane of the output
                 auto lane_at = [&](const unsigned char* base, int off, int site) {
                     return reinterpret_cast<const double2*>(base + off)[site * g.TL + l];
                 };
@@ -403,6 +405,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     for (int k = 0; k < 3; ++k) {
         double* rowk = k == 0 ? g.red0 : (k == 1 ? g.red1 : (tail ? g.red2 : nullptr));
         if (rowk == nullptr) continue;
+        rowk += (size_t)g.row_off * g.RP;
         for (int v = threadIdx.x; v < g.RP; v += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + v] = sacc[k * g.RP + v];
         for (int rr = blockIdx.x + gridDim.x; rr < g.rows_total; rr += gridDim.x)
             for (int v = threadIdx.x; v < g.RP; v += blockDim.x) rowk[(size_t)rr * g.RP + v] = 0.0;

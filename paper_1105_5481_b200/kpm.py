@@ -255,6 +255,7 @@ class Handle:
         d = {k: int(v) for k, v in zip(keys, info) if k != "_"}
         d["round_robin"] = int(info[7] & 1)
         d["two_step"] = int((info[7] >> 1) & 1)
+        d["overlap"] = int((info[7] >> 2) & 1)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
         return d
 

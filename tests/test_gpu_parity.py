@@ -288,7 +288,7 @@ ROW_CASES = {
 
 @pytest.mark.parametrize("comm", ["self", "nccl"])
 @pytest.mark.parametrize("case", sorted(ROW_CASES))
-def test_row_partition_world1_matches_oracle(kpm, case, comm):
+def test_row_partition_world1_matches_oracle(kpm, case, comm, monkeypatch):
     """KPM_PART_ROWS with one rank: slab + ghost planes refreshed after every step (a local
     copy, or NCCL send/recv to itself), moment sums through the NCCL all-reduce."""
     lat, N, R = ROW_CASES[case]
@@ -301,13 +301,19 @@ def test_row_partition_world1_matches_oracle(kpm, case, comm):
     else:
         dist = (kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_NCCL, kpm.kpm_nccl_unique_id())
     h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"], dist=dist)
-    assert h.plan_info(N, R)["two_step"] == 0
+    info = h.plan_info(N, R)
+    assert info["two_step"] == 0
+    assert info["overlap"] == (info["tma"] == 1 and lat["L"][lat["ndim"] - 1] >= 3)
     mu = h.moments(N, R, 8)
     assert normwise(mu, ref) < TOL
     assert normwise(h.moments_ex(N, R, 8, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
     assert np.array_equal(h.moments_ex(N, R, 8, r0=r), mu)  # a_0 ghosts exchanged before the first step
     whole = make(kpm, lat, a, b).moments(N, R, 8)
     assert normwise(mu, whole) < 1e-13
+    if info["overlap"]:  # boundary planes + exchange on the comm stream + interior, vs serialised
+        monkeypatch.setenv("KPM_NO_OVERLAP", "1")
+        assert h.plan_info(N, R)["overlap"] == 0
+        assert normwise(h.moments(N, R, 8), mu) < 1e-13
 
 
 @pytest.mark.parametrize("world", [2, 3, 4])
