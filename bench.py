@@ -31,6 +31,7 @@ import numpy as np  # noqa: E402
 import kpm_inputs as ki  # noqa: E402
 
 METRIC = "KPM vector-element updates/s (D*N*R/s)"
+_OUT = sys.stdout  # replaced in main() by the saved stdout descriptor
 UNIT = "updates/s"
 
 
@@ -171,7 +172,7 @@ def run_reference(args, cfg, lat, a, b, rank, world):
             "data": "synthetic", "config": config_obj(args, cfg, lat, world),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    print(json.dumps(line), file=_OUT, flush=True)
 
 
 def config_obj(args, cfg, lat, world):
@@ -189,6 +190,12 @@ def config_obj(args, cfg, lat, world):
 
 
 def main():
+    # stdout carries exactly one JSON line: libraries that print to fd 1 (NCCL's version banner)
+    # are sent to stderr; the result line is written to the saved descriptor.
+    global _OUT
+    sys.stdout.flush()
+    _OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
@@ -415,7 +422,7 @@ def main():
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
                                                         "max_abs_mu": float(np.abs(mu_host).max())}}
-        print(json.dumps(line), flush=True)
+        print(json.dumps(line), file=_OUT, flush=True)
     if dist.is_initialized():
         dist.destroy_process_group()
 
