@@ -24,6 +24,7 @@
 #include "kpm_tma.cuh"
 #include "kpm_tma2.cuh"
 #include "kpm_tmak.cuh"
+#include "kpm_tma3.cuh"
 #include "kpm_ell.cuh"
 #include "kpm_small.cuh"
 #include "kpm_dense.cuh"
@@ -123,6 +124,8 @@ struct Plan {
     // row partition: boundary planes first, halo exchange on a comm stream while the interior
     // planes compute; partial rows [0, G) interior, [G, 2G) and [2G, 3G) boundary
     bool overlap = false;
+    // 3D: dense halo box + z rolled in registers (kpm_tma3.cuh) for the instantiated tiles
+    bool use_tma3 = false;
     size_t tma_smem = 0;
     // two steps per launch (temporal blocking, 2D), see kpm_tma2.cuh; needs 4 vector blocks
     bool use_tma2 = false, no_fused = false;
@@ -202,6 +205,16 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     p->TX = TX;
     p->TY = TY;
     p->tma_grid = (int)std::min<long long>(W, h->num_sms);
+    p->use_tma3 = false;
+    if (h->ndim == 3 && !env_on("KPM_NO_TMA3")) {
+        const bool on = h->d_eps != nullptr;
+        size_t sm3 = 0;
+        if (TX == 16 && TY == 8 && TL == 8) sm3 = on ? kpm::step3_smem_bytes<16, 8, 8, true>(p->RP) : kpm::step3_smem_bytes<16, 8, 8, false>(p->RP);
+        if (sm3 && sm3 <= 227 * 1024) {
+            p->use_tma3 = true;
+            p->tma_smem = sm3;
+        }
+    }
     // 3D: whole columns round-robin when there are enough of them (in-plane halos then hit L2)
     const long long cols = W / Lm;
     p->tma_rr = (h->ndim == 3 && cols >= 4LL * p->tma_grid && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
@@ -510,6 +523,7 @@ struct BufMaps {
     CUtensorMap A, Col, Row, P, Col2;  // main, 1-site column, row, (=main), 2-site column (2D)
     CUtensorMap A2;                    // main box of the two-step kernel (width TX2)
     CUtensorMap AK, AKH, AKH1;         // KS-step kernel: main (TXK), KS-site and (KS-1)-site boxes, TLK lanes
+    CUtensorMap Box3, Row3;            // 3D dense-box kernel: (TX+2) x TY box, (TX+2)-site row
 };
 
 kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMaps* bm) {
@@ -519,6 +533,10 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     KPM_TRY(make_vec_map(h, p, base, p.TX, 1, 1, &bm->Row));
     if (h->ndim == 2) KPM_TRY(make_vec_map(h, p, base, 2, 1, 1, &bm->Col2));
     if (p.use_tma2) KPM_TRY(make_vec_map(h, p, base, p.TX2, 1, 1, &bm->A2));
+    if (p.use_tma3) {
+        KPM_TRY(make_vec_map(h, p, base, p.TX + 2, p.TY, 1, &bm->Box3));
+        KPM_TRY(make_vec_map(h, p, base, p.TX + 2, 1, 1, &bm->Row3));
+    }
     if (p.use_tmak) {
         KPM_TRY(make_vec_map(h, p, base, p.TXK, 1, 1, &bm->AK, p.TLK));
         KPM_TRY(make_vec_map(h, p, base, p.KSK, 1, 1, &bm->AKH, p.TLK));
@@ -617,6 +635,21 @@ kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d", p.KSK, p.TLK);
 }
 
+template <int TX, int TY, int TL, bool ONSITE>
+kpm_status launch_tma3_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
+                         const kpm::TmaGeom& g, int tail, int grid) {
+    auto kern = kpm::kpm_step3_tma_kernel<TX, TY, TL, ONSITE>;
+    static size_t configured = 0;
+    if (configured < p.tma_smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma_smem));
+        configured = p.tma_smem;
+    }
+    kern<<<grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.Box3, cur.Row3, prev.P, E, g, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
 template <int NDIM, bool ONSITE, bool PEIERLS>
 kpm_status launch_tma_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
                         const kpm::TmaGeom& g, int tail, int grid) {
@@ -643,6 +676,11 @@ kpm_status launch_tma(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const 
         }
         if (on) return launch_tma_t<2, true, false>(h, p, cur, prev, E, g, tail, grid);
         return launch_tma_t<2, false, false>(h, p, cur, prev, E, g, tail, grid);
+    }
+    if (p.use_tma3) {
+        // the only instantiated tile (lanes per site a multiple of 8 always pick TL = 8)
+        return on ? launch_tma3_t<16, 8, 8, true>(h, p, cur, prev, E, g, tail, grid)
+                  : launch_tma3_t<16, 8, 8, false>(h, p, cur, prev, E, g, tail, grid);
     }
     if (on) return launch_tma_t<3, true, false>(h, p, cur, prev, E, g, tail, grid);
     return launch_tma_t<3, false, false>(h, p, cur, prev, E, g, tail, grid);
@@ -1754,7 +1792,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[4] = p.gx;
     info[5] = (int64_t)p.tma_smem;
     info[6] = p.RG;
-    info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0) | (p.overlap ? 4 : 0);
+    info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0) | (p.overlap ? 4 : 0) | (p.use_tma3 ? 8 : 0);
     info[8] = p.use_tma2 ? p.TX2 : 0;
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;

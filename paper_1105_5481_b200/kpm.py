@@ -256,6 +256,7 @@ class Handle:
         d["round_robin"] = int(info[7] & 1)
         d["two_step"] = int((info[7] >> 1) & 1)
         d["overlap"] = int((info[7] >> 2) & 1)
+        d["box3"] = int((info[7] >> 3) & 1)  # 3D dense-box march kernel (kpm_tma3.cuh)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
         return d
 

@@ -115,6 +115,11 @@ def test_tma_march_matches_oracle(kpm, case, monkeypatch):
     assert normwise(pv, ref_pv) < TOL
     assert np.array_equal(h.moments(N, R, 21), mu), "not deterministic"
     assert np.array_equal(h.moments_ex(N, R, 21, r0=r), mu)
+    if lat["ndim"] == 3:  # dense-box kernel (kpm_tma3.cuh) vs the generic-tile march kernel
+        assert info["box3"] == (info["TX"] == 16 and info["TY"] == 8 and info["TL"] == 8), info
+        monkeypatch.setenv("KPM_NO_TMA3", "1")
+        assert h.plan_info(N, R)["box3"] == 0
+        assert normwise(h.moments(N, R, 21), ref) < TOL
 
 
 @pytest.mark.parametrize("case", [c for c in sorted(TMA_CASES) if c.startswith("2d")])
