@@ -178,6 +178,8 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     const int cands2[3] = {32, 16, 8}, cands3[3] = {8, 16, 32};
     for (int c : (h->ndim == 2 ? cands2 : cands3))
         if (RG % c == 0) { TL = c; break; }
+    const int tl_env = env_int("KPM_TMA_TL", 0);  // experiment: lanes per tile site
+    if (tl_env && RG % tl_env == 0) TL = tl_env;
     if (!TL) return;
     int TX, TY;
     if (h->ndim == 2) {
@@ -210,6 +212,8 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
         const bool on = h->d_eps != nullptr;
         size_t sm3 = 0;
         if (TX == 16 && TY == 8 && TL == 8) sm3 = on ? kpm::step3_smem_bytes<16, 8, 8, true>(p->RP) : kpm::step3_smem_bytes<16, 8, 8, false>(p->RP);
+        if (TX == 8 && TY == 8 && TL == 16) sm3 = on ? kpm::step3_smem_bytes<8, 8, 16, true>(p->RP) : kpm::step3_smem_bytes<8, 8, 16, false>(p->RP);
+        if (TX == 4 && TY == 8 && TL == 32) sm3 = on ? kpm::step3_smem_bytes<4, 8, 32, true>(p->RP) : kpm::step3_smem_bytes<4, 8, 32, false>(p->RP);
         if (sm3 && sm3 <= 227 * 1024) {
             p->use_tma3 = true;
             p->tma_smem = sm3;
@@ -678,7 +682,10 @@ kpm_status launch_tma(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const 
         return launch_tma_t<2, false, false>(h, p, cur, prev, E, g, tail, grid);
     }
     if (p.use_tma3) {
-        // the only instantiated tile (lanes per site a multiple of 8 always pick TL = 8)
+        if (p.TL == 16) return on ? launch_tma3_t<8, 8, 16, true>(h, p, cur, prev, E, g, tail, grid)
+                                  : launch_tma3_t<8, 8, 16, false>(h, p, cur, prev, E, g, tail, grid);
+        if (p.TL == 32) return on ? launch_tma3_t<4, 8, 32, true>(h, p, cur, prev, E, g, tail, grid)
+                                  : launch_tma3_t<4, 8, 32, false>(h, p, cur, prev, E, g, tail, grid);
         return on ? launch_tma3_t<16, 8, 8, true>(h, p, cur, prev, E, g, tail, grid)
                   : launch_tma3_t<16, 8, 8, false>(h, p, cur, prev, E, g, tail, grid);
     }
