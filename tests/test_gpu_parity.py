@@ -116,10 +116,27 @@ def test_tma_march_matches_oracle(kpm, case, monkeypatch):
     assert np.array_equal(h.moments(N, R, 21), mu), "not deterministic"
     assert np.array_equal(h.moments_ex(N, R, 21, r0=r), mu)
     if lat["ndim"] == 3:  # dense-box kernel (kpm_tma3.cuh) vs the generic-tile march kernel
-        assert info["box3"] == (info["TX"] == 16 and info["TY"] == 8 and info["TL"] == 8), info
+        assert info["box3"] == ((info["TX"], info["TY"], info["TL"]) in [(16, 8, 8), (8, 8, 16), (4, 8, 32)]), info
         monkeypatch.setenv("KPM_NO_TMA3", "1")
         assert h.plan_info(N, R)["box3"] == 0
         assert normwise(h.moments(N, R, 21), ref) < TOL
+
+
+@pytest.mark.parametrize("tl", [8, 16, 32])
+def test_3d_box_kernel_every_tile_width(kpm, tl, monkeypatch):
+    """The 3D dense-box kernel for each instantiated tile (TL = 8, 16, 32 lanes per site; the
+    plan's TL forced by KPM_TMA_TL), on-site disorder, round-robin columns, vs the oracle."""
+    monkeypatch.setenv("KPM_NO_SMALL", "1")
+    monkeypatch.setenv("KPM_TMA_TL", str(tl))
+    lat = lat_of(3, (32, 24, 10), W=2.0)
+    N, R = 23, 64
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(6, R, lat["D"]), N)
+    h = make(kpm, lat, a, b)
+    info = h.plan_info(N, R)
+    assert info["TL"] == tl and info["box3"] == 1, info
+    assert normwise(h.moments(N, R, 6), ref) < TOL
 
 
 @pytest.mark.parametrize("case", [c for c in sorted(TMA_CASES) if c.startswith("2d")])
