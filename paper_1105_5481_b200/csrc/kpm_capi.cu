@@ -597,6 +597,7 @@ kpm_status launch_tma2_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const
 // instantiated tile shapes of the two-step kernel (TX * TL = 1024 lanes per row tile)
 kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                        const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
+    if (p.TL == 64 && p.TX2 == 16) return launch_tma2_s<64, 16, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 32 && p.TX2 == 32) return launch_tma2_s<32, 32, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 16 && p.TX2 == 64) return launch_tma2_s<16, 64, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 8 && p.TX2 == 128) return launch_tma2_s<8, 128, 1>(h, p, A, P, E, E2, g, tail);
