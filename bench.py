@@ -106,7 +106,7 @@ def profiled_traffic(config, plan):
     except Exception:
         return None
     want = ("stepk" if plan.get("ks") else "step2" if plan.get("two_step")
-            else ("step_tma" if plan["tma"] else "kpm_step_kernel"))
+            else "step3_tma" if plan.get("box3") else ("step_tma" if plan.get("tma") else "kpm_step_kernel"))
     if want not in rec.get("kernel", ""):
         return None  # the committed capture is of another kernel: no traffic claim
     return rec["dram_bytes_per_launch"]
@@ -337,7 +337,9 @@ def main():
              f"kpm_stepk_tma_kernel ({plan['ks']} recursion steps per HBM pass, TMA-fed march; remainder steps "
              "by the two-/single-step kernels, included)" if plan.get("ks")
              else "kpm_step2_tma_kernel (two recursion steps per HBM pass, TMA-fed march)" if plan.get("two_step")
-             else "kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan["tma"]
+             else "kpm_step3_tma_kernel (3D TMA march, dense halo box per plane, z rolled in registers; fused "
+                  "stencil SpMM + recursion + reductions)" if plan.get("box3")
+             else "kpm_step_tma_kernel (TMA-fed march: fused stencil SpMM + recursion + reductions)" if plan.get("tma")
              else "kpm_step_kernel (fused stencil SpMM + recursion + reductions)")
     avg_step_ms = steps_ms / max(step_launches, 1)
     step_bytes = steps_bytes / max(step_launches, 1)

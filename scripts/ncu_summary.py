@@ -35,7 +35,7 @@ def main(src, rnd):
     os.makedirs(prof, exist_ok=True)
     tpath = os.path.join(prof, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    for c in ["c1", "c2", "c3", "c4", "c5"]:
+    for c in ["c1", "c2", "c3", "c4", "c5", "pd"]:
         ll = os.path.join(src, f"launchlist_{c}.csv")
         if os.path.exists(ll):
             rows = read_ncu_csv(ll)
@@ -91,6 +91,14 @@ def main(src, rnd):
                     for k, u, v in zip(rr[0], rr[1], rr[2]):
                         if k in keys:
                             f.write(f"{k} = {v} {u}\n")
+                    st = [(k.replace("smsp__pcsamp_warps_issue_stalled_", ""), v) for k, v in zip(rr[0], rr[2])
+                          if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")]
+                    st = sorted(((k, num(v)) for k, v in st if v.replace(",", "").replace(".", "").isdigit()),
+                                key=lambda kv: -kv[1])
+                    tot = sum(v for _, v in st) or 1.0
+                    f.write("# warp stall samples (share)\n")
+                    for k, v in st[:10]:
+                        f.write(f"stall {k:28s} {v / tot:6.3f}\n")
     json.dump(traffic, open(tpath, "w"), indent=1)
 
 

@@ -5,16 +5,18 @@
 set -u
 cd "${GRAFT_REPO_ROOT:-/root/repo}"
 OUT=gpurun_out/$1; shift
-CONFIGS=${*:-c2 c3 c4 c5}
+CONFIGS=${*:-c2 c3 c4 c5 pd}
 mkdir -p $OUT
 python -c "import __graft_entry__ as g; g.build()"
 B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
+# the recursion-step kernels (2D two-step, 3D dense-box / generic march, dense DMMA GEMM)
+K="kpm_step2_tma|kpm_step3_tma|kpm_step_tma|kpm_dense_step"
 for c in $CONFIGS; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv \
     --log-file $OUT/launchlist_$c.csv $B --config $c > /dev/null 2>&1
   timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
-    -k regex:"kpm_step2?_tma|kpm_step_kernel" -s 4 -c 8 --csv --log-file $OUT/dram_$c.csv $B --config $c > /dev/null 2>&1
-  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"kpm_step2?_tma" -s 5 -c 1 \
+    -k regex:"$K" -s 4 -c 8 --csv --log-file $OUT/dram_$c.csv $B --config $c > /dev/null 2>&1
+  timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 5 -c 1 \
     -o $OUT/full_$c $B --config $c > $OUT/full_$c.log 2>&1
 done
 ls -la $OUT
