@@ -30,8 +30,8 @@ def num(v):
     return float(v.replace(",", ""))
 
 
-def main(src, rnd):
-    prof = os.path.join(ROOT, "profiles")
+def main(src, rnd, dest=None):
+    prof = dest or os.path.join(ROOT, "profiles")
     os.makedirs(prof, exist_ok=True)
     tpath = os.path.join(prof, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
@@ -103,4 +103,4 @@ def main(src, rnd):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(sys.argv[1], sys.argv[2], sys.argv[3] if len(sys.argv) > 3 else None)

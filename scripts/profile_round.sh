@@ -19,4 +19,9 @@ for c in $CONFIGS; do
   timeout 600 ncu --set full --clock-control none --import-source on -k regex:"$K" -s 5 -c 1 \
     -o $OUT/full_$c $B --config $c > $OUT/full_$c.log 2>&1
 done
-ls -la $OUT
+# summaries on the box (the .ncu-rep files are too large to bring back, except one)
+mkdir -p $OUT/profiles
+cp profiles/traffic.json $OUT/profiles/ 2>/dev/null
+python scripts/ncu_summary.py $OUT ${ROUND:-r01} $OUT/profiles
+for c in $CONFIGS; do [ "$c" = "${KEEP_REP:-c3}" ] || rm -f $OUT/full_$c.ncu-rep; done
+ls -la $OUT $OUT/profiles
