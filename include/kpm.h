@@ -116,7 +116,11 @@ typedef struct {
                           KPM_PART_ROWS (stencils): rank owns the slab of the slowest lattice
                           dimension [Lm*rank/world, Lm*(rank+1)/world) (z in 3D, y in 2D, x in
                           1D) plus one ghost plane on each side, exchanged after every step
-                          (periodic: rank 0 and rank world-1 are neighbours). */
+                          (periodic: rank 0 and rank world-1 are neighbours).
+                          KPM_PART_ROWS (CSR / ELL): every rank passes the
+                          WHOLE matrix; rank owns rows [D*rank/world, D*(rank+1)/world) plus ghost
+                          copies of the off-block columns its rows reference, refreshed after
+                          every step (kpm_csr_partition gives the lists). */
     int32_t rank;
     int32_t world;
     int32_t comm;            /* KPM_COMM_* (row partition only) */
@@ -129,6 +133,18 @@ kpm_status kpm_nccl_unique_id(void* out128);
 
 /* Slab of the row partition: planes [begin, begin + count) of an extent Lm.  Host only. */
 kpm_status kpm_slab_range(int64_t Lm, int32_t rank, int32_t world, int64_t* begin, int64_t* count);
+
+/* Row partition of a general sparse H (host only, no device): for rank `rank` of `world`,
+ * counts[0] = local rows n (rows [D*rank/world, D*rank/world + n)), counts[1] = ghost sites
+ * n_ghost (the distinct columns outside the block referenced by the block's rows), counts[2] =
+ * rows to send n_send.  Optional outputs (NULL = skip; call once with NULL to size them):
+ * ghosts int64[n_ghost] = global index of ghost k, ascending (so grouped by owner rank);
+ * send_rows int64[n_send] = local row indices the other ranks need, peer by peer in rank
+ * order, ascending within a peer; peers int64[4*world] = per peer q: (offset into ghosts,
+ * count, offset into send_rows, count).  This is the plan kpm_create_csr/ell use for
+ * KPM_PART_ROWS; errors: KPM_ERR_INVALID_ARG for malformed CSR or a rank that owns no rows. */
+kpm_status kpm_csr_partition(int64_t D, const int64_t* rowptr, const int32_t* col, int32_t rank, int32_t world,
+                             int64_t counts[3], int64_t* ghosts, int64_t* send_rows, int64_t* peers);
 
 /* ---- creation (host -> device upload of H~; "the CPU copies the data to
  *      the VRAM") ------------------------------------------------------------------- */
@@ -145,7 +161,12 @@ kpm_status kpm_create_csr(int64_t D, const int64_t* rowptr, const int32_t* col, 
                           int32_t dtype, double a, double b, int32_t device, const kpm_dist* dist,
                           kpm_handle* out);
 
-/* H given in ELL: K entries per row, col int32[K][D] (-1 = padding), val [K][D] of dtype. */
+/* H given in ELL: K entries per row, col int32[K][D] (-1 = padding), val [K][D] of dtype.
+ * With dist->partition == KPM_PART_ROWS (both CSR and ELL), see kpm_dist and kpm_csr_partition:
+ * KPM_COMM_SELF (world 1), KPM_COMM_NCCL (one process per GPU: the rows each peer needs are
+ * packed and sent with ncclSend/ncclRecv straight into the peer's ghost range, then one
+ * all-reduce of the moment sums) or KPM_COMM_LOCAL (in-process handles on ONE device, through
+ * kpm_moments_group). */
 kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* val, int32_t dtype,
                           double a, double b, int32_t device, const kpm_dist* dist,
                           kpm_handle* out);
@@ -192,8 +213,9 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
                           uint32_t flags, void* out);
 
 /* Row partition with KPM_COMM_LOCAL: run kpm_moments for the `n` slab handles hs[0..n-1]
- * (rank i = hs[i], world n, any devices) in lock step, exchanging halo planes between
- * them after every step; mu[N] (host) is the moment estimate of the whole lattice. */
+ * (rank i = hs[i], world n, any devices; CSR/ELL handles: one device) in lock step,
+ * exchanging halo planes (ghost sites) between them after every step; mu[N] (host) is the
+ * moment estimate of the whole matrix. */
 kpm_status kpm_moments_group(kpm_handle* hs, int32_t n, int32_t N, int64_t R, uint64_t seed, double* mu);
 
 /* Raw sums S[N] (summed over all ranks) -> mu[N]: mu_0 = S_0/(D R), mu_1 = S_1/(D R),

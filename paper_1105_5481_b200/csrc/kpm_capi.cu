@@ -25,6 +25,7 @@
 #include "kpm_tma2.cuh"
 #include "kpm_tmak.cuh"
 #include "kpm_tma3.cuh"
+#include "kpm_tma32.cuh"
 #include "kpm_ell.cuh"
 #include "kpm_small.cuh"
 #include "kpm_dense.cuh"
@@ -78,6 +79,7 @@ struct kpm_handle_s {
     int64_t L[3] = {1, 1, 1};
     double t_scaled = 0.0;
     double* d_eps = nullptr;      // (eps_i - b)/a
+    double* d_epsf = nullptr;     // 3D: the same in the x-row frame layout [L2][L1][L0+4] (kpm_tma32.cuh)
     double2* d_phase = nullptr;   // e^{i 2 pi phi x}
     // ELL
     int K = 0;
@@ -94,6 +96,14 @@ struct kpm_handle_s {
     int slow = 0;
     int64_t z0 = 0, nloc = 0, Lm_global = 0, plane = 1;
     int64_t D_total = 0;  // global number of sites (normalisation, RNG counters)
+    // row partition of a general sparse H (KIND_ELL): local rows [z0, z0 + D),
+    // then n_ghost ghost sites (the off-block columns the local rows reference, ascending global index,
+    // hence grouped by owner rank).  ELL columns index that extended block.
+    int64_t n_ghost = 0, n_send = 0;
+    long long* d_gmap = nullptr;     // [n_ghost] global index of each ghost site (RNG counters of a_0)
+    int32_t* d_ghost_src = nullptr;  // [n_ghost] row of the ghost inside its owner's block (in-process groups)
+    int32_t* d_send = nullptr;       // [n_send] local rows the other ranks need, peer by peer, ascending
+    std::vector<int64_t> roff, rcnt, soff, scnt;  // per peer: ghost / send list offsets and counts
     ncclComm_t nccl = nullptr;
     // workspace
     char* ws = nullptr;
@@ -131,6 +141,10 @@ struct Plan {
     bool use_tma2 = false, no_fused = false;
     size_t tma2_smem = 0;
     int TX2 = 0, tma2_minb = 1, tma2_grid = 0;  // two-step tile width, CTAs per SM, grid
+    // two steps per launch for 3D lattices (kpm_tma32.cuh); needs 4 vector blocks
+    bool use_tma32 = false;
+    int TX32 = 0, TY32 = 0, TL32 = 0, tma32_grid = 0, tma32_rr = 0;
+    size_t tma32_smem = 0;
     // KS steps per launch (deep temporal blocking, 2D), see kpm_tmak.cuh; needs 4 vector blocks
     bool use_tmak = false;
     int KSK = 0, TLK = 0, TXK = 0, tmak_grid = 0;
@@ -143,7 +157,7 @@ struct Plan {
     int xpad = 0;            // 3D stencils: x-row frame of periodic images (row pitch L0 + 2 xpad)
     size_t mem_sites = 0;    // memory sites of the local block (with frames, without ghost planes)
     size_t off_P = 0, off_C = 0, off_R = 0, off_X2 = 0, off_X3 = 0, off_part = 0, off_Sv = 0, off_S = 0, off_out = 0,
-           off_sites = 0, total = 0;
+           off_sites = 0, off_send = 0, total = 0;
 };
 
 bool is_cplx(const kpm_handle_s* h) { return h->dtype == KPM_COMPLEX128; }
@@ -166,6 +180,51 @@ size_t stepk_smem(int ks, int tl, bool onsite, int RP) {
     if (ks == 3 && tl == 16) return onsite ? stepk_smem_bytes<3, 16, 32, true>(RP) : stepk_smem_bytes<3, 16, 32, false>(RP);
     if (ks == 3 && tl == 8) return onsite ? stepk_smem_bytes<3, 8, 64, true>(RP) : stepk_smem_bytes<3, 8, 64, false>(RP);
     return 0;
+}
+
+// Shared memory of the instantiated 3D two-step kernels (0 = not instantiated); KA, KP ring depths.
+constexpr int kKA32 = 5, kKP32 = 4;
+int nt32() { return env_int("KPM_TMA32_NT", 256) == 512 ? 512 : 256; }  // experiment: threads per CTA
+size_t step32_smem(int tx, int ty, int tl, bool onsite, int RP) {
+    using namespace kpm;
+    constexpr int NT = 512, KA = kKA32, KP = kKP32;  // (NT only sizes the reduction scratch)
+    if (tx == 8 && ty == 8 && tl == 8)
+        return onsite ? step32_smem_bytes<8, 8, 8, true, NT, KA, KP>(RP) : step32_smem_bytes<8, 8, 8, false, NT, KA, KP>(RP);
+    if (tx == 16 && ty == 4 && tl == 8)
+        return onsite ? step32_smem_bytes<16, 4, 8, true, NT, KA, KP>(RP) : step32_smem_bytes<16, 4, 8, false, NT, KA, KP>(RP);
+    if (tx == 8 && ty == 4 && tl == 16)
+        return onsite ? step32_smem_bytes<8, 4, 16, true, NT, KA, KP>(RP) : step32_smem_bytes<8, 4, 16, false, NT, KA, KP>(RP);
+    if (tx == 16 && ty == 8 && tl == 8)  // larger plane tile, shallower rings
+        return onsite ? step32_smem_bytes<16, 8, 8, true, NT, 3, 2>(RP) : step32_smem_bytes<16, 8, 8, false, NT, 3, 2>(RP);
+    return 0;
+}
+
+// 3D two-step kernel (kpm_tma32.cuh): real 3D stencils on whole lattices (not slabs), tiles
+// dividing the lattice, 4 vector blocks (the caller falls back to single steps otherwise).
+void plan_tma32(const kpm_handle_s* h, Plan* p) {
+    p->use_tma32 = false;
+    // Opt-in (KPM_TMA32=1): correct (GPU parity tests) but measured slower than the single-step
+    // dense-box kernel on c3 (2.64 ms per launch = 1.32 ms per step vs 1.02 ms).
+    if (!env_on("KPM_TMA32")) return;
+    if (h->ndim != 3 || p->no_fused || h->rows || is_cplx(h) || env_on("KPM_NO_TMA32")) return;
+    const int RG = p->RG;
+    int TX = 8, TY = 8, TL = 8;
+    const int shape = env_int("KPM_TMA32_SHAPE", 0);  // experiment: 1 = 16x4x8, 2 = 8x4x16
+    if (shape == 1) { TX = 16; TY = 4; TL = 8; }
+    if (shape == 2) { TX = 8; TY = 4; TL = 16; }
+    if (shape == 3) { TX = 16; TY = 8; TL = 8; }
+    if (RG % TL || h->L[0] % TX || h->L[1] % TY || h->L[0] < 2 || h->L[1] < 2) return;
+    const size_t sm = step32_smem(TX, TY, TL, h->d_eps != nullptr, p->RP);
+    if (!sm || sm > 227 * 1024) return;
+    const long long cols = (long long)(RG / TL) * (h->L[0] / TX) * (h->L[1] / TY);
+    p->TX32 = TX;
+    p->TY32 = TY;
+    p->TL32 = TL;
+    p->tma32_smem = sm;
+    // whole columns round-robin when there are enough of them (in-plane halos then hit L2)
+    p->tma32_rr = (cols >= 4LL * h->num_sms && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
+    p->tma32_grid = (int)std::min<long long>(p->tma32_rr ? cols : cols * h->L[2], (long long)h->num_sms);
+    p->use_tma32 = true;
 }
 
 // Tile choice for the TMA march: ~16 KB main tiles (TX*TY*TL = 1024 lanes), full passes
@@ -265,6 +324,7 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
             p->use_tmak = true;
         }
     }
+    plan_tma32(h, p);
 }
 
 kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p,
@@ -299,14 +359,15 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->use_small = !h->rows && !(flags & KPM_DIRECT) && p->small_smem <= kpm::kSmallSmemMax && !env_on("KPM_NO_SMALL") &&
                    h->kind != KIND_DENSE;
     if (p->use_small) {
-        p->use_tma = p->use_tma2 = false;
+        p->use_tma = p->use_tma2 = p->use_tma32 = false;
         p->TS = kpm::kSmallThreads / p->TR;
         p->gx = p->TS;  // partial-sum rows per slot = thread rows of the single CTA
     }
     if (p->use_tma2) p->gx = std::max(p->gx, p->tma2_grid);  // partial rows per slot (max over kernels)
     if (p->use_tmak) p->gx = std::max(p->gx, p->tmak_grid);
+    if (p->use_tma32) p->gx = std::max(p->gx, p->tma32_grid);
     p->nslots = N;
-    if (h->rows) p->use_tma2 = p->use_tmak = false;  // multi-step kernels need deep halos; not with slabs
+    if (h->rows) p->use_tma2 = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
     p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL && !(flags & KPM_DIRECT) &&
                  !env_on("KPM_NO_OVERLAP");
     if (p->overlap) p->gx = 3 * p->tma_grid;
@@ -315,7 +376,8 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     const size_t rows_of_x = (size_t)(h->D / h->L[0]);
     p->mem_sites = (size_t)h->D + 2 * (size_t)p->xpad * rows_of_x;
     if (h->kind == KIND_DENSE) p->mem_sites = (size_t)h->Dp;
-    const size_t plane_mem = !h->rows ? 0
+    if (h->kind == KIND_ELL) p->mem_sites = (size_t)(h->D + h->n_ghost);  // ghost sites after the local rows
+    const size_t plane_mem = (!h->rows || h->kind == KIND_ELL) ? 0
                              : p->xpad ? (size_t)(h->plane / h->L[0]) * (h->L[0] + 2 * p->xpad) : (size_t)h->plane;
     p->ghost_lanes = plane_mem * p->RG;
     p->lane_bytes = (p->mem_sites * p->RG + 2 * p->ghost_lanes) * sizeof(double2);
@@ -325,7 +387,8 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_R = off;
     if ((flags & KPM_DIRECT) && with_r0) off = align_up(off + p->lane_bytes);
     if (p->use_tma2 && p->M - 1 < 2) p->use_tma2 = false;
-    if (p->use_tma2 || p->use_tmak) {  // out-of-place multi-step launches: two spare blocks
+    if (p->use_tma32 && p->M - 1 < 2) p->use_tma32 = false;
+    if (p->use_tma2 || p->use_tmak || p->use_tma32) {  // out-of-place multi-step launches: two spare blocks
         p->off_X2 = off; off = align_up(off + p->lane_bytes);
         p->off_X3 = off; off = align_up(off + p->lane_bytes);
     }
@@ -334,6 +397,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_S = off; off = align_up(off + (size_t)N * sizeof(double));
     p->off_out = off; off = align_up(off + (size_t)N * p->R_loc * sizeof(double));
     p->off_sites = off; off = align_up(off + ((flags & KPM_LOCAL) ? (size_t)R * sizeof(long long) : 0));
+    p->off_send = off; off = align_up(off + (size_t)h->n_send * p->RG * sizeof(double2));
     p->total = off;
     if (h->D * (long long)p->RG > (1LL << 40)) return fail(KPM_ERR_INVALID_ARG, "problem too large");
     return KPM_OK;
@@ -530,6 +594,7 @@ struct BufMaps {
     CUtensorMap A2;                    // main box of the two-step kernel (width TX2)
     CUtensorMap AK, AKH, AKH1;         // KS-step kernel: main (TXK), KS-site and (KS-1)-site boxes, TLK lanes
     CUtensorMap Box3, Row3;            // 3D dense-box kernel: (TX+2) x TY box, (TX+2)-site row
+    CUtensorMap A32, A32r, P32, P32r;  // 3D two-step kernel: (TX+4) x TY, (TX+4) x 2, (TX+2) x TY, (TX+2) x 1
 };
 
 kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMaps* bm) {
@@ -542,6 +607,12 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     if (p.use_tma3) {
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, p.TY, 1, &bm->Box3));
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, 1, 1, &bm->Row3));
+    }
+    if (p.use_tma32) {
+        KPM_TRY(make_vec_map(h, p, base, p.TX32 + 4, p.TY32, 1, &bm->A32, p.TL32));
+        KPM_TRY(make_vec_map(h, p, base, p.TX32 + 4, 2, 1, &bm->A32r, p.TL32));
+        KPM_TRY(make_vec_map(h, p, base, p.TX32 + 2, p.TY32, 1, &bm->P32, p.TL32));
+        KPM_TRY(make_vec_map(h, p, base, p.TX32 + 2, 1, 1, &bm->P32r, p.TL32));
     }
     if (p.use_tmak) {
         KPM_TRY(make_vec_map(h, p, base, p.TXK, 1, 1, &bm->AK, p.TLK));
@@ -640,6 +711,57 @@ kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     if (p.KSK == 3 && p.TLK == 16) return launch_tmak_s<3, 16, 32>(h, p, A, P, E, EH, g, tail);
     if (p.KSK == 3 && p.TLK == 8) return launch_tmak_s<3, 8, 64>(h, p, A, P, E, EH, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d", p.KSK, p.TLK);
+}
+
+// eps~ in the x-row frame layout [L2][L1][L0+4] with a box of bx x by sites (3D two-step kernel)
+kpm_status make_epsf_map(const kpm_handle_s* h, int bx, int by, CUtensorMap* m) {
+    EncodeFn enc = get_encode();
+    if (!enc) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t pitch = (cuuint64_t)h->L[0] + 4;
+    cuuint64_t dims[3] = {pitch, (cuuint64_t)h->L[1], (cuuint64_t)h->L[2]};
+    cuuint64_t strides[2] = {pitch * 8, pitch * h->L[1] * 8};
+    cuuint32_t box[3] = {(cuuint32_t)bx, (cuuint32_t)by, 1};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, h->d_epsf, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(KPM_ERR_CUDA, "cuTensorMapEncodeTiled (eps frame) failed: %d", (int)r);
+    return KPM_OK;
+}
+
+template <int TX, int TY, int TL, bool ONSITE, int NT, int KA = kKA32, int KP = kKP32>
+kpm_status launch_tma32_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                          const CUtensorMap& E1, const kpm::Tma32Geom& g, int tail) {
+    auto kern = kpm::kpm_step32_tma_kernel<TX, TY, TL, ONSITE, NT, KA, KP>;
+    static size_t configured = 0;
+    if (configured < p.tma32_smem) {
+        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma32_smem));
+        configured = p.tma32_smem;
+    }
+    kern<<<p.tma32_grid, NT, p.tma32_smem, h->stream>>>(A.A32, A.A32r, P.P32, P.P32r, E, E1, g, tail);
+    KPM_CUDA(cudaGetLastError());
+    h->total_launches++;
+    return KPM_OK;
+}
+
+// instantiated shapes of the 3D two-step kernel (see step32_smem)
+kpm_status launch_tma32(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                        const CUtensorMap& E1, const kpm::Tma32Geom& g, int tail) {
+    const bool on = h->d_eps != nullptr;
+    if (p.TX32 == 8 && p.TY32 == 8 && p.TL32 == 8) {
+        if (nt32() == 512)
+            return on ? launch_tma32_t<8, 8, 8, true, 512>(h, p, A, P, E, E1, g, tail)
+                      : launch_tma32_t<8, 8, 8, false, 512>(h, p, A, P, E, E1, g, tail);
+        return on ? launch_tma32_t<8, 8, 8, true, 256>(h, p, A, P, E, E1, g, tail)
+                  : launch_tma32_t<8, 8, 8, false, 256>(h, p, A, P, E, E1, g, tail);
+    }
+    if (p.TX32 == 16 && p.TY32 == 4 && p.TL32 == 8)
+        return on ? launch_tma32_t<16, 4, 8, true, 256>(h, p, A, P, E, E1, g, tail) : launch_tma32_t<16, 4, 8, false, 256>(h, p, A, P, E, E1, g, tail);
+    if (p.TX32 == 8 && p.TY32 == 4 && p.TL32 == 16)
+        return on ? launch_tma32_t<8, 4, 16, true, 256>(h, p, A, P, E, E1, g, tail) : launch_tma32_t<8, 4, 16, false, 256>(h, p, A, P, E, E1, g, tail);
+    if (p.TX32 == 16 && p.TY32 == 8 && p.TL32 == 8)
+        return on ? launch_tma32_t<16, 8, 8, true, 256, 3, 2>(h, p, A, P, E, E1, g, tail)
+                  : launch_tma32_t<16, 8, 8, false, 256, 3, 2>(h, p, A, P, E, E1, g, tail);
+    return fail(KPM_ERR_UNSUPPORTED, "no 3D two-step kernel for %dx%dx%d", p.TX32, p.TY32, p.TL32);
 }
 
 template <int TX, int TY, int TL, bool ONSITE>
@@ -791,6 +913,8 @@ struct Run {
     kpm::TmaGeom tg{};
     kpm::Tma2Geom tg2{};
     kpm::TmaKGeom tgk{};
+    kpm::Tma32Geom tg32{};
+    CUtensorMap mapE32, mapE32r;     // eps~ frame: (TX+4) x TY box, (TX+4) x 1 box (3D two-step kernel)
     double2 *cur = nullptr, *prev = nullptr, *spare0 = nullptr, *spare1 = nullptr;
     int n = 1, nsteps = 0;
     double vbytes = 0, ebytes = 0, mbytes = 0;
@@ -827,7 +951,7 @@ struct Run {
         KPM_CUDA(cudaSetDevice(h->device));
         KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p));
         if (ensure_workspace(h, p.total) != KPM_OK) {
-            if (!p.use_tma2) return KPM_ERR_OOM;
+            if (!p.use_tma2 && !p.use_tma32) return KPM_ERR_OOM;
             // four vector blocks do not fit: fall back to in-place single steps (two blocks)
             KPM_TRY(make_plan(h, N, R, flags, r0 != nullptr, &p, true));
             KPM_TRY(ensure_workspace(h, p.total));
@@ -866,6 +990,7 @@ struct Run {
         v.D_total = h->D_total;
         v.i_off = h->rows ? h->z0 * h->plane : 0;
         v.ghost = h->rows ? 1 : 0;
+        v.gmap = h->kind == KIND_ELL ? h->d_gmap : nullptr;
         v.L0 = (int)h->L[0];
         v.xpad = p.xpad;
 
@@ -911,15 +1036,21 @@ struct Run {
         memset(&mapEf, 0, sizeof mapEf);
         memset(&mapEK, 0, sizeof mapEK);
         memset(&mapEKH, 0, sizeof mapEKH);
+        memset(&mapE32, 0, sizeof mapE32);
+        memset(&mapE32r, 0, sizeof mapE32r);
         if (p.use_tma && nsteps > 0) {
             double2* bufs[4] = {P, C, X2, X3};
-            nmaps = (p.use_tma2 || p.use_tmak) ? 4 : 2;
+            nmaps = (p.use_tma2 || p.use_tmak || p.use_tma32) ? 4 : 2;
             for (int i = 0; i < nmaps; ++i) KPM_TRY(make_buf_maps(h, p, base_of(bufs[i]), &maps[i]));
             if (h->d_eps) {
                 KPM_TRY(make_eps_map(h, p, &mapE));
                 if (p.use_tma2) {
                     KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
                     KPM_TRY(make_eps_map_w(h, p, p.TX2, &mapEf));
+                }
+                if (p.use_tma32) {
+                    KPM_TRY(make_epsf_map(h, p.TX32 + 4, p.TY32, &mapE32));
+                    KPM_TRY(make_epsf_map(h, p.TX32 + 4, 1, &mapE32r));
                 }
                 if (p.use_tmak) {
                     KPM_TRY(make_eps_map_w(h, p, p.TXK, &mapEK));
@@ -975,6 +1106,24 @@ struct Run {
             tgk.phase = tg.phase;
             tgk.slot_stride = (long long)slot;
             tgk.rows_total = p.gx;
+            if (p.use_tma32) {
+                tg32.L0 = tg.L0;
+                tg32.L1 = tg.L1;
+                tg32.L2 = tg.L2;
+                tg32.PX = (int)(h->L[0] / p.TX32);
+                tg32.PY = (int)(h->L[1] / p.TY32);
+                tg32.G_L = p.RG / p.TL32;
+                tg32.RG = p.RG;
+                tg32.RP = p.RP;
+                const long long cols = (long long)tg32.G_L * tg32.PX * tg32.PY;
+                tg32.rr = p.tma32_rr;
+                tg32.W = p.tma32_rr ? cols : cols * tg32.L2;
+                tg32.rows_total = p.gx;
+                tg32.pfirst = env_int("KPM_TMA32_PFIRST", 1);  // measured: evict-first a_{n-1} 5.3 GB vs 6.2 GB DRAM reads
+                tg32.lg_fast = env_int("KPM_TMA32_LGFAST", 0);
+                tg32.t = tg.t;
+                tg32.shift = tg.shift;
+            }
         }
         cur = C;
         prev = P;
@@ -1097,6 +1246,31 @@ struct Run {
         return exchange_hook ? exchange_hook(this) : KPM_OK;
     }
     kpm_status exchange_on(double2* X, cudaStream_t st);
+    // General sparse row partition: pack the rows each peer needs, NCCL send/recv straight into
+    // the ghost range of that peer (ghosts are grouped by owner).  World 1 has no ghosts.
+    kpm_status exchange_ell(double2* X, cudaStream_t st) {
+        if (h->dist.world == 1 || (h->n_ghost == 0 && h->n_send == 0)) return KPM_OK;
+        if (h->dist.comm != KPM_COMM_NCCL || !h->nccl) return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL handles need kpm_moments_group");
+        double2* sendbuf = reinterpret_cast<double2*>(h->ws + p.off_send);
+        if (h->n_send) {
+            const long long ne = h->n_send * (long long)p.RG;
+            const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
+            kpm::gather_lanes_kernel<<<blocks, 256, 0, st>>>(X, h->d_send, h->n_send, p.RG, sendbuf);
+            KPM_CUDA(cudaGetLastError());
+            h->total_launches++;
+        }
+        const size_t lb = (size_t)p.RG * sizeof(double2);
+        ncclResult_t e = ncclGroupStart();
+        for (int q = 0; q < h->dist.world && e == ncclSuccess; ++q) {
+            if (h->scnt[q]) e = ncclSend(sendbuf + h->soff[q] * p.RG, h->scnt[q] * lb, ncclUint8, q, h->nccl, st);
+            if (e == ncclSuccess && h->rcnt[q])
+                e = ncclRecv(X + (h->D + h->roff[q]) * p.RG, h->rcnt[q] * lb, ncclUint8, q, h->nccl, st);
+        }
+        ncclResult_t e2 = ncclGroupEnd();
+        if (e != ncclSuccess || e2 != ncclSuccess)
+            return fail(KPM_ERR_UNSUPPORTED, "NCCL ghost exchange: %s", ncclGetErrorString(e != ncclSuccess ? e : e2));
+        return KPM_OK;
+    }
     kpm_status (*exchange_hook)(Run*) = nullptr;
 
     bool more() const { return n <= nsteps; }
@@ -1130,6 +1304,25 @@ struct Run {
             h->steps_bytes += 4.0 * vbytes + ebytes;
             h->step_launches++;
             n += KS;
+            return KPM_OK;
+        }
+        if (!direct && p.use_tma32 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1))) {
+            // steps n and n+1 (3D): slots 2n .. 2n+3 (+ odd-N tail 2n+4)
+            const bool tail = (N & 1) && n + 1 == nsteps;
+            for (int k = 0; k < 4; ++k) tg32.red[k] = part + (size_t)(2 * n + k) * slot;
+            tg32.red[4] = tail ? part + (size_t)(2 * n + 4) * slot : nullptr;
+            tg32.outB = spare0;
+            tg32.outC = spare1;
+            KPM_TRY(launch_tma32(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapE32, mapE32r, tg32, tail));
+            double2* oc = cur;
+            double2* op = prev;
+            cur = spare1;
+            prev = spare0;
+            spare0 = oc;
+            spare1 = op;
+            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->step_launches++;
+            n += 2;
             return KPM_OK;
         }
         const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1));
@@ -1255,6 +1448,7 @@ struct Run {
 // Halo exchange of a single row-partitioned handle: world 1 (periodic wrap inside the
 // slab) or NCCL send/recv with the two neighbouring ranks, on the handle's stream.
 kpm_status Run::exchange_on(double2* X, cudaStream_t st) {
+    if (h->kind == KIND_ELL) return exchange_ell(X, st);
     const size_t pb = plane_bytes();
     if (h->dist.comm == KPM_COMM_SELF) {
         KPM_CUDA(cudaMemcpyAsync(ghost_lo(X), last_plane(X), pb, cudaMemcpyDeviceToDevice, st));
@@ -1288,6 +1482,25 @@ kpm_status exchange_group(std::vector<Run>& runs, std::vector<cudaEvent_t>& evs)
         KPM_CUDA(cudaSetDevice(runs[i].h->device));
         KPM_CUDA(cudaEventRecord(evs[i], runs[i].h->stream));
     }
+    if (runs[0].h->kind == KIND_ELL) {
+        // every rank gathers its ghost sites, peer by peer, from the owners' fresh blocks
+        // (same device: plain loads; see kpm_moments_group)
+        for (int i = 0; i < W; ++i) {
+            Run& r = runs[i];
+            KPM_CUDA(cudaSetDevice(r.h->device));
+            for (int q = 0; q < W; ++q) {
+                if (!r.h->rcnt[q]) continue;
+                KPM_CUDA(cudaStreamWaitEvent(r.h->stream, evs[q], 0));
+                const long long n = r.h->rcnt[q], ne = n * r.p.RG;
+                const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * r.h->num_sms);
+                kpm::gather_lanes_kernel<<<blocks, 256, 0, r.h->stream>>>(runs[q].pending, r.h->d_ghost_src + r.h->roff[q], n,
+                                                                          r.p.RG, r.pending + (r.h->D + r.h->roff[q]) * r.p.RG);
+                KPM_CUDA(cudaGetLastError());
+                r.h->total_launches++;
+            }
+        }
+        return KPM_OK;
+    }
     for (int i = 0; i < W; ++i) {
         Run& r = runs[i];
         Run& rl = runs[(i - 1 + W) % W];
@@ -1317,9 +1530,13 @@ void kpm_destroy(kpm_handle h) {
     if (h->ws_own && h->ws) cudaFreeAsync(h->ws, h->stream);
     if (h->stream) cudaStreamSynchronize(h->stream);
     cudaFree(h->d_eps);
+    cudaFree(h->d_epsf);
     cudaFree(h->d_phase);
     cudaFree(h->d_col);
     cudaFree(h->d_val);
+    cudaFree(h->d_gmap);
+    cudaFree(h->d_ghost_src);
+    cudaFree(h->d_send);
     cudaFree(h->d_dense);
     if (h->nccl) ncclCommDestroy(h->nccl);
     if (h->ev_begin) cudaEventDestroy(h->ev_begin);
@@ -1416,6 +1633,20 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
         cudaError_t ce = cudaMalloc(&h->d_eps, h->D * sizeof(double));
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_eps, e.data(), h->D * sizeof(double), cudaMemcpyHostToDevice);
         if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site upload: %s", cudaGetErrorString(ce));
+        if (st == KPM_OK && h->ndim == 3 && !h->rows) {
+            // x-row frame copy for the 3D two-step kernel: row pitch L0 + 4, two periodic images per side
+            const size_t L0 = (size_t)h->L[0], rowsN = (size_t)(h->L[1] * h->L[2]), pf = (L0 + 4) * 8;
+            ce = cudaMalloc(&h->d_epsf, rowsN * pf);
+            if (ce == cudaSuccess) ce = cudaMemcpy2D(h->d_epsf + 2, pf, h->d_eps, L0 * 8, L0 * 8, rowsN, cudaMemcpyDeviceToDevice);
+            for (int s2 = 0; s2 < 2 && ce == cudaSuccess; ++s2) {
+                // frame x = s2 (site L0-2+s2) and frame x = L0+2+s2 (site s2)
+                const size_t src_lo = (L0 - 2 + s2) % L0, src_hi = (size_t)s2 % L0;
+                ce = cudaMemcpy2D(h->d_epsf + s2, pf, h->d_eps + src_lo, L0 * 8, 8, rowsN, cudaMemcpyDeviceToDevice);
+                if (ce == cudaSuccess)
+                    ce = cudaMemcpy2D(h->d_epsf + L0 + 2 + s2, pf, h->d_eps + src_hi, L0 * 8, 8, rowsN, cudaMemcpyDeviceToDevice);
+            }
+            if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site frame: %s", cudaGetErrorString(ce));
+        }
     }
     if (st == KPM_OK && d->flux != 0.0) {
         std::vector<double2> ph(h->L[0]);
@@ -1436,6 +1667,132 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
     return KPM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Row partition of an ELL matrix (every rank passes the whole matrix):
+// rank g keeps rows [r0, r1) = kpm_slab_range(D, g, W); the columns outside them become ghost
+// sites after the local rows (ascending global index = grouped by owner rank, so each peer's
+// ghosts are one contiguous receive range); the send lists are the other ranks' ghost sets
+// restricted to [r0, r1), computed here from the same matrix (no communication).
+struct EllPartition {
+    int64_t r0 = 0, nl = 0;
+    std::vector<int32_t> ghosts;  // global index of ghost k (ascending)
+    std::vector<int32_t> gsrc;    // row of ghost k inside its owner's block
+    std::vector<int32_t> send;    // local rows to send, peer by peer
+    std::vector<int64_t> roff, rcnt, soff, scnt;
+};
+
+// c: [K][D] global columns (padding = the row itself)
+kpm_status ell_partition(int64_t D, int64_t K, const int32_t* c, int g, int W, EllPartition* P) {
+    if (W < 1 || g < 0 || g >= W) return fail(KPM_ERR_INVALID_ARG, "bad rank %d / world %d", g, W);
+    std::vector<int64_t> r0s(W + 1);
+    for (int q = 0; q <= W; ++q) r0s[q] = D * q / W;
+    P->r0 = r0s[g];
+    P->nl = r0s[g + 1] - P->r0;
+    if (P->nl < 1) return fail(KPM_ERR_INVALID_ARG, "rank %d of %d owns no rows (D=%lld)", g, W, (long long)D);
+    auto owner = [&](int64_t j) { return (int)(std::upper_bound(r0s.begin(), r0s.end(), j) - r0s.begin()) - 1; };
+    auto ghosts_of = [&](int q) {  // sorted distinct columns of rank q's rows outside its range
+        std::vector<int32_t> gs;
+        for (int64_t k = 0; k < K; ++k)
+            for (int64_t i = r0s[q]; i < r0s[q + 1]; ++i) {
+                const int32_t j = c[k * D + i];
+                if (j < r0s[q] || j >= r0s[q + 1]) gs.push_back(j);
+            }
+        std::sort(gs.begin(), gs.end());
+        gs.erase(std::unique(gs.begin(), gs.end()), gs.end());
+        return gs;
+    };
+    P->ghosts = ghosts_of(g);
+    P->roff.assign(W, 0);
+    P->rcnt.assign(W, 0);
+    P->soff.assign(W, 0);
+    P->scnt.assign(W, 0);
+    P->gsrc.resize(P->ghosts.size());
+    for (size_t k = 0; k < P->ghosts.size(); ++k) {
+        const int q = owner(P->ghosts[k]);
+        if (P->rcnt[q] == 0) P->roff[q] = (int64_t)k;
+        P->rcnt[q]++;
+        P->gsrc[k] = (int32_t)(P->ghosts[k] - r0s[q]);
+    }
+    P->send.clear();
+    for (int q = 0; q < W; ++q) {
+        P->soff[q] = (int64_t)P->send.size();
+        if (q != g)
+            for (int32_t j : ghosts_of(q))
+                if (j >= P->r0 && j < P->r0 + P->nl) P->send.push_back((int32_t)(j - P->r0));
+        P->scnt[q] = (int64_t)P->send.size() - P->soff[q];
+    }
+    return KPM_OK;
+}
+
+// Turn handle h into rank dist->rank's block of the row partition; `c`, `v` ([K][D] global) are
+// replaced by the local [K][r1-r0] arrays with extended-block columns.
+kpm_status ell_rows_setup(kpm_handle_s* h, const kpm_dist* dist, std::vector<int32_t>& c, std::vector<double>& v,
+                          int w) {
+    const int W = dist->world, g = dist->rank;
+    const int64_t D = h->D_total, K = h->K;
+    EllPartition P;
+    KPM_TRY(ell_partition(D, K, c.data(), g, W, &P));
+    const int64_t r0 = P.r0, nl = P.nl;
+    const std::vector<int32_t>& mine = P.ghosts;
+    h->rows = true;
+    h->slow = 0;
+    h->plane = 1;
+    h->z0 = r0;
+    h->nloc = nl;
+    h->Lm_global = D;
+    h->D = nl;
+    h->n_ghost = (int64_t)mine.size();
+    h->roff = P.roff;
+    h->rcnt = P.rcnt;
+    h->soff = P.soff;
+    h->scnt = P.scnt;
+    std::vector<long long> gmap(mine.begin(), mine.end());
+    const std::vector<int32_t>& gsrc = P.gsrc;
+    const std::vector<int32_t>& send = P.send;
+    h->n_send = (int64_t)send.size();
+    // local ELL: rows [r0, r0+nl), columns -> extended block index
+    std::vector<int32_t> cl((size_t)K * nl);
+    std::vector<double> vl((size_t)K * nl * w);
+    for (int64_t k = 0; k < K; ++k)
+        for (int64_t i = 0; i < nl; ++i) {
+            const int32_t j = c[k * D + r0 + i];
+            int32_t jl;
+            if (j >= r0 && j < r0 + nl) jl = (int32_t)(j - r0);
+            else jl = (int32_t)(nl + (std::lower_bound(mine.begin(), mine.end(), j) - mine.begin()));
+            cl[k * nl + i] = jl;
+            for (int q = 0; q < w; ++q) vl[(k * nl + i) * w + q] = v[(k * D + r0 + i) * w + q];
+        }
+    c.swap(cl);
+    v.swap(vl);
+    cudaError_t ce = cudaSuccess;
+    if (h->n_ghost) {
+        ce = cudaMalloc(&h->d_gmap, gmap.size() * sizeof(long long));
+        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_gmap, gmap.data(), gmap.size() * sizeof(long long), cudaMemcpyHostToDevice);
+        if (ce == cudaSuccess) ce = cudaMalloc(&h->d_ghost_src, gsrc.size() * sizeof(int32_t));
+        if (ce == cudaSuccess)
+            ce = cudaMemcpy(h->d_ghost_src, gsrc.data(), gsrc.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    }
+    if (ce == cudaSuccess && h->n_send) {
+        ce = cudaMalloc(&h->d_send, send.size() * sizeof(int32_t));
+        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_send, send.data(), send.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
+    }
+    if (ce != cudaSuccess) return fail(KPM_ERR_CUDA, "row-partition lists: %s", cudaGetErrorString(ce));
+    if (dist->comm == KPM_COMM_NCCL) {
+        ncclUniqueId id;
+        memcpy(&id, dist->nccl_id, sizeof id);
+        ncclResult_t nr = ncclCommInitRank(&h->nccl, W, id, g);
+        if (nr != ncclSuccess) return fail(KPM_ERR_UNSUPPORTED, "ncclCommInitRank: %s", ncclGetErrorString(nr));
+    }
+    return KPM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* val, int32_t dtype, double a,
                           double b, int32_t device, const kpm_dist* dist, kpm_handle* out) {
     if (D < 1 || D >= (1LL << 31) || K < 0 || (K > 0 && (!col || !val)))
@@ -1453,8 +1810,6 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
         c[e] = j < 0 ? (int32_t)i : j;  // padding -> (row, 0)
         for (int q = 0; q < w; ++q) v[e * w + q] = j < 0 ? 0.0 : vin[e * w + q] / a;
     }
-    if (dist && dist->partition == KPM_PART_ROWS)
-        return fail(KPM_ERR_UNSUPPORTED, "row partition is implemented for lattice stencils only");
     kpm_handle_s* h = nullptr;
     KPM_TRY(new_handle(device, dist, &h));
     h->kind = KIND_ELL;
@@ -1465,7 +1820,8 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
     h->D = D;
     h->K = K;
     kpm_status st = KPM_OK;
-    if (K > 0) {
+    if (dist && dist->partition == KPM_PART_ROWS) st = ell_rows_setup(h, dist, c, v, w);
+    if (st == KPM_OK && K > 0) {
         cudaError_t ce = cudaMalloc(&h->d_col, c.size() * sizeof(int32_t));
         if (ce == cudaSuccess) ce = cudaMalloc(&h->d_val, v.size() * sizeof(double));
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_col, c.data(), c.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
@@ -1556,6 +1912,40 @@ kpm_status kpm_create_csr(int64_t D, const int64_t* rowptr, const int32_t* col, 
     return kpm_create_ell(D, K, c.data(), v.data(), dtype, a, b, device, dist, out);
 }
 
+kpm_status kpm_csr_partition(int64_t D, const int64_t* rowptr, const int32_t* col, int32_t rank, int32_t world,
+                             int64_t counts[3], int64_t* ghosts, int64_t* send_rows, int64_t* peers) {
+    if (D < 1 || D >= (1LL << 31) || !rowptr || !col || !counts) return fail(KPM_ERR_INVALID_ARG, "bad CSR arguments");
+    if (rowptr[0] != 0) return fail(KPM_ERR_INVALID_ARG, "rowptr[0] must be 0");
+    int64_t K = 0;
+    for (int64_t i = 0; i < D; ++i) {
+        if (rowptr[i + 1] < rowptr[i]) return fail(KPM_ERR_INVALID_ARG, "rowptr not monotone at row %lld", (long long)i);
+        K = std::max<int64_t>(K, rowptr[i + 1] - rowptr[i]);
+    }
+    std::vector<int32_t> c((size_t)K * D);
+    for (int64_t i = 0; i < D; ++i)
+        for (int64_t k = 0; k < K; ++k) {
+            const int64_t e = rowptr[i] + k;
+            const int32_t j = e < rowptr[i + 1] ? col[e] : (int32_t)i;
+            if (j < 0 || j >= D) return fail(KPM_ERR_INVALID_ARG, "CSR column %d out of range in row %lld", j, (long long)i);
+            c[k * D + i] = j;
+        }
+    EllPartition P;
+    KPM_TRY(ell_partition(D, K, c.data(), rank, world, &P));
+    counts[0] = P.nl;
+    counts[1] = (int64_t)P.ghosts.size();
+    counts[2] = (int64_t)P.send.size();
+    if (ghosts) std::copy(P.ghosts.begin(), P.ghosts.end(), ghosts);
+    if (send_rows) std::copy(P.send.begin(), P.send.end(), send_rows);
+    if (peers)
+        for (int q = 0; q < world; ++q) {
+            peers[4 * q] = P.roff[q];
+            peers[4 * q + 1] = P.rcnt[q];
+            peers[4 * q + 2] = P.soff[q];
+            peers[4 * q + 3] = P.scnt[q];
+        }
+    return KPM_OK;
+}
+
 kpm_status kpm_set_stream(kpm_handle h, void* stream) {
     if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
     KPM_CUDA(cudaSetDevice(h->device));
@@ -1622,6 +2012,8 @@ kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, u
         if (!hs[i] || !hs[i]->rows || hs[i]->dist.comm != KPM_COMM_LOCAL || hs[i]->dist.rank != i ||
             hs[i]->dist.world != nh)
             return fail(KPM_ERR_INVALID_ARG, "handle %d is not rank %d of a KPM_COMM_LOCAL row partition of %d", i, i, nh);
+        if (hs[i]->kind != hs[0]->kind || (hs[i]->kind == KIND_ELL && hs[i]->device != hs[0]->device))
+            return fail(KPM_ERR_UNSUPPORTED, "in-process ELL row partitions: one kind, one device");
     }
     std::vector<Run> runs(nh);
     std::vector<cudaEvent_t> evs(nh, nullptr);
@@ -1802,8 +2194,9 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[4] = p.gx;
     info[5] = (int64_t)p.tma_smem;
     info[6] = p.RG;
-    info[7] = p.tma_rr | (p.use_tma2 ? 2 : 0) | (p.overlap ? 4 : 0) | (p.use_tma3 ? 8 : 0);
-    info[8] = p.use_tma2 ? p.TX2 : 0;
+    info[7] = p.tma_rr | ((p.use_tma2 || p.use_tma32) ? 2 : 0) | (p.overlap ? 4 : 0) | (p.use_tma3 ? 8 : 0) |
+              (p.use_tma32 ? 16 : 0);
+    info[8] = p.use_tma2 ? p.TX2 : (p.use_tma32 ? p.TX32 * 100 + p.TY32 : 0);
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;
     info[11] = p.use_tmak ? p.KSK : 0;

@@ -149,6 +149,7 @@ struct VecArgs {
     long long D_total;     // global number of sites (RNG counter stride)
     long long i_off;       // global index of this GPU's site 0
     const long long* sites;// KPM_LOCAL: global site of each global vector (unit start vectors e_site), else nullptr
+    const long long* gmap; // ELL row partition: global index of ghost site D + k (k < n_ghost), else nullptr
     int ghost;             // row partition: site indices j < 0 or >= D are ghost sites (wrap globally)
     int L0;                // x extent
     int xpad;              // 3D lattices: 2 -- vector blocks store each x-row with a 2-site frame of
@@ -184,7 +185,11 @@ __device__ __forceinline__ void store_site(const VecArgs& v, double2* buf, int s
 template <bool CPLX>
 __device__ __forceinline__ double2 gen_lane(const VecArgs& v, int j, int rg) {
     long long ig = v.i_off + j;
-    if (v.ghost) ig = (ig % v.D_total + v.D_total) % v.D_total;  // ghost plane of a neighbouring slab
+    if (v.gmap) {
+        if (j >= v.D) ig = __ldg(v.gmap + (j - v.D));  // ghost site of a general sparse row partition
+    } else if (v.ghost) {
+        ig = (ig % v.D_total + v.D_total) % v.D_total;  // ghost plane of a neighbouring slab
+    }
     if (v.sites) {  // unit start vectors |r> = e_{site(r)} (local DoS)
         auto unit = [&](long long r) { return (r < v.R_loc && __ldg(v.sites + v.r_off + r) == ig) ? 1.0 : 0.0; };
         return CPLX ? make_double2(unit(rg), 0.0) : make_double2(unit(2LL * rg), unit(2LL * rg + 1));
@@ -295,6 +300,15 @@ __global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restric
             val = make_double2(r < R_loc ? r0[(size_t)r * D + s] : 0.0, r + 1 < R_loc ? r0[(size_t)(r + 1) * D + s] : 0.0);
         }
         store_site(v, out, s, v.mem(s), rg, val, false);
+    }
+}
+
+// dst[k][l] = src[idx[k]][l] over n sites of RG 16-byte lanes (row-partition ghost exchange).
+__global__ void gather_lanes_kernel(const double2* __restrict__ src, const int* __restrict__ idx, long long n, int RG,
+                                    double2* __restrict__ dst) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * RG; e += (long long)gridDim.x * blockDim.x) {
+        const long long k = e / RG;
+        dst[e] = src[(long long)__ldg(idx + k) * RG + (e - k * RG)];
     }
 }
 

@@ -36,7 +36,7 @@ EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershg
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
            "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moments_local", "kpm_create_dense",
-           "kpm_gershgorin_dense", "kpm_destroy",
+           "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_destroy",
            "kpm_last_error", "kpm_version"]
 
 
@@ -56,6 +56,7 @@ _SIG = {
     "kpm_create_stencil": [ctypes.POINTER(kpm_stencil_desc), _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
     "kpm_create_csr": [_i64, _P, _P, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
     "kpm_create_ell": [_i64, _i32, _P, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
+    "kpm_csr_partition": [_i64, _P, _P, _i32, _i32, _P, _P, _P, _P],
     "kpm_gershgorin_stencil": [ctypes.POINTER(kpm_stencil_desc), _f64, _P, _P],
     "kpm_gershgorin_csr": [_i64, _P, _P, _P, _i32, _f64, _P, _P],
     "kpm_set_stream": [_P, _P],
@@ -257,6 +258,7 @@ class Handle:
         d["two_step"] = int((info[7] >> 1) & 1)
         d["overlap"] = int((info[7] >> 2) & 1)
         d["box3"] = int((info[7] >> 3) & 1)  # 3D dense-box march kernel (kpm_tma3.cuh)
+        d["two_step3d"] = int((info[7] >> 4) & 1)  # 3D two-step kernel (kpm_tma32.cuh)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
         return d
 
@@ -287,7 +289,15 @@ def kpm_create_csr(D, rowptr, col, val, a, b, device=0, dist=None) -> Handle:
     dp, _keep = _dist(dist)
     _check(_lib.kpm_create_csr(int(D), _ptr(rowptr), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
                                dp, ctypes.byref(h)))
-    return Handle(h.value, D, dist=dist)
+    return _sparse_handle(h.value, D, dist)
+
+
+def _sparse_handle(raw, D, dist):
+    """Row partition of a general sparse H: this rank owns rows kpm_slab_range(D, rank, world)."""
+    hd = Handle(raw, D, dist=dist)
+    if dist is not None and dist[0] == KPM_PART_ROWS:
+        hd.D_local = kpm_slab_range(D, dist[1], dist[2])[1]
+    return hd
 
 
 def kpm_create_dense(H, a, b, device=0, dist=None) -> Handle:
@@ -319,7 +329,7 @@ def kpm_create_ell(D, K, col, val, a, b, device=0, dist=None) -> Handle:
     dp, _keep = _dist(dist)
     _check(_lib.kpm_create_ell(int(D), int(K), _ptr(col), _ptr(v), dt, float(a), float(b), int(device),
                                dp, ctypes.byref(h)))
-    return Handle(h.value, D, dist=dist)
+    return _sparse_handle(h.value, D, dist)
 
 
 def kpm_moments(h: Handle, N, R, seed):
@@ -340,6 +350,23 @@ def kpm_assemble_host(S, N, D, R, flags=0):
     mu = np.zeros(int(N), dtype=np.float64)
     _check(_lib.kpm_assemble(None, _ptr(S), int(N), int(D), int(R), int(flags) & ~KPM_DEVICE_OUT, _ptr(mu)))
     return mu
+
+
+def kpm_csr_partition(D, rowptr, col, rank, world):
+    """Host-side row-partition plan of a CSR matrix (include/kpm.h): dict with n_local, ghosts
+    (global indices, ascending), send_rows (local rows per peer) and peers [world][4] =
+    (ghost offset, ghost count, send offset, send count)."""
+    rowptr = np.ascontiguousarray(rowptr, dtype=np.int64)
+    col = np.ascontiguousarray(col, dtype=np.int32)
+    counts = np.zeros(3, dtype=np.int64)
+    _check(_lib.kpm_csr_partition(int(D), _ptr(rowptr), _ptr(col), int(rank), int(world), _ptr(counts),
+                                  None, None, None))
+    ghosts = np.zeros(int(counts[1]), dtype=np.int64)
+    send = np.zeros(int(counts[2]), dtype=np.int64)
+    peers = np.zeros((int(world), 4), dtype=np.int64)
+    _check(_lib.kpm_csr_partition(int(D), _ptr(rowptr), _ptr(col), int(rank), int(world), _ptr(counts),
+                                  _ptr(ghosts), _ptr(send), _ptr(peers)))
+    return dict(n_local=int(counts[0]), ghosts=ghosts, send_rows=send, peers=peers)
 
 
 def kpm_slab_range(Lm, rank, world):

@@ -108,7 +108,10 @@ def test_tma_march_matches_oracle(kpm, case, monkeypatch):
     info = h.plan_info(N, R)
     assert info["tma"] == 1, info
     assert info["round_robin"] == (case == "3d_round_robin"), info
-    assert info["two_step"] == (lat["ndim"] == 2 and lat["L"][0] % (1024 // info["TL"]) == 0), info
+    if lat["ndim"] == 2:
+        assert info["two_step"] == (lat["L"][0] % (1024 // info["TL"]) == 0), info
+    else:  # the 3D two-step kernel (kpm_tma32.cuh) is opt-in
+        assert info["two_step"] == info["two_step3d"] == 0, info
     mu = h.moments(N, R, 21)
     assert normwise(mu, ref) < TOL
     pv = h.moments_ex(N, R, 21, flags=kpm.KPM_PER_VECTOR)
@@ -117,6 +120,10 @@ def test_tma_march_matches_oracle(kpm, case, monkeypatch):
     assert np.array_equal(h.moments_ex(N, R, 21, r0=r), mu)
     if lat["ndim"] == 3:  # dense-box kernel (kpm_tma3.cuh) vs the generic-tile march kernel
         assert info["box3"] == ((info["TX"], info["TY"], info["TL"]) in [(16, 8, 8), (8, 8, 16), (4, 8, 32)]), info
+        monkeypatch.setenv("KPM_TMA32", "1")  # opt-in 3D two-step kernel
+        assert h.plan_info(N, R)["two_step3d"] == 1
+        assert normwise(h.moments(N, R, 21), ref) < TOL
+        monkeypatch.delenv("KPM_TMA32")
         monkeypatch.setenv("KPM_NO_TMA3", "1")
         assert h.plan_info(N, R)["box3"] == 0
         assert normwise(h.moments(N, R, 21), ref) < TOL
@@ -128,6 +135,7 @@ def test_3d_box_kernel_every_tile_width(kpm, tl, monkeypatch):
     plan's TL forced by KPM_TMA_TL), on-site disorder, round-robin columns, vs the oracle."""
     monkeypatch.setenv("KPM_NO_SMALL", "1")
     monkeypatch.setenv("KPM_TMA_TL", str(tl))
+    monkeypatch.setenv("KPM_NO_TMA32", "1")  # every step through the single-step kernel
     lat = lat_of(3, (32, 24, 10), W=2.0)
     N, R = 23, 64
     H = oracle.lattice_csr(lat)
@@ -157,6 +165,47 @@ def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
     assert h.plan_info(N, R)["two_step"] == 0
     mu1 = h.moments(N, R, 5)
     assert normwise(mu2, ref) < TOL and normwise(mu1, ref) < TOL
+
+
+THREE_D_TWO_STEP_CASES = {
+    "anderson_rr": (lat_of(3, (64, 32, 6), W=2.0), 64),          # 4 lane groups x 32 pencils: round-robin
+    "clean_rr": (lat_of(3, (64, 64, 5)), 48),                    # 3 lane groups, no on-site array
+    "anderson_contig": (lat_of(3, (16, 16, 10), W=2.0), 32),     # 8 columns -> contiguous plane ranges
+    "single_pencil_L2_2": (lat_of(3, (16, 8, 2), W=1.0), 16),    # z wraps onto itself, H = 1 segments
+    "one_pencil_wide_R": (lat_of(3, (8, 8, 9), W=1.0), 128),     # 8 lane groups of one pencil
+}
+
+
+@pytest.mark.parametrize("shape", [0, 1, 2, 3])
+@pytest.mark.parametrize("case", sorted(THREE_D_TWO_STEP_CASES))
+@pytest.mark.parametrize("N", [6, 7, 8, 9, 12, 15])
+def test_3d_two_step_kernel_matches_oracle(kpm, case, N, shape, monkeypatch):
+    """3D temporal blocking (kpm_tma32.cuh, opt-in KPM_TMA32=1) for every instantiated tile
+    (KPM_TMA32_SHAPE: 8x8 sites x 8 lanes, 16x4x8, 8x4x16, 16x8x8) and every parity of the step count and of N, vs
+    the oracle and vs the single-step dense-box kernel."""
+    monkeypatch.setenv("KPM_NO_SMALL", "1")
+    monkeypatch.setenv("KPM_TMA32", "1")  # opt-in kernel
+    monkeypatch.setenv("KPM_TMA32_SHAPE", str(shape))
+    lat, R = THREE_D_TWO_STEP_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b += 0.02 * a
+    a *= 1.03
+    r = ki.rademacher(8, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b)
+    info = h.plan_info(N, R)
+    tx, ty, tl = {0: (8, 8, 8), 1: (16, 4, 8), 2: (8, 4, 16), 3: (16, 8, 8)}[shape]
+    fits = (lat["L"][0] % tx == 0 and lat["L"][1] % ty == 0 and ((R + 1) // 2) % tl == 0)
+    assert info["two_step3d"] == int(N // 2 - 1 >= 2 and fits), info
+    mu = h.moments(N, R, 8)
+    assert normwise(mu, ref) < TOL
+    pv = h.moments_ex(N, R, 8, flags=kpm.KPM_PER_VECTOR)
+    assert normwise(pv, ref_pv) < TOL
+    assert np.array_equal(h.moments(N, R, 8), mu), "not deterministic"
+    assert np.array_equal(h.moments_ex(N, R, 8, r0=r), mu)
+    monkeypatch.setenv("KPM_NO_TMA32", "1")
+    assert normwise(h.moments(N, R, 8), ref) < TOL
 
 
 KSTEP_CASES = {
@@ -351,6 +400,68 @@ def test_row_partition_local_group_matches_oracle(kpm, case, world):
                                  dist=(kpm.KPM_PART_ROWS, rk, world, kpm.KPM_COMM_LOCAL)) for rk in range(world)]
     mu = kpm.kpm_moments_group(hs, N, R, 8)
     assert normwise(mu, ref) < TOL
+
+
+def random_sparse_hermitian(D, deg, seed, cplx):
+    """Irregular sparse Hermitian H (random graph, long-range bonds, ragged row lengths)."""
+    rng = np.random.default_rng(seed)
+    A = np.zeros((D, D), dtype=np.complex128 if cplx else np.float64)
+    for i in range(D):
+        for j in rng.choice(D, size=int(rng.integers(1, deg + 1)), replace=False):
+            v = rng.normal() + (1j * rng.normal() if cplx else 0.0)
+            A[i, j] += v
+    A = A + A.conj().T
+    A[np.diag_indices(D)] = rng.normal(size=D)
+    return oracle.csr_from_dense(A)
+
+
+SPARSE_ROW_CASES = {
+    "3d_anderson_csr": lambda: oracle.lattice_csr(lat_of(3, (6, 5, 8), W=2.0)),
+    "2d_peierls_csr": lambda: oracle.lattice_csr(lat_of(2, (16, 12), flux=1 / 4)),
+    "random_real": lambda: random_sparse_hermitian(150, 5, 3, False),
+    "random_complex_wide_rows": lambda: random_sparse_hermitian(97, 12, 4, True),
+}
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
+@pytest.mark.parametrize("case", sorted(SPARSE_ROW_CASES))
+def test_csr_row_partition_matches_oracle(kpm, case, world):
+    """General-sparse row partition: `world` CSR handles, each with its
+    row block + ghost sites gathered from the owners after every step (KPM_COMM_LOCAL, one GPU;
+    world 1: KPM_COMM_SELF through kpm_moments), vs the oracle on the same global vectors."""
+    H = SPARSE_ROW_CASES[case]()
+    a, b = oracle.gershgorin(H)
+    b += 0.01 * a
+    a *= 1.02
+    N, R = 29, 6
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(4, R, H.D), N)
+    val = H.val_re + 1j * H.val_im if H.is_complex else H.val_re
+    if world == 1:
+        h = kpm.kpm_create_csr(H.D, H.rowptr, H.col, val, a, b, dist=(kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_SELF))
+        mu = h.moments(N, R, 4)
+        direct = h.moments_ex(N, R, 4, flags=kpm.KPM_DIRECT)
+        assert normwise(direct, oracle.moments_direct(H, a, b, ki.rademacher(4, R, H.D), N)) < TOL
+    else:
+        hs = [kpm.kpm_create_csr(H.D, H.rowptr, H.col, val, a, b,
+                                 dist=(kpm.KPM_PART_ROWS, rk, world, kpm.KPM_COMM_LOCAL)) for rk in range(world)]
+        assert sum(h.D_local for h in hs) == H.D
+        mu = kpm.kpm_moments_group(hs, N, R, 4)
+    assert normwise(mu, ref) < TOL
+
+
+def test_csr_row_partition_nccl_world1(kpm):
+    """The NCCL path of the CSR row partition at world 1 (no ghosts; all-reduce of the sums),
+    with caller start vectors and per-vector output."""
+    H = SPARSE_ROW_CASES["random_real"]()
+    a, b = oracle.gershgorin(H)
+    N, R = 24, 5
+    r = ki.rademacher(2, R, H.D)
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = kpm.kpm_create_csr(H.D, H.rowptr, H.col, H.val_re, a, b,
+                           dist=(kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_NCCL, kpm.kpm_nccl_unique_id()))
+    assert normwise(h.moments(N, R, 2), ref) < TOL
+    assert normwise(h.moments_ex(N, R, 2, r0=r), ref) < TOL
+    assert normwise(h.moments_ex(N, R, 2, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
 
 
 def test_randomized_shapes_sweep(kpm):

@@ -116,12 +116,9 @@ def test_row_partition_nccl_id_broadcast_over_gloo():
     assert out[0] == out[1] and len(out[0]) == 256
 
 
-def test_slab_range_tiles_planes_and_ell_rows_rejected():
+def test_slab_range_tiles_planes():
     from paper_1105_5481_b200 import kpm
     for Lm, world in [(512, 8), (10, 3), (7, 7), (128, 5)]:
         got = [kpm.kpm_slab_range(Lm, r, world) for r in range(world)]
         assert got[0][0] == 0 and sum(c for _, c in got) == Lm and min(c for _, c in got) >= 1
         assert all(got[i][0] + got[i][1] == got[i + 1][0] for i in range(world - 1))
-    with pytest.raises(kpm.KPMError) as e:
-        kpm.kpm_create_ell(10, 1, [[0] * 10], [[0.0] * 10], 1.0, 0.0, dist=(kpm.KPM_PART_ROWS, 0, 1))
-    assert e.value.status == kpm.KPM_ERR_UNSUPPORTED
