@@ -638,19 +638,29 @@ kpm_status make_eps_map_w(const kpm_handle_s* h, const Plan& p, int bx, CUtensor
     return KPM_OK;
 }
 
-template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB>
-kpm_status launch_tma2_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB, int XW>
+kpm_status launch_tma2_x(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
-    auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS, MINB>;
+    auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS, MINB, XW>;
     static size_t configured = 0;
     if (configured < p.tma2_smem) {
         KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma2_smem));
         configured = p.tma2_smem;
     }
-    kern<<<p.tma2_grid, kpm::kThreads2, p.tma2_smem, h->stream>>>(A.A2, A.Col2, P.A2, P.Col, E, E2, g, tail);
+    kern<<<p.tma2_grid, kpm::Threads2<XW>::N, p.tma2_smem, h->stream>>>(A.A2, A.Col2, P.A2, P.Col, E, E2, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
     return KPM_OK;
+}
+
+// Halo warp (XW = 1, kpm_tma2.cuh) for complex128 (Peierls) lattices: c4 3178 vs 3387 ms per call;
+// real lattices keep XW = 0 (c2 26.8 vs 25.9 ms: the 168-register cap of nine warps spills there).
+// KPM_TMA2_XW=0/1 overrides.
+template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB>
+kpm_status launch_tma2_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                         const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
+    if (env_int("KPM_TMA2_XW", PEIERLS ? 1 : 0)) return launch_tma2_x<TL, TX, ONSITE, PEIERLS, MINB, 1>(h, p, A, P, E, E2, g, tail);
+    return launch_tma2_x<TL, TX, ONSITE, PEIERLS, MINB, 0>(h, p, A, P, E, E2, g, tail);
 }
 
 template <int TL, int TX, int MINB>

@@ -110,8 +110,17 @@ struct LoadCursor {
     }
 };
 
-template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB>
-__global__ void __launch_bounds__(kThreads2, MINB)
+// XW = 1: a ninth warp computes the two halo sites of a_{n+1} (and issues the TMA refills), so
+// the eight interior warps carry equal work per row (with XW = 0 the two warps holding the halo
+// sites ran 5 site passes per row against 4, and ncu showed 25% of warp time stalled on the
+// per-row barrier).
+template <int XW>
+struct Threads2 {
+    static constexpr int N = kThreads2 + 32 * XW;
+};
+
+template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB, int XW = 0>
+__global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     kpm_step2_tma_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
                          const __grid_constant__ CUtensorMap mapA2,   // a_n 2-site box {2TL, 2, 1}
                          const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(kThreads2, MINB)
     auto flush = [&](int lgf) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            sred[t] = acc[k];
+            if (t < CONS) sred[t] = acc[k];
             __syncthreads();
             if (t < TL) {
                 double2 s = make_double2(0.0, 0.0);
@@ -236,8 +245,9 @@ __global__ void __launch_bounds__(kThreads2, MINB)
     // refills -> thread PRODUCER (a warp without halo work).
     constexpr int NPI = TX / KSTEP;
     static_assert(TX % KSTEP == 0 && KSTEP >= 4, "interior sites must fill whole passes");
-    constexpr int PRODUCER = 32;  // thread 0 of warp 1
-    const int hs = k0 - (KSTEP - 2);             // 0, 1: halo site of this thread, else < 0
+    constexpr int PRODUCER = XW ? CONS : 32;  // the halo warp's first thread, else thread 0 of warp 1
+    const bool halo_warp = XW && t >= CONS;
+    const int hs = XW ? -1 : k0 - (KSTEP - 2);   // 0, 1: halo site of this thread, else < 0
     const int hlx = hs == 0 ? -1 : TX;           // its tile x index
     LoadCursor cs;  // segment iterator of the consumers (same sequence)
     cs.init(g, w_begin, w_end, 0);
@@ -287,6 +297,7 @@ __global__ void __launch_bounds__(kThreads2, MINB)
             double2* outC = g.outC + rC * growstep + g0;
 #pragma unroll
             for (int p = 0; p < NPI; ++p) {
+                if (halo_warp) break;
                 const int lx = k0 + p * KSTEP;       // interior site
                 const int oa = (lx + 2) * SITE + lo;  // a_n slot index
                 const int ob = (lx + 1) * SITE + lo;  // a_{n+1} / a_{n-1} slot index
@@ -332,6 +343,18 @@ __global__ void __launch_bounds__(kThreads2, MINB)
                 const double2 b = step_val(ld(A1 + oa), ld(A1 + oa - SITE), ld(A1 + oa + SITE), ld(A0 + oa), ld(A2 + oa), e1,
                                            ph, ld(Pq + ob));
                 *reinterpret_cast<double2*>(Bq + ob) = b;
+            }
+            if (halo_warp) {  // the two halo sites x0-1, x0+TX of a_{n+1}, all lanes
+                for (int j = t - CONS; j < 2 * TL; j += 32) {
+                    const int hx = j < TL ? -1 : TX, hl = j % TL;
+                    const int oa = (hx + 2) * SITE + hl * 16;
+                    const int ob = (hx + 1) * SITE + hl * 16;
+                    const double2 ph = PEIERLS ? sphase[hx + 1] : make_double2(0.0, 0.0);
+                    const double e1 = ONSITE ? SL.eps(A1, hx, TX) : g.shift;
+                    const double2 b = step_val(ld(A1 + oa), ld(A1 + oa - SITE), ld(A1 + oa + SITE), ld(A0 + oa),
+                                               ld(A2 + oa), e1, ph, ld(Pq + ob));
+                    *reinterpret_cast<double2*>(Bq + ob) = b;
+                }
             }
             __syncthreads();  // row q done: slots of a_n row r-1 and a_{n-1} row r are free
             if (t == PRODUCER) {

@@ -161,6 +161,9 @@ def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
     info = h.plan_info(N, R)
     assert info["two_step"] == (N // 2 - 1 >= 2 and lat["L"][0] % (1024 // info["TL"]) == 0)
     mu2 = h.moments(N, R, 5)
+    for xw in ("0", "1"):  # with and without the halo warp
+        monkeypatch.setenv("KPM_TMA2_XW", xw)
+        assert normwise(h.moments(N, R, 5), ref) < TOL
     monkeypatch.setenv("KPM_NO_TMA2", "1")
     assert h.plan_info(N, R)["two_step"] == 0
     mu1 = h.moments(N, R, 5)
