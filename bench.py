@@ -186,7 +186,9 @@ def config_obj(args, cfg, lat, world):
             "vector_seed": cfg["seed"], "disorder_seed": cfg["disorder_seed"],
             "parallelism": f"rows{world}" if rows else f"vectors{world}",
             "H_format": getattr(args, "format", "stencil"),
-            "l2": "inputs larger than L2 (2 x D*R*s vector blocks)"}
+            "l2": ("inputs larger than L2 (2 x D*R*s vector blocks)"
+                   if 2 * lat["D"] * cfg["R"] * (16 if lat["flux"] else 8) > 126e6
+                   else "L2-resident vector blocks (2 x D*R*s < 126 MB L2): not an HBM number")}
 
 
 def main():
@@ -211,6 +213,9 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="process-group backend for N > 1 (gloo: all-reduce through host memory; lets several "
                          "ranks share one GPU to test the multi-rank path)")
+    ap.add_argument("--r-per-gpu", type=int, default=None,
+                    help="override the config's vectors per GPU (e.g. c2 with R=8: one GPU's share of c2 "
+                         "at 8 GPUs under strong scaling, whose vector blocks stay in L2)")
     ap.add_argument("--partition", default="vectors", choices=["vectors", "rows"],
                     help="vectors: each rank owns R vectors of its own (weak scaling, one all-reduce); rows: "
                          "the lattice is cut into slabs of the slowest dimension with halo exchange over NCCL "
@@ -221,6 +226,8 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = ki.CONFIGS[args.config]
+    if args.r_per_gpu:
+        cfg = dict(cfg, R=args.r_per_gpu)
     lat = ki.lattice(cfg)
     if args.format is None:
         args.format = cfg.get("format", "stencil")

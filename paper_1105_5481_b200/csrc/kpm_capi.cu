@@ -26,6 +26,7 @@
 #include "kpm_tmak.cuh"
 #include "kpm_tma3.cuh"
 #include "kpm_tma32.cuh"
+#include "kpm_persist.cuh"
 #include "kpm_ell.cuh"
 #include "kpm_small.cuh"
 #include "kpm_dense.cuh"
@@ -111,6 +112,7 @@ struct kpm_handle_s {
     bool ws_own = true;
     // device facts
     int num_sms = 148;
+    int l2_bytes = 0;
     // timing of the last call
     cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
     // row partition, overlapped halo exchange: a second stream and two events (created on demand)
@@ -149,6 +151,8 @@ struct Plan {
     bool use_tmak = false;
     int KSK = 0, TLK = 0, TXK = 0, tmak_grid = 0;
     size_t tmak_smem = 0;
+    // whole recursion in one cooperative launch with the vector blocks L2-resident (kpm_persist.cuh)
+    bool use_persist = false;
     // whole recursion in one launch with the vector blocks in shared memory (kpm_small.cuh)
     bool use_small = false;
     size_t small_smem = 0;
@@ -381,6 +385,19 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
                              : p->xpad ? (size_t)(h->plane / h->L[0]) * (h->L[0] + 2 * p->xpad) : (size_t)h->plane;
     p->ghost_lanes = plane_mem * p->RG;
     p->lane_bytes = (p->mem_sites * p->RG + 2 * p->ghost_lanes) * sizeof(double2);
+    // Persistent L2-resident mode (opt-in, KPM_PERSIST=1): the whole recursion in one cooperative
+    // launch, one 512-thread CTA per SM per lane-group row of the grid.  Measured on c2 with R = 8
+    // (2 x 16.8 MB, L2-resident): 7.85 ms vs 7.42 ms for the per-step launches -- the launch gaps
+    // it removes are smaller than what the grid barrier costs.
+    p->use_persist = false;
+    if (!p->use_small && h->kind != KIND_DENSE && !h->rows && !(flags & KPM_DIRECT) && p->M >= 2 &&
+        !env_on("KPM_NO_PERSIST") && p->gy <= h->num_sms && env_on("KPM_PERSIST")) {
+        p->use_persist = true;
+        p->use_tma = p->use_tma2 = p->use_tma32 = p->use_tmak = p->use_tma3 = false;
+        p->overlap = false;
+        const long long site_ctas = (h->D + p->TS - 1) / p->TS;
+        p->gx = (int)std::max<long long>(1, std::min<long long>(site_ctas, h->num_sms / p->gy));
+    }
     size_t off = 0;
     p->off_P = off; off = align_up(off + p->lane_bytes);
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
@@ -513,6 +530,30 @@ kpm_status launch_small(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, i
     }
 }
 
+template <class OP, bool CPLX>
+kpm_status launch_persist_t(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int first_buf, int N,
+                            long long slot, double* part) {
+    auto kern = kpm::kpm_persist_kernel<OP, CPLX>;
+    dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
+    const size_t smem = 3 * (size_t)kThreads * sizeof(double2);
+    int per_sm = 0;
+    KPM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, p.TR * p.TS, smem));
+    if ((long long)per_sm * h->num_sms < (long long)p.gx * p.gy)
+        return fail(KPM_ERR_UNSUPPORTED, "persistent kernel: %d x %d CTAs not co-resident (%d per SM)", p.gx, p.gy, per_sm);
+    kpm::VecArgs va = v;
+    int M = p.M;
+    void* args[] = {(void*)&op, (void*)&va, (void*)&N, (void*)&M, (void*)&first_buf, (void*)&slot, (void*)&part};
+    KPM_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, block, args, smem, h->stream));
+    h->total_launches++;
+    return KPM_OK;
+}
+
+template <bool CPLX, class OP>
+kpm_status launch_persist_op(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int first_buf, int N,
+                             long long slot, double* part) {
+    return launch_persist_t<OP, CPLX>(h, p, op, v, first_buf, N, slot, part);
+}
+
 // Dispatch on the operator type of the handle.
 kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& v, int tail) {
     using namespace kpm;
@@ -535,6 +576,32 @@ kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& 
         case 5: return launch_mode<false>(h, p, StencilOp<2, true, false>{g}, mode, v, tail);
         case 6: return launch_mode<false>(h, p, StencilOp<3, false, false>{g}, mode, v, tail);
         default: return launch_mode<false>(h, p, StencilOp<3, true, false>{g}, mode, v, tail);
+    }
+}
+
+kpm_status launch_persist(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int first_buf, int N, long long slot,
+                          double* part) {
+    using namespace kpm;
+    if (h->kind == KIND_ELL) {
+        if (is_cplx(h))
+            return launch_persist_op<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, v, first_buf, N,
+                                           slot, part);
+        return launch_persist_op<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, v, first_buf,
+                                        N, slot, part);
+    }
+    const StencilGeom g = stencil_geom(h);
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_persist_op<true>(h, p, StencilOp<2, true, true>{g}, v, first_buf, N, slot, part);
+        return launch_persist_op<true>(h, p, StencilOp<2, false, true>{g}, v, first_buf, N, slot, part);
+    }
+    switch (h->ndim * 2 + (on ? 1 : 0)) {
+        case 2: return launch_persist_op<false>(h, p, StencilOp<1, false, false>{g}, v, first_buf, N, slot, part);
+        case 3: return launch_persist_op<false>(h, p, StencilOp<1, true, false>{g}, v, first_buf, N, slot, part);
+        case 4: return launch_persist_op<false>(h, p, StencilOp<2, false, false>{g}, v, first_buf, N, slot, part);
+        case 5: return launch_persist_op<false>(h, p, StencilOp<2, true, false>{g}, v, first_buf, N, slot, part);
+        case 6: return launch_persist_op<false>(h, p, StencilOp<3, false, false>{g}, v, first_buf, N, slot, part);
+        default: return launch_persist_op<false>(h, p, StencilOp<3, true, false>{g}, v, first_buf, N, slot, part);
     }
 }
 
@@ -854,6 +921,7 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
     if (dist) h->dist = *dist;
     h->dist.nccl_id = nullptr;  // not kept
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
+    cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, device);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t keep = UINT64_MAX;  // keep freed workspace in the pool for the next handle
@@ -1023,6 +1091,18 @@ struct Run {
         }
         if (first_mode == kpm::FIRST_BUF && h->rows) KPM_TRY(need_exchange(P));
         if (h->kind == KIND_DENSE) return begin_dense(first_mode);
+        if (p.use_persist) {  // the whole recursion in one cooperative launch (kpm_persist.cuh)
+            KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
+            KPM_TRY(launch_persist(h, p, v, first_mode == kpm::FIRST_BUF, N, (long long)slot, part));
+            h->step_launches = 1;
+            const double s_el = cplx ? 16.0 : 8.0;
+            const double vb = (double)h->D * (double)p.R_loc * s_el;
+            const double mb = h->kind == KIND_ELL ? (double)h->K * (double)h->D * (4.0 + s_el) : 0.0;
+            h->steps_bytes = 2.0 * vb + (p.M - 1) * (3.0 * vb + (h->d_eps ? 8.0 * (double)h->D : 0.0) + mb);
+            nsteps = 0;
+            n = 1;
+            return KPM_OK;
+        }
         if (p.use_small) {  // the whole recursion in one launch (kpm_small.cuh)
             KPM_CUDA(cudaEventRecord(h->ev_begin, h->stream));
             KPM_TRY(launch_small(h, p, v, first_mode == kpm::FIRST_BUF, N, part));
@@ -2210,6 +2290,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;
     info[11] = p.use_tmak ? p.KSK : 0;
+    if (p.use_persist) info[7] |= 32;
     return KPM_OK;
 }
 

@@ -211,8 +211,16 @@ __device__ __forceinline__ double2 gen_lane(const VecArgs& v, int j, int rg) {
 // window of the lattice and the neighbour planes they re-read stay in L2; the
 // a_{n-1} read and a_{n+1} write are cache-streaming (evict-first) so they do not
 // displace those planes.
-template <class OP, int MODE, bool CPLX>
-__global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArgs v, const int tail) {
+//
+// PERSIST (the L2-resident persistent kernel, kpm_persist.cuh): vector blocks change during the
+// kernel, so they are read through L2 only (ld.global.cg) -- the non-coherent L1 path of __ldg
+// could return a value another SM overwrote in an earlier step.
+template <bool PERSIST>
+__device__ __forceinline__ double2 ld_vec(const double2* p) {
+    return PERSIST ? __ldcg(p) : __ldg(p);
+}
+template <class OP, int MODE, bool CPLX, bool PERSIST = false>
+__device__ __forceinline__ void step_body(const OP& op, const VecArgs& v, const int tail) {
     const int TR = blockDim.x, TS = blockDim.y;
     const int rg = blockIdx.y * TR + threadIdx.x;
     const bool active = rg < v.RG;
@@ -231,7 +239,7 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
                 dot_acc<CPLX>(acc1, x, y);
                 if (tail) dot_acc<CPLX>(acc2, y, y);
             } else if (MODE == FIRST_BUF) {
-                auto X = [&](int j) { return __ldg(v.P + (size_t)v.mem(j) * v.RG + rg); };
+                auto X = [&](int j) { return ld_vec<PERSIST>(v.P + (size_t)v.mem(j) * v.RG + rg); };
                 const double2 x = X(s);
                 const double2 y = op.apply(s, X, x);
                 store_site(v, v.C, s, ms, rg, y, false);
@@ -239,12 +247,12 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
                 dot_acc<CPLX>(acc1, x, y);
                 if (tail) dot_acc<CPLX>(acc2, y, y);
             } else {
-                auto X = [&](int j) { return __ldg(v.C + (size_t)v.mem(j) * v.RG + rg); };
+                auto X = [&](int j) { return ld_vec<PERSIST>(v.C + (size_t)v.mem(j) * v.RG + rg); };
                 const double2 x = X(s);
                 const double2 h = op.apply(s, X, x);
-                const double2 p = __ldcs(v.P + idx);
+                const double2 p = PERSIST ? __ldcg(v.P + idx) : __ldcs(v.P + idx);
                 const double2 y = make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));  // Eq 18
-                store_site(v, v.P, s, ms, rg, y, true);
+                store_site(v, v.P, s, ms, rg, y, !PERSIST);
                 if (MODE == STEP) {
                     dot_acc<CPLX>(acc0, x, x);
                     dot_acc<CPLX>(acc1, x, y);
@@ -281,6 +289,11 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
             }
         }
     }
+}
+
+template <class OP, int MODE, bool CPLX>
+__global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArgs v, const int tail) {
+    step_body<OP, MODE, CPLX>(op, v, tail);
 }
 
 // ------------------------------------------------------------ helpers

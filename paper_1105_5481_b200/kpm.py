@@ -259,6 +259,7 @@ class Handle:
         d["overlap"] = int((info[7] >> 2) & 1)
         d["box3"] = int((info[7] >> 3) & 1)  # 3D dense-box march kernel (kpm_tma3.cuh)
         d["two_step3d"] = int((info[7] >> 4) & 1)  # 3D two-step kernel (kpm_tma32.cuh)
+        d["persist"] = int((info[7] >> 5) & 1)  # whole recursion in one cooperative launch (kpm_persist.cuh)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
         return d
 

@@ -405,6 +405,34 @@ def test_row_partition_local_group_matches_oracle(kpm, case, world):
     assert normwise(mu, ref) < TOL
 
 
+PERSIST_CASES = dict(**{k: v for k, v in CASES.items()}, **{"tma_" + k: v for k, v in TMA_CASES.items()})
+
+
+@pytest.mark.parametrize("form", ["stencil", "csr"])
+@pytest.mark.parametrize("case", sorted(PERSIST_CASES))
+def test_persistent_kernel_matches_oracle(kpm, case, form, monkeypatch):
+    """The whole recursion in one cooperative launch with grid-wide barriers between steps
+    (kpm_persist.cuh, L2-resident blocks): same moments as the oracle, per vector too, with
+    generated and caller-supplied start vectors, deterministic."""
+    monkeypatch.delenv("KPM_NO_PERSIST", raising=False)
+    monkeypatch.setenv("KPM_PERSIST", "1")  # opt-in (any size that is co-resident)
+    monkeypatch.setenv("KPM_NO_SMALL", "1")
+    lat, N, R = PERSIST_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b -= 0.02 * a
+    a *= 1.04
+    r = ki.rademacher(12, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b, form)
+    assert h.plan_info(N, R)["persist"] == int(N // 2 >= 2), h.plan_info(N, R)
+    mu = h.moments(N, R, 12)
+    assert normwise(mu, ref) < TOL
+    assert normwise(h.moments_ex(N, R, 12, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
+    assert np.array_equal(h.moments_ex(N, R, 12, r0=r), mu)
+    assert np.array_equal(h.moments(N, R, 12), mu), "not deterministic"
+
+
 def random_sparse_hermitian(D, deg, seed, cplx):
     """Irregular sparse Hermitian H (random graph, long-range bonds, ragged row lengths)."""
     rng = np.random.default_rng(seed)
