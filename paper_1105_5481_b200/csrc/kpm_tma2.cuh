@@ -80,9 +80,15 @@ __host__ __device__ inline size_t step2_smem_bytes(int TX, int TL, bool onsite, 
 
 // Walks one CTA's segments (lane group, pencil, rows [m0, m0+H)) and, within a segment,
 // its loads q = 0 .. H+extra-1: a_n rows m0-2+q (extra 4) or a_{n-1} rows m0-1+q (extra 2).
+// Per segment it also precomputes what every load of the segment needs -- the wrapped row of
+// load q (advanced with one compare per load), the tile's x0, its periodic halo columns x0-hw
+// and x0+TX (hw = extra/2 sites) and the lane coordinate c0 -- so that a refill costs no integer
+// division (ncu: the producer's divisions and modulos kept its warp ~250 instructions per row
+// behind the others, and every warp waited for it at the next row barrier).
 struct LoadCursor {
     long long w, w_end;
     int lg, px, m0, H, q, nq;
+    int row, x0, xl, xr, c0;
     bool valid;
     template <class G>
     __device__ void seg(const G& g, int extra) {
@@ -97,6 +103,15 @@ struct LoadCursor {
         w = e;
         q = 0;
         nq = H + extra;
+        const int hw = extra / 2;
+        row = m0 - hw;
+        while (row < 0) row += g.L1;
+        x0 = px * g.TX;
+        xl = x0 - hw;
+        while (xl < 0) xl += g.L0;
+        xr = x0 + g.TX;
+        while (xr >= g.L0) xr -= g.L0;
+        c0 = 2 * lg * g.TL;
     }
     template <class G>
     __device__ void init(const G& g, long long b, long long e, int extra) {
@@ -106,6 +121,7 @@ struct LoadCursor {
     }
     template <class G>
     __device__ void next(const G& g, int extra) {
+        if (++row == g.L1) row = 0;
         if (++q >= nq) seg(g, extra);
     }
 };
@@ -154,9 +170,7 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     LoadCursor& cp = cur_smem[1];
     auto issueA = [&](int slot) {  // next a_n row of the sequence into `slot`
         if (!ca.valid) return;
-        const int row = (ca.m0 - 2 + ca.q + 2 * g.L1) % g.L1;
-        const int c0 = 2 * ca.lg * TL, x0 = ca.px * TX;
-        const int xl2 = (x0 - 2 + g.L0) % g.L0, xr2 = (x0 + TX) % g.L0;
+        const int row = ca.row, c0 = ca.c0, x0 = ca.x0, xl2 = ca.xl, xr2 = ca.xr;
         unsigned char* dst = ringA + slot * SL.a_bytes;
         mbar_expect_tx(fullA + slot, (TX + 4) * SITE + (ONSITE ? (TX + 4) * 8 : 0));
         tma_load(dst, &mapA2, fullA + slot, c0, xl2, row);
@@ -171,9 +185,7 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     };
     auto issueP = [&](int slot) {  // next a_{n-1} row of the sequence into `slot`
         if (!cp.valid) return;
-        const int row = (cp.m0 - 1 + cp.q + g.L1) % g.L1;
-        const int c0 = 2 * cp.lg * TL, x0 = cp.px * TX;
-        const int xl1 = (x0 - 1 + g.L0) % g.L0, xr1 = (x0 + TX) % g.L0;
+        const int row = cp.row, c0 = cp.c0, x0 = cp.x0, xl1 = cp.xl, xr1 = cp.xr;
         unsigned char* dst = ringP + slot * SL.p_bytes;
         mbar_expect_tx(fullP + slot, (TX + 2) * SITE);
         const uint64_t pol = pol_smem;
@@ -245,7 +257,9 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     // refills -> thread PRODUCER (a warp without halo work).
     constexpr int NPI = TX / KSTEP;
     static_assert(TX % KSTEP == 0 && KSTEP >= 4, "interior sites must fill whole passes");
+    // refills: a_n by PRODUCER, a_{n-1} by PRODUCER_P (two warps share the issue work)
     constexpr int PRODUCER = XW ? CONS : 32;  // the halo warp's first thread, else thread 0 of warp 1
+    constexpr int PRODUCER_P = XW ? CONS : 64;
     const bool halo_warp = XW && t >= CONS;
     const int hs = XW ? -1 : k0 - (KSTEP - 2);   // 0, 1: halo site of this thread, else < 0
     const int hlx = hs == 0 ? -1 : TX;           // its tile x index
@@ -360,6 +374,9 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
             if (t == PRODUCER) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issueA(s0);
+            }
+            if (t == PRODUCER_P) {
+                if (PRODUCER_P != PRODUCER) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issueP(ps);
             }
             ++ip;

@@ -88,6 +88,7 @@ struct Cursor32 {
     long long w, w_end;
     int col_step;
     int lg, px, py, m0, H, q, nq;
+    int z;  // wrapped plane of load q (m0 - extra/2 + q), advanced with one compare per load
     bool valid;
     __device__ void seg(const Tma32Geom& g, int extra) {
         valid = w < w_end;
@@ -117,6 +118,8 @@ struct Cursor32 {
         py = pencil / g.PX;
         q = 0;
         nq = H + extra;
+        z = m0 - extra / 2;
+        while (z < 0) z += g.L2;
     }
     __device__ void init(const Tma32Geom& g, int extra) {
         if (g.rr) {
@@ -131,6 +134,7 @@ struct Cursor32 {
         seg(g, extra);
     }
     __device__ void next(const Tma32Geom& g, int extra) {
+        if (++z == g.L2) z = 0;
         if (++q >= nq) seg(g, extra);
     }
 };
@@ -166,7 +170,7 @@ __global__ void __launch_bounds__(NT, 1)
     const int L0f = g.L0 + 2 * XP;  // frame row pitch (sites)
     auto issueA = [&](int slot) {   // next a_n plane (m0-2+q) of the sequence
         if (!ca.valid) return;
-        const int z = (ca.m0 - 2 + ca.q + 2 * g.L2) % g.L2;
+        const int z = ca.z;
         const int c0 = 2 * ca.lg * TL, x0 = ca.px * TX, y0 = ca.py * TY;
         const int yt = (y0 - 2 + g.L1) % g.L1, yb = (y0 + TY) % g.L1;
         unsigned char* dst = ringA + slot * Y::A_SLOT;
@@ -185,7 +189,7 @@ __global__ void __launch_bounds__(NT, 1)
     };
     auto issueP = [&](int slot) {  // next a_{n-1} plane (m0-1+q) of the sequence
         if (!cp.valid) return;
-        const int z = (cp.m0 - 1 + cp.q + g.L2) % g.L2;
+        const int z = cp.z;
         const int c0 = 2 * cp.lg * TL, x0 = cp.px * TX, y0 = cp.py * TY;
         const int yt = (y0 - 1 + g.L1) % g.L1, yb = (y0 + TY) % g.L1;
         unsigned char* dst = ringP + slot * Y::B_SLOT;
