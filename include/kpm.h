@@ -280,6 +280,12 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
  * info[10] = two-step grid; info[11] = 0. */
 kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[12]);
 
+/* Counters of the last kpm_moments_ex / kpm_moments_group call on this handle: stats[0] =
+ * recursion-step launches, stats[1] = all kernel launches, stats[2] = halo plane copies (row
+ * partition, copy exchange), stats[3] = recursion launches that stored their boundary planes
+ * straight into the neighbours' ghost planes (fused halo, in-process slab groups). */
+kpm_status kpm_last_stats(kpm_handle h, int64_t stats[4]);
+
 /* Algorithmic HBM bytes moved by the recursion-step launches of the last kpm_moments_ex
  * call: 3 D R s per single step (read a_n, read a_{n-1}, write
  * a_{n+1}), 4 D R s per two-step launch, plus 8 D per launch for an on-site array and

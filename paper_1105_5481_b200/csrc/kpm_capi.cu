@@ -119,6 +119,7 @@ struct kpm_handle_s {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
     int step_launches = 0, total_launches = 0;
+    int halo_copies = 0, fused_halo_launches = 0;  // row partition: plane copies / launches storing into peers
     double steps_bytes = 0.0;  // algorithmic HBM bytes of the recursion-step launches of the last call
 };
 
@@ -1054,6 +1055,8 @@ struct Run {
         slot = (size_t)p.gx * p.RP;  // doubles per moment slot of partials
         h->total_launches = 0;
         h->step_launches = 0;
+        h->halo_copies = 0;
+        h->fused_halo_launches = 0;
         h->steps_bytes = 0.0;
 
         v.P = P;
@@ -1165,6 +1168,9 @@ struct Run {
             tg.rows_total = p.gx;
             tg.row_off = 0;
             tg.zoff = 0;
+            tg.peer_lo = tg.peer_hi = nullptr;  // fused halo: set per launch by kpm_moments_group
+            tg.plane_lanes = (long long)p.ghost_lanes;
+            tg.nloc = (int)h->nloc;
             tg.xpad = p.xpad;
             tg.t = h->t_scaled;
             tg.shift = -h->b / h->a;
@@ -1603,6 +1609,7 @@ kpm_status exchange_group(std::vector<Run>& runs, std::vector<cudaEvent_t>& evs)
                                      r.h->stream));
         KPM_CUDA(cudaMemcpyPeerAsync(r.ghost_hi(X), r.h->device, rh.first_plane(rh.pending), rh.h->device, r.plane_bytes(),
                                      r.h->stream));
+        r.h->halo_copies += 2;
     }
     return KPM_OK;
 }
@@ -2117,13 +2124,41 @@ kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, u
         for (auto& r : runs) r.pending = r.fresh();
         return exchange_group(runs, evs);
     };
-    if (st == KPM_OK) st = exch();
+    if (st == KPM_OK) st = exch();  // ghosts of a_1 (first-step kernel): plane copies
+    // Fused halo (stencil slabs on one device, TMA march kernels): every recursion launch stores its
+    // boundary planes straight into the neighbours' ghost planes of the same block (peer memory),
+    // so between launches only stream ordering remains -- each rank's next launch waits for its two
+    // neighbours' current one (their ghost writes into it, and their reads of the ghosts it
+    // overwrites next).  KPM_NO_FUSED_HALO=1 keeps the copy exchange.
+    bool fused = st == KPM_OK && !env_on("KPM_NO_FUSED_HALO");
+    for (int i = 0; i < nh && fused; ++i)
+        fused = hs[i]->kind == KIND_STENCIL && runs[i].p.use_tma && !runs[i].p.overlap && hs[i]->device == hs[0]->device;
     while (st == KPM_OK && runs[0].more()) {
-        for (int i = 0; i < nh && st == KPM_OK; ++i) st = runs[i].launch_next();
-        if (st == KPM_OK) st = exch();
+        for (int i = 0; i < nh && fused; ++i) {
+            Run& lo = runs[(i - 1 + nh) % nh];
+            Run& hi = runs[(i + 1) % nh];
+            runs[i].tg.peer_lo = lo.ghost_hi(lo.prev);
+            runs[i].tg.peer_hi = hi.ghost_lo(hi.prev);
+        }
+        for (int i = 0; i < nh && st == KPM_OK; ++i) {
+            st = runs[i].launch_next();
+            if (fused) hs[i]->fused_halo_launches++;
+        }
+        if (st != KPM_OK) break;
+        if (!fused) {
+            st = exch();
+            continue;
+        }
+        for (int i = 0; i < nh && st == KPM_OK; ++i)
+            if (cudaEventRecord(evs[i], hs[i]->stream) != cudaSuccess) st = fail(KPM_ERR_CUDA, "event record");
+        for (int i = 0; i < nh && st == KPM_OK; ++i)
+            if (cudaStreamWaitEvent(hs[i]->stream, evs[(i - 1 + nh) % nh], 0) != cudaSuccess ||
+                cudaStreamWaitEvent(hs[i]->stream, evs[(i + 1) % nh], 0) != cudaSuccess)
+                st = fail(KPM_ERR_CUDA, "event wait");
     }
     std::vector<double> Ssum(N, 0.0), Si(N);
     for (int i = 0; i < nh && st == KPM_OK; ++i) {
+        runs[i].tg.peer_lo = runs[i].tg.peer_hi = nullptr;
         st = runs[i].collect();
         if (st != KPM_OK) break;
         cudaSetDevice(hs[i]->device);
@@ -2270,6 +2305,15 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
     }
     if (step_launches) *step_launches = h->step_launches;
     if (total_launches) *total_launches = h->total_launches;
+    return KPM_OK;
+}
+
+kpm_status kpm_last_stats(kpm_handle h, int64_t stats[4]) {
+    if (!h || !stats) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
+    stats[0] = h->step_launches;
+    stats[1] = h->total_launches;
+    stats[2] = h->halo_copies;
+    stats[3] = h->fused_halo_launches;
     return KPM_OK;
 }
 

@@ -124,7 +124,23 @@ struct TmaGeom {
     double* red1;
     double* red2;     // odd-N tail, nullable
     double2* out;     // a_{n-1} in place -> a_{n+1} (global, lane layout)
+    // Row partition, fused halo (in-process slab handles, kpm_moments_group): the step kernel
+    // itself stores its first / last local plane of a_{n+1} into the lower / upper neighbour's
+    // ghost plane of the same block (peer memory; nullptr = exchanged separately).  plane_lanes:
+    // lanes of one buffer plane; nloc: local planes (the last one is buffer plane nloc).
+    double2* peer_lo;
+    double2* peer_hi;
+    long long plane_lanes;
+    int nloc;
 };
+
+// a_{n+1} value y stored at `o` of buffer plane m: its copies in the neighbours' ghost planes
+__device__ __forceinline__ void store_peers(const TmaGeom& g, int m, const double2* o, double2 y) {
+    if (g.peer_lo == nullptr) return;
+    const long long inpl = o - (g.out + (long long)m * g.plane_lanes);
+    if (m == 1) __stcs(g.peer_lo + inpl, y);
+    if (m == g.nloc) __stcs(g.peer_hi + inpl, y);
+}
 
 constexpr int kTmaConsumerWarps = 8;
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
@@ -375,9 +391,16 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                                                      : ((long long)m * g.L1 + (y0 + ly)) * (g.L0 + 2 * g.xpad) + xs + g.xpad;
                     double2* o = g.out + site * g.RG + s.lg * g.TL + l;
                     __stcs(o, y);
+                    store_peers(g, m, o, y);
                     if (NDIM == 3 && g.xpad) {  // periodic x images in the frame
-                        if (xs < g.xpad) __stcs(o + (long long)g.L0 * g.RG, y);
-                        if (xs >= g.L0 - g.xpad) __stcs(o - (long long)g.L0 * g.RG, y);
+                        if (xs < g.xpad) {
+                            __stcs(o + (long long)g.L0 * g.RG, y);
+                            store_peers(g, m, o + (long long)g.L0 * g.RG, y);
+                        }
+                        if (xs >= g.L0 - g.xpad) {
+                            __stcs(o - (long long)g.L0 * g.RG, y);
+                            store_peers(g, m, o - (long long)g.L0 * g.RG, y);
+                        }
                     }
                     dot_acc<PEIERLS>(acc0, x, x);
                     dot_acc<PEIERLS>(acc1, x, y);

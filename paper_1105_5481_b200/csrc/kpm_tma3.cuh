@@ -190,6 +190,12 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     __stcs(out, y);
                     if (img_lo) __stcs(out + (long long)g.L0 * g.RG, y);   // periodic x images in the frame
                     if (img_hi) __stcs(out - (long long)g.L0 * g.RG, y);
+                    if (g.peer_lo) {  // fused halo: the neighbours' ghost planes (row partition)
+                        const int mb = g.zoff + s.m0 + j + g.ghost;
+                        store_peers(g, mb, out, y);
+                        if (img_lo) store_peers(g, mb, out + (long long)g.L0 * g.RG, y);
+                        if (img_hi) store_peers(g, mb, out - (long long)g.L0 * g.RG, y);
+                    }
                     dot_acc<false>(acc0, x, x);
                     dot_acc<false>(acc1, x, y);
                     if (tail) dot_acc<false>(acc2, y, y);

@@ -36,7 +36,7 @@ EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershg
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
            "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moments_local", "kpm_create_dense",
-           "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_destroy",
+           "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_last_stats", "kpm_destroy",
            "kpm_last_error", "kpm_version"]
 
 
@@ -57,6 +57,7 @@ _SIG = {
     "kpm_create_csr": [_i64, _P, _P, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
     "kpm_create_ell": [_i64, _i32, _P, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
     "kpm_csr_partition": [_i64, _P, _P, _i32, _i32, _P, _P, _P, _P],
+    "kpm_last_stats": [_P, _P],
     "kpm_gershgorin_stencil": [ctypes.POINTER(kpm_stencil_desc), _f64, _P, _P],
     "kpm_gershgorin_csr": [_i64, _P, _P, _P, _i32, _f64, _P, _P],
     "kpm_set_stream": [_P, _P],
@@ -262,6 +263,12 @@ class Handle:
         d["persist"] = int((info[7] >> 5) & 1)  # whole recursion in one cooperative launch (kpm_persist.cuh)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
         return d
+
+    def last_stats(self):
+        """step launches, all launches, halo plane copies, fused-halo launches of the last call"""
+        st = np.zeros(4, dtype=np.int64)
+        _check(_lib.kpm_last_stats(self._h, _ptr(st)))
+        return dict(step_launches=int(st[0]), launches=int(st[1]), halo_copies=int(st[2]), fused_halo=int(st[3]))
 
     def step_bytes(self):
         """Algorithmic HBM bytes of the recursion-step launches of the last call."""

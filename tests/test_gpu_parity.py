@@ -390,11 +390,15 @@ def test_row_partition_world1_matches_oracle(kpm, case, comm, monkeypatch):
         assert normwise(h.moments(N, R, 8), mu) < 1e-13
 
 
-@pytest.mark.parametrize("world", [2, 3, 4])
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("case", ["1d", "2d_tma", "2d_peierls_tma", "3d_simple", "3d_tma"])
-def test_row_partition_local_group_matches_oracle(kpm, case, world):
+def test_row_partition_local_group_matches_oracle(kpm, case, world, fused, monkeypatch):
     """KPM_COMM_LOCAL: `world` slab handles in one process (one GPU) exchange halo planes
-    after every step; uneven slabs included.  Same global vectors as one whole lattice."""
+    after every step; uneven slabs included.  Same global vectors as one whole lattice.
+    fused = 1: the TMA march kernels store their boundary planes straight into the neighbours'
+    ghost planes (peer memory, no copy step); fused = 0: plane copies between launches."""
+    monkeypatch.setenv("KPM_NO_FUSED_HALO", "0" if fused == "1" else "1")
     lat, N, R = ROW_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -403,6 +407,11 @@ def test_row_partition_local_group_matches_oracle(kpm, case, world):
                                  dist=(kpm.KPM_PART_ROWS, rk, world, kpm.KPM_COMM_LOCAL)) for rk in range(world)]
     mu = kpm.kpm_moments_group(hs, N, R, 8)
     assert normwise(mu, ref) < TOL
+    st = hs[0].last_stats()
+    tma = hs[0].plan_info(N, R)["tma"] == 1
+    on = fused == "1" and tma  # the fused halo needs the TMA march kernels
+    assert st["fused_halo"] == (st["step_launches"] if on else 0), st
+    assert st["halo_copies"] == (2 if on else 2 * (st["step_launches"] + 1)), st  # + the first step's copies
 
 
 PERSIST_CASES = dict(**{k: v for k, v in CASES.items()}, **{"tma_" + k: v for k, v in TMA_CASES.items()})
