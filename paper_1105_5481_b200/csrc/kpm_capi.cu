@@ -2132,7 +2132,28 @@ kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, u
     // overwrites next).  KPM_NO_FUSED_HALO=1 keeps the copy exchange.
     bool fused = st == KPM_OK && !env_on("KPM_NO_FUSED_HALO");
     for (int i = 0; i < nh && fused; ++i)
-        fused = hs[i]->kind == KIND_STENCIL && runs[i].p.use_tma && !runs[i].p.overlap && hs[i]->device == hs[0]->device;
+        fused = hs[i]->kind == KIND_STENCIL && runs[i].p.use_tma && !runs[i].p.overlap;
+    // slabs on different GPUs: the kernels store into the neighbours' memory over NVLink, which
+    // needs peer access in both directions (else: plane copies, cudaMemcpyPeerAsync)
+    for (int i = 0; i < nh && fused; ++i) {
+        for (int d : {(i - 1 + nh) % nh, (i + 1) % nh}) {
+            const int a0 = hs[i]->device, a1 = hs[d]->device;
+            if (a0 == a1) continue;
+            int ok = 0;
+            if (cudaDeviceCanAccessPeer(&ok, a0, a1) != cudaSuccess || !ok) {
+                fused = false;
+                break;
+            }
+            cudaSetDevice(a0);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(a1, 0);
+            if (e == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+            else if (e != cudaSuccess) {
+                cudaGetLastError();
+                fused = false;
+                break;
+            }
+        }
+    }
     while (st == KPM_OK && runs[0].more()) {
         for (int i = 0; i < nh && fused; ++i) {
             Run& lo = runs[(i - 1 + nh) % nh];
@@ -2141,7 +2162,8 @@ kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, u
             runs[i].tg.peer_hi = hi.ghost_lo(hi.prev);
         }
         for (int i = 0; i < nh && st == KPM_OK; ++i) {
-            st = runs[i].launch_next();
+            if (cudaSetDevice(hs[i]->device) != cudaSuccess) st = fail(KPM_ERR_CUDA, "cudaSetDevice");
+            if (st == KPM_OK) st = runs[i].launch_next();
             if (fused) hs[i]->fused_halo_launches++;
         }
         if (st != KPM_OK) break;
@@ -2150,15 +2172,18 @@ kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, u
             continue;
         }
         for (int i = 0; i < nh && st == KPM_OK; ++i)
-            if (cudaEventRecord(evs[i], hs[i]->stream) != cudaSuccess) st = fail(KPM_ERR_CUDA, "event record");
+            if (cudaSetDevice(hs[i]->device) != cudaSuccess || cudaEventRecord(evs[i], hs[i]->stream) != cudaSuccess)
+                st = fail(KPM_ERR_CUDA, "event record");
         for (int i = 0; i < nh && st == KPM_OK; ++i)
-            if (cudaStreamWaitEvent(hs[i]->stream, evs[(i - 1 + nh) % nh], 0) != cudaSuccess ||
+            if (cudaSetDevice(hs[i]->device) != cudaSuccess ||
+                cudaStreamWaitEvent(hs[i]->stream, evs[(i - 1 + nh) % nh], 0) != cudaSuccess ||
                 cudaStreamWaitEvent(hs[i]->stream, evs[(i + 1) % nh], 0) != cudaSuccess)
                 st = fail(KPM_ERR_CUDA, "event wait");
     }
     std::vector<double> Ssum(N, 0.0), Si(N);
     for (int i = 0; i < nh && st == KPM_OK; ++i) {
         runs[i].tg.peer_lo = runs[i].tg.peer_hi = nullptr;
+        cudaSetDevice(hs[i]->device);
         st = runs[i].collect();
         if (st != KPM_OK) break;
         cudaSetDevice(hs[i]->device);
