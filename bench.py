@@ -427,6 +427,10 @@ def main():
                 "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Rademacher vectors, lattice H)",
                 "config": config_obj(args, cfg, lat, world),
                 "hbm_gbs_alg": steps_bytes / args.steps / (ms_per_step / 1000.0) / 1e9 * world,
+                # the metric counts D*N*R (two moments per product with doubling);
+                # the products actually performed are floor(N/2) per vector
+                "physical_updates_per_s": lat["D"] * (cfg["N"] // 2) * R
+                / (ms_per_step / 1000.0),
                 "roofline": roofline,
                 "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
                 "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
