@@ -126,6 +126,12 @@ typedef struct {
     int32_t comm;            /* KPM_COMM_* (row partition only) */
     const void* nccl_id;     /* KPM_COMM_NCCL: the 128-byte ncclUniqueId from kpm_nccl_unique_id on
                                 rank 0, the same on every rank */
+    int32_t vrank, vworld;   /* KPM_PART_ROWS only -- hybrid rows x vectors:
+                                with vworld > 1 this row group runs only the global vectors
+                                kpm_vector_range(R, vrank, vworld) (0 / 0 = all vectors).  The moment
+                                sums are combined inside the row group (rank/world, comm); across the
+                                vworld groups the caller sums the raw sums (KPM_RAW_SUMS, allowed for
+                                row partitions) and calls kpm_assemble with the global R. */
 } kpm_dist;
 
 /* 128-byte NCCL unique id for KPM_COMM_NCCL (call on rank 0, broadcast to the others). */

@@ -336,8 +336,10 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
                      bool no_fused = false) {
     if (N < 1) return fail(KPM_ERR_INVALID_ARG, "N must be >= 1 (got %d)", N);
     if (R < 1) return fail(KPM_ERR_INVALID_ARG, "R must be >= 1 (got %lld)", (long long)R);
-    const int world = h->dist.partition == KPM_PART_VECTORS ? h->dist.world : 1;  // vector shards
-    const int rank = h->dist.partition == KPM_PART_VECTORS ? h->dist.rank : 0;
+    // vector shards: the vector partition, or the vector groups of a hybrid row partition
+    const bool hybrid = h->dist.partition == KPM_PART_ROWS && h->dist.vworld > 1;
+    const int world = h->dist.partition == KPM_PART_VECTORS ? h->dist.world : (hybrid ? h->dist.vworld : 1);
+    const int rank = h->dist.partition == KPM_PART_VECTORS ? h->dist.rank : (hybrid ? h->dist.vrank : 0);
     p->N = N;
     p->M = N / 2;
     p->no_fused = no_fused;
@@ -911,6 +913,8 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
                 return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_SELF needs world == 1");
             if (dist->comm == KPM_COMM_NCCL && !dist->nccl_id)
                 return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_NCCL needs nccl_id");
+            if (dist->vworld > 1 && (dist->vrank < 0 || dist->vrank >= dist->vworld))
+                return fail(KPM_ERR_INVALID_ARG, "bad vector group %d of %d", dist->vrank, dist->vworld);
         }
     }
     int ndev = 0;
@@ -2082,8 +2086,6 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
     if (!out) return fail(KPM_ERR_INVALID_ARG, "NULL output");
     if (h->rows && h->dist.comm == KPM_COMM_LOCAL)
         return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL slab handles run through kpm_moments_group");
-    if (h->rows && h->dist.comm == KPM_COMM_NCCL && (flags & (KPM_RAW_SUMS | KPM_DEVICE_OUT)))
-        return fail(KPM_ERR_UNSUPPORTED, "row partition returns host moments (no raw sums / device output)");
     Run run;
     if (h->rows) run.exchange_hook = exchange_single;
     KPM_TRY(run.begin(h, N, R, seed, r0, flags));

@@ -47,7 +47,8 @@ class kpm_stencil_desc(ctypes.Structure):
 
 class kpm_dist(ctypes.Structure):
     _fields_ = [("partition", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
-                ("comm", ctypes.c_int32), ("nccl_id", ctypes.c_void_p)]
+                ("comm", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("vrank", ctypes.c_int32),
+                ("vworld", ctypes.c_int32)]
 
 
 _P, _i32, _i64, _u32, _u64, _f64, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
@@ -123,14 +124,17 @@ def _desc(ndim, L, t, onsite, flux):
 
 
 def _dist(dist):
-    """dist: None, (partition, rank, world) or (partition, rank, world, comm[, nccl_id bytes])."""
+    """dist: None, (partition, rank, world) or (partition, rank, world, comm[, nccl_id bytes[, vrank,
+    vworld]]) -- the last two: hybrid rows x vectors (row partitions only)."""
     if dist is None:
         return None, None
     part, rank, world = dist[:3]
     comm = dist[3] if len(dist) > 3 else KPM_COMM_SELF
     nid = dist[4] if len(dist) > 4 else None
     keep = ctypes.create_string_buffer(bytes(nid), 128) if nid is not None else None
-    st = kpm_dist(int(part), int(rank), int(world), int(comm), ctypes.cast(keep, ctypes.c_void_p) if keep else None)
+    vrank, vworld = (int(dist[5]), int(dist[6])) if len(dist) > 6 else (0, 0)
+    st = kpm_dist(int(part), int(rank), int(world), int(comm), ctypes.cast(keep, ctypes.c_void_p) if keep else None,
+                  vrank, vworld)
     return ctypes.byref(st), (st, keep)
 
 
@@ -192,9 +196,11 @@ class Handle:
         _check(_lib.kpm_set_workspace(self._h, ctypes.c_void_p(int(dev_ptr)) if dev_ptr else None, int(nbytes)))
 
     def r_local(self, R):
+        if self.dist is not None and self.dist[0] == KPM_PART_ROWS and len(self.dist) > 6 and self.dist[6] > 1:
+            return kpm_vector_range(R, self.dist[5], self.dist[6])  # hybrid rows x vectors
         if self.dist is None or self.dist[0] != KPM_PART_VECTORS:
             return 0, int(R)
-        _, rank, world = self.dist
+        _, rank, world = self.dist[:3]
         return kpm_vector_range(R, rank, world)
 
     def moments(self, N, R, seed):

@@ -504,6 +504,42 @@ def test_csr_row_partition_nccl_world1(kpm):
     assert normwise(h.moments_ex(N, R, 2, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
 
 
+@pytest.mark.parametrize("vworld", [2, 3])
+@pytest.mark.parametrize("case", ["2d_tma", "3d_tma", "3d_simple"])
+def test_hybrid_rows_x_vectors_matches_oracle(kpm, case, vworld):
+    """Hybrid decomposition: vworld vector groups, each a 2-slab row
+    partition (in-process group) over its share of the global vectors; the groups' moments
+    combine with weights R_g / R (the doubling transform is linear in the raw sums)."""
+    lat, N, R = ROW_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(8, R, lat["D"]), N)
+    mu = np.zeros(N)
+    for vg in range(vworld):
+        hs = [kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
+                                     dist=(kpm.KPM_PART_ROWS, rk, 2, kpm.KPM_COMM_LOCAL, None, vg, vworld))
+              for rk in range(2)]
+        _, Rg = hs[0].r_local(R)
+        assert Rg == kpm.kpm_vector_range(R, vg, vworld)[1]
+        mu += Rg / R * kpm.kpm_moments_group(hs, N, R, 8)
+    assert normwise(mu, ref) < TOL
+
+
+def test_hybrid_raw_sums_over_nccl_row_groups(kpm):
+    """Row partition over NCCL (world 1 per group) with KPM_RAW_SUMS: the vector groups' raw
+    sums add up to the whole estimate through kpm_assemble with the global R."""
+    lat, N, R = ROW_CASES["3d_tma"]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(8, R, lat["D"]), N)
+    S = np.zeros(N)
+    for vg in range(2):
+        h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
+                                   dist=(kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_NCCL, kpm.kpm_nccl_unique_id(), vg, 2))
+        S += h.moments_ex(N, R, 8, flags=kpm.KPM_RAW_SUMS)
+    assert normwise(h.assemble(S, N, R), ref) < TOL
+
+
 def test_randomized_shapes_sweep(kpm):
     """Random small lattices (1D/2D/3D, with/without disorder or flux), R, N and (a, b): all
     kernel paths (generic, TMA march, two-step) against the oracle."""
