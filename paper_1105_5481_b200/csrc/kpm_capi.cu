@@ -241,8 +241,10 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     int TL = 0;
     // 3D: 16 lanes (256 contiguous bytes per site) first -- c3 measured 1119 ms vs 1358 ms with 8 lanes
     // (DRAM locality of the TMA box rows; with the dense-box kernel, kpm_tma3.cuh)
-    const int cands2[3] = {32, 16, 8}, cands3[3] = {16, 32, 8};
-    for (int c : (h->ndim == 2 ? cands2 : cands3))
+    // 2D real: 16 lanes first -- c2 25.35 vs 26.13 ms per call with 32 (same box, A/B); 2D complex:
+    // 32 first -- c4 3114 vs 3166-3274 ms with 16
+    const int cands2r[3] = {16, 32, 8}, cands2c[3] = {32, 16, 8}, cands3[3] = {16, 32, 8};
+    for (int c : (h->ndim == 2 ? (is_cplx(h) ? cands2c : cands2r) : cands3))
         if (RG % c == 0) { TL = c; break; }
     const int tl_env = env_int("KPM_TMA_TL", 0);  // experiment: lanes per tile site
     if (tl_env && RG % tl_env == 0) TL = tl_env;

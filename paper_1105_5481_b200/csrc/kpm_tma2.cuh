@@ -257,9 +257,10 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     // refills -> thread PRODUCER (a warp without halo work).
     constexpr int NPI = TX / KSTEP;
     static_assert(TX % KSTEP == 0 && KSTEP >= 4, "interior sites must fill whole passes");
-    // refills: a_n by PRODUCER, a_{n-1} by PRODUCER_P (two warps share the issue work)
+    // refills: one thread issues both (measured: splitting a_n / a_{n-1} refills over two warps
+    // made c2 2% slower in sustained runs, 26.39 vs 25.85 ms, though one ncu launch was faster)
     constexpr int PRODUCER = XW ? CONS : 32;  // the halo warp's first thread, else thread 0 of warp 1
-    constexpr int PRODUCER_P = XW ? CONS : 64;
+    constexpr int PRODUCER_P = PRODUCER;
     const bool halo_warp = XW && t >= CONS;
     const int hs = XW ? -1 : k0 - (KSTEP - 2);   // 0, 1: halo site of this thread, else < 0
     const int hlx = hs == 0 ? -1 : TX;           // its tile x index
