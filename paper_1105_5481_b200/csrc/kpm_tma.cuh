@@ -144,8 +144,15 @@ __device__ __forceinline__ void store_peers(const TmaGeom& g, int m, const doubl
 
 constexpr int kTmaConsumerWarps = 8;
 constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
-constexpr int kSA = 5;  // a_n ring slots
-constexpr int kSP = 3;  // a_{n-1} ring slots
+#ifndef KPM_SA
+#define KPM_SA 5
+#endif
+// a_{n-1} ring depth 4: c3 1093 vs 1132 ms per call with 3 (same-box A/B; a_n ring 6: no change, 4: slower)
+#ifndef KPM_SP
+#define KPM_SP 4
+#endif
+constexpr int kSA = KPM_SA;  // a_n ring slots
+constexpr int kSP = KPM_SP;  // a_{n-1} ring slots
 
 // Shared-memory carve-up of one a_n slot: [main TY*TX][left TY][right TY][top TX][bottom TX][eps TX*TY doubles]
 struct SlotLayout {

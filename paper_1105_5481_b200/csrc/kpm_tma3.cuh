@@ -25,13 +25,14 @@ struct Slot3 {
     static constexpr int EPS = VEC;                        // eps~ [TY][TX] doubles after the box
     static constexpr int BYTES = (VEC + (ONSITE ? TX * TY * 8 : 0) + 127) / 128 * 128;
     static constexpr int TILE = TX * TY * SITE;            // a_{n-1} tile (no halo)
+    static constexpr int SP = TL >= 32 ? 3 : kSP;          // a_{n-1} ring (32-lane tiles: smem)
 };
 
 template <int TX, int TY, int TL, bool ONSITE>
 __host__ __device__ inline size_t step3_smem_bytes(int RP) {
     using S = Slot3<TX, TY, TL, ONSITE>;
-    return (size_t)kSA * S::BYTES + (size_t)kSP * S::TILE + 3 * (size_t)RP * 8 +
-           3 * (size_t)kTmaConsumerWarps * 32 * 16 + (2 * kSA + 2 * kSP) * 8;
+    return (size_t)kSA * S::BYTES + (size_t)S::SP * S::TILE + 3 * (size_t)RP * 8 +
+           3 * (size_t)kTmaConsumerWarps * 32 * 16 + (2 * kSA + 2 * S::SP) * 8;
 }
 
 template <int TX, int TY, int TL, bool ONSITE>
@@ -49,13 +50,13 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ringA = smem;
     unsigned char* ringP = ringA + kSA * S::BYTES;
-    double* sacc = reinterpret_cast<double*>(ringP + kSP * S::TILE);  // [3][RP]
+    double* sacc = reinterpret_cast<double*>(ringP + S::SP * S::TILE);  // [3][RP]
     double2* sred = reinterpret_cast<double2*>(sacc + 3 * g.RP);     // [3][CONS]
     uint64_t* bars = reinterpret_cast<uint64_t*>(sred + 3 * CONS);
     uint64_t* fullA = bars;
     uint64_t* emptyA = fullA + kSA;
     uint64_t* fullP = emptyA + kSA;
-    uint64_t* emptyP = fullP + kSP;
+    uint64_t* emptyP = fullP + S::SP;
 
     const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
     if (threadIdx.x == 0) {
@@ -63,7 +64,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             mbar_init(fullA + i, 1);
             mbar_init(emptyA + i, kTmaConsumerWarps);
         }
-        for (int i = 0; i < kSP; ++i) {
+        for (int i = 0; i < S::SP; ++i) {
             mbar_init(fullP + i, 1);
             mbar_init(emptyP + i, kTmaConsumerWarps);
         }
@@ -103,8 +104,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     ++ia;
                     if (q >= 1 && q - 1 < H) {
                         const int mp = g.zoff + s.m0 + q - 1 + g.ghost;
-                        const int ps = (int)(ip % kSP);
-                        if (ip >= kSP) mbar_wait(emptyP + ps, (uint32_t)(((ip / kSP) - 1) & 1));
+                        const int ps = (int)(ip % S::SP);
+                        if (ip >= S::SP) mbar_wait(emptyP + ps, (uint32_t)(((ip / S::SP) - 1) & 1));
                         mbar_expect_tx(fullP + ps, S::TILE);
                         tma_load_hint(ringP + ps * S::TILE, &mapP, fullP + ps, c0, x0 + g.xpad, y0, mp, pol_first);
                         ++ip;
@@ -163,8 +164,8 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     mbar_wait(fullA + (int)(i1 % kSA), (uint32_t)((i1 / kSA) & 1));
                 }
                 mbar_wait(fullA + (int)(i2 % kSA), (uint32_t)((i2 / kSA) & 1));
-                const int ps = (int)(ip % kSP);
-                mbar_wait(fullP + ps, (uint32_t)((ip / kSP) & 1));
+                const int ps = (int)(ip % S::SP);
+                mbar_wait(fullP + ps, (uint32_t)((ip / S::SP) & 1));
                 const unsigned char* S0 = ringA + (int)(i0 % kSA) * S::BYTES;  // plane m-1
                 const unsigned char* S1 = ringA + (int)(i1 % kSA) * S::BYTES;  // plane m
                 const unsigned char* S2 = ringA + (int)(i2 % kSA) * S::BYTES;  // plane m+1
