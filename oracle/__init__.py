@@ -173,4 +173,4 @@ def local_moments(H: CSR, a, b, sites, N):
 
 from .exact import (chebyshev_nodes, dos, dos_closed_1d, dos_closed_2d,  # noqa: E402,F401
                     exact_moments_dense, exact_moments_from_eigs, green, green_closed_1d,
-                    harper_spectrum, jackson, kernel_coeffs, lattice_spectrum)
+                    harper_spectrum, jackson, kernel_coeffs, lattice_spectrum, moment_stats)

@@ -136,6 +136,20 @@ def green_closed_1d(E, t: float = -1.0) -> np.ndarray:
     return out
 
 
+def moment_stats(mu_pv):
+    """Error bars of the stochastic trace (Eq 16: mu_n is the average over
+    R random vectors; reading X28).  mu_pv[r][n] = the moment from vector r alone.
+    Returns (mean_n, sem_n): the sample mean over r and its standard error
+    sqrt(sum_r (mu_n^(r) - mean_n)^2 / ((R - 1) R)); sem = NaN for R = 1."""
+    pv = np.asarray(mu_pv, dtype=np.float64)
+    R = pv.shape[0]
+    mean = pv.sum(axis=0) / R
+    if R < 2:
+        return mean, np.full(pv.shape[1], np.nan)
+    dev = pv - mean[None, :]
+    return mean, np.sqrt((dev * dev).sum(axis=0) / ((R - 1) * R))
+
+
 def chebyshev_nodes(K: int) -> np.ndarray:
     """x_k = cos(pi (k + 1/2) / K), k = 0..K-1 (reading X7)."""
     return np.cos(np.pi * (np.arange(K) + 0.5) / K)

@@ -412,3 +412,59 @@ def test_local_moments_average_to_trace_and_are_uniform_on_clean_lattices():
     lm2 = oracle.local_moments(H2, 6.0, 0.0, [0, 7, 33, 119], 30)
     ex2 = oracle.exact_moments_from_eigs(oracle.lattice_spectrum(3, (6, 5, 4), -1.0), 6.0, 0.0, 30)
     assert np.abs(lm2 - ex2[None, :]).max() < 1e-13
+
+
+# ---------------------------------------------------------------- error bars (X28)
+def test_moment_stats_textbook_mean_and_standard_error():
+    """oracle.moment_stats against the textbook sample mean / stdev (statistics module) on a
+    fixed table, column by column; R = 1 gives NaN standard errors."""
+    import statistics
+    pv = np.array([[1.0, 0.5, -2.0], [3.0, 0.25, 4.0], [2.0, -1.0, 1.5], [0.5, 0.0, 2.5]])
+    mean, sem = oracle.moment_stats(pv)
+    for n in range(3):
+        col = list(pv[:, n])
+        assert mean[n] == pytest.approx(statistics.fmean(col), rel=1e-15)
+        assert sem[n] == pytest.approx(statistics.stdev(col) / math.sqrt(len(col)), rel=1e-14)
+    m1, s1 = oracle.moment_stats(pv[:1])
+    assert np.array_equal(m1, pv[0]) and np.isnan(s1).all()
+
+
+def test_moment_stats_mean_is_the_estimate_and_diagonal_H_has_zero_error():
+    """Mean over per-vector moments = the R-vector estimate (Eq 16 is their average); for a
+    diagonal H (t = 0, Anderson only) xi^2 = 1 makes every vector's moment equal exactly, so
+    the standard error is 0 up to the rounding of the mean; mu_0^(r) = 1 exactly for every vector on any H."""
+    D, R, N = 64, 9, 20
+    lat0 = lat(2, (8, 8), t=0.0, onsite=ki.anderson_onsite(4, D, 2.0))
+    H0 = oracle.lattice_csr(lat0)
+    a, b = oracle.gershgorin(H0, eps=0.01)
+    mu, pv = oracle.moments_doubling(H0, a, b, ki.rademacher(8, R, D), N, per_vector=True)
+    mean, sem = oracle.moment_stats(pv)
+    assert np.abs(mean - mu).max() < 1e-14
+    assert (pv == pv[0]).all() and sem.max() < 1e-15  # only the rounding of sum/R
+    H = oracle.lattice_csr(lat(2, (8, 8), onsite=ki.anderson_onsite(4, D, 2.0)))
+    a, b = oracle.gershgorin(H)
+    mu, pv = oracle.moments_doubling(H, a, b, ki.rademacher(8, R, D), N, per_vector=True)
+    mean, sem = oracle.moment_stats(pv)
+    assert np.abs(mean - mu).max() < 1e-14
+    assert sem[0] == 0.0 and (sem[1:] > 0).all()
+
+
+def test_moment_stats_standard_error_matches_rademacher_variance_closed_form():
+    """For Rademacher vectors Var(mu_n^(r)) = 2 sum_{i!=j} [T_n(H~)]_ij^2 / D^2 (Hutchinson);
+    the sample standard error times sqrt(R) must approach it (R = 4000: the relative error
+    of a sample variance is ~ sqrt(2/R) times the kurtosis factor, well inside 20%)."""
+    L, R, N = 6, 4000, 12
+    D = L * L
+    H = oracle.lattice_csr(lat(2, (L, L), onsite=ki.anderson_onsite(2, D, 1.5)))
+    a, b = oracle.gershgorin(H)
+    w, V = np.linalg.eigh(H.dense())
+    x = np.clip((w - b) / a, -1, 1)
+    sig = np.zeros(N)
+    for n in range(N):
+        Tn = (V * np.cos(n * np.arccos(x))) @ V.T
+        sig[n] = np.sqrt(2 * ((Tn ** 2).sum() - (np.diag(Tn) ** 2).sum())) / D
+    _, pv = oracle.moments_doubling(H, a, b, ki.rademacher(77, R, D), N, per_vector=True)
+    _, sem = oracle.moment_stats(pv)
+    assert sem[0] == 0.0 and sig[0] < 1e-12
+    ratio = sem[1:] * math.sqrt(R) / sig[1:]
+    assert np.abs(ratio - 1).max() < 0.2, ratio
