@@ -262,6 +262,15 @@ kpm_status kpm_green(const double* mu, int32_t N, int32_t kernel, double lambda,
 /* Damping factors g[0..N-1] of `kernel` (host output; computed on `device`). */
 kpm_status kpm_damping(int32_t N, int32_t kernel, double lambda, double* g, int32_t device);
 
+/* Statistical error bars of the stochastic trace (Eq 16; SURVEY.md 8(f)
+ * NEXT-1): from per-vector moments mu_pv (host, [R][N] row-major, the output of
+ * kpm_moments_ex with KPM_PER_VECTOR after the doubling transform), writes mean[n] =
+ * (1/R) sum_r mu_n^(r) (equal to kpm_moments up to rounding) and sem[n] = the standard error
+ * of that mean, sqrt(sum_r (mu_n^(r) - mean[n])^2 / ((R-1) R)); sem = NaN for R = 1.
+ * Computed on `device` (two passes, fp64).  Caller owns all buffers.  KPM_ERR_INVALID_ARG on
+ * NULL pointers, R < 1 or N < 1; KPM_ERR_CUDA on a CUDA failure (outputs undefined). */
+kpm_status kpm_moment_stats(const double* mu_pv, int64_t R, int32_t N, double* mean, double* sem, int32_t device);
+
 /* Local moments mu_n^(i) = <i|T_n(H~)|i> of the global sites i = sites[0..nsites-1] (local DoS;
  * SURVEY.md 8(f) NEXT-1): kpm_moments_ex(h, N, nsites, 0, sites, KPM_LOCAL, out), out host
  * [nsites_local][N].  With KPM_PART_VECTORS the sites are split like vectors. */

@@ -2318,6 +2318,27 @@ kpm_status kpm_damping(int32_t N, int32_t kernel, double lambda, double* g, int3
     return KPM_OK;
 }
 
+kpm_status kpm_moment_stats(const double* mu_pv, int64_t R, int32_t N, double* mean, double* sem, int32_t device) {
+    if (!mu_pv || !mean || !sem || R < 1 || N < 1) return fail(KPM_ERR_INVALID_ARG, "kpm_moment_stats: bad arguments");
+    if ((size_t)R > SIZE_MAX / sizeof(double) / (size_t)N) return fail(KPM_ERR_INVALID_ARG, "kpm_moment_stats: R*N too large");
+    KPM_CUDA(cudaSetDevice(device));
+    const size_t in = (size_t)R * N * sizeof(double), out = (size_t)N * sizeof(double);
+    double* d = nullptr;
+    KPM_CUDA(cudaMalloc(&d, in + 2 * out));
+    cudaError_t e = cudaMemcpy(d, mu_pv, in, cudaMemcpyHostToDevice);
+    double* dm = d + (size_t)R * N;
+    double* ds = dm + N;
+    if (e == cudaSuccess) {
+        kpm::moment_stats_kernel<<<(N + 127) / 128, 128>>>(d, (long long)R, N, dm, ds);
+        e = cudaGetLastError();
+    }
+    if (e == cudaSuccess) e = cudaMemcpy(mean, dm, out, cudaMemcpyDeviceToHost);
+    if (e == cudaSuccess) e = cudaMemcpy(sem, ds, out, cudaMemcpyDeviceToHost);
+    cudaFree(d);
+    if (e != cudaSuccess) return fail(KPM_ERR_CUDA, "kpm_moment_stats: %s", cudaGetErrorString(e));
+    return KPM_OK;
+}
+
 kpm_status kpm_moments_local(kpm_handle h, int32_t N, const int64_t* sites, int64_t nsites, double* out) {
     if (!sites) return fail(KPM_ERR_INVALID_ARG, "kpm_moments_local: NULL sites");
     return kpm_moments_ex(h, N, nsites, 0, sites, KPM_LOCAL, out);

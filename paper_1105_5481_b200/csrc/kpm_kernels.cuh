@@ -395,6 +395,26 @@ __global__ void dos_coeff_kernel(const double* __restrict__ mu, int N, int kerne
     c[n] = mu ? (n == 0 ? 1.0 : 2.0) * g * mu[n] : g;
 }
 
+// Statistics of the per-vector moments mu_n^(r) (KPM_PER_VECTOR, layout [R][N]): the
+// sample mean over r (the estimate of Eq 16) and its standard error
+// sqrt(sum_r (mu_n^(r) - mean_n)^2 / ((R - 1) R)), two passes in fp64 (X28).
+// One thread per n; consecutive threads read consecutive n of one vector (coalesced).
+__global__ void moment_stats_kernel(const double* __restrict__ pv, long long R, int N, double* __restrict__ mean,
+                                    double* __restrict__ sem) {
+    const int n = blockIdx.x * blockDim.x + threadIdx.x;
+    if (n >= N) return;
+    double s = 0.0;
+    for (long long r = 0; r < R; ++r) s += pv[r * N + n];
+    const double m = s / (double)R;
+    double q = 0.0;
+    for (long long r = 0; r < R; ++r) {
+        const double d = pv[r * N + n] - m;
+        q = fma(d, d, q);
+    }
+    mean[n] = m;
+    sem[n] = R > 1 ? sqrt(q / ((double)(R - 1) * (double)R)) : CUDART_NAN;
+}
+
 // rho(omega) = sum_n c_n T_n(x) / (pi a sqrt(1 - x^2)), x = (omega - b)/a; T_n by Eq (4)-(5).
 __global__ void dos_kernel(const double* __restrict__ c, int N, double a, double b, const double* __restrict__ omega,
                            long long K, double* __restrict__ rho) {

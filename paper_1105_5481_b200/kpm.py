@@ -5,7 +5,7 @@ here computes moments.  If libkpm.so is missing this module raises on import
 (there is no CPU fallback).  Names follow the C ABI: kpm_create_stencil,
 kpm_create_csr, kpm_create_ell, kpm_gershgorin_stencil, kpm_gershgorin_csr,
 kpm_moments, kpm_moments_ex, kpm_moments_local, kpm_assemble, kpm_dos, kpm_dos_ex,
-kpm_green, kpm_damping, kpm_workspace_size,
+kpm_green, kpm_damping, kpm_moment_stats, kpm_workspace_size,
 kpm_set_workspace, kpm_set_stream, kpm_last_timing, kpm_step_bytes,
 kpm_destroy, kpm_last_error, kpm_version.
 """
@@ -35,7 +35,7 @@ EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershg
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
-           "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moments_local", "kpm_create_dense",
+           "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moment_stats", "kpm_moments_local", "kpm_create_dense",
            "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_last_stats", "kpm_destroy",
            "kpm_last_error", "kpm_version"]
 
@@ -72,6 +72,7 @@ _SIG = {
     "kpm_dos_ex": [_P, _i32, _i32, _f64, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_green": [_P, _i32, _i32, _f64, _f64, _f64, _P, _i64, _P, _i32],
     "kpm_damping": [_i32, _i32, _f64, _P, _i32],
+    "kpm_moment_stats": [_P, _i64, _i32, _P, _P, _i32],
     "kpm_create_dense": [_i64, _P, _i32, _f64, _f64, _i32, ctypes.POINTER(kpm_dist), _P],
     "kpm_gershgorin_dense": [_i64, _P, _i32, _f64, _P, _P],
     "kpm_moments_local": [_P, _i32, _P, _i64, _P],
@@ -458,6 +459,18 @@ def kpm_damping(N, kernel=KPM_KERNEL_JACKSON, lam=KPM_LORENTZ_DEFAULT_LAMBDA, de
     g = np.zeros(int(N), dtype=np.float64)
     _check(_lib.kpm_damping(int(N), int(kernel), float(lam), _ptr(g), int(device)))
     return g
+
+
+def kpm_moment_stats(mu_pv, device=0):
+    """(mean[N], sem[N]) of per-vector moments [R][N] (KPM_PER_VECTOR): the stochastic
+    estimate and its standard error."""
+    pv = np.ascontiguousarray(mu_pv, dtype=np.float64)
+    if pv.ndim != 2:
+        raise ValueError("mu_pv must be [R][N]")
+    R, N = pv.shape
+    mean, sem = np.zeros(N), np.zeros(N)
+    _check(_lib.kpm_moment_stats(_ptr(pv), R, N, _ptr(mean), _ptr(sem), int(device)))
+    return mean, sem
 
 
 def kpm_moments_local(h: Handle, N, sites):

@@ -144,3 +144,34 @@ def test_ldos_green_of_gpu_local_moments_matches_dense_resolvent(kpm):
         G = kpm.kpm_green(lm[k], a, b, om, kernel=kpm.KPM_KERNEL_NONE)
         ref = np.array([np.linalg.inv(w * np.eye(H.D) - Hd)[i, i] for w in om])
         assert rel(G, ref) < 1e-10
+
+
+def test_moment_stats_fixed_table_matches_oracle(kpm):
+    """kpm_moment_stats (error bars, reading X28) vs oracle.moment_stats on a seeded table
+    spanning several 128-thread blocks and a ragged tail; R = 1 gives NaN; bad args raise."""
+    pv = np.random.default_rng(5).normal(0.3, 0.02, size=(37, 301))
+    mean, sem = kpm.kpm_moment_stats(pv)
+    rm, rs = oracle.moment_stats(pv)
+    assert rel(mean, rm) < 1e-14 and rel(sem, rs) < 1e-12
+    m1, s1 = kpm.kpm_moment_stats(pv[:1])
+    assert np.array_equal(m1, pv[0]) and np.isnan(s1).all()
+    with pytest.raises(kpm.KPMError):
+        kpm.kpm_moment_stats(np.zeros((0, 4)))
+
+
+@pytest.mark.parametrize("L,R,N", [((16, 16, 10), 32, 31), ((64, 40, 1), 16, 50)])
+def test_moment_stats_of_gpu_per_vector_moments(kpm, L, R, N):
+    """Error bars end to end: per-vector moments from the GPU recursion (KPM_PER_VECTOR),
+    then kpm_moment_stats; the mean equals kpm_moments (same vectors) and both outputs
+    match the oracle's per-vector moments run through oracle.moment_stats."""
+    lat = lat_of(3 if L[2] > 1 else 2, L, W=2.0)
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    _, ref_pv = oracle.moments_doubling(H, a, b, ki.rademacher(13, R, lat["D"]), N, per_vector=True)
+    rm, rs = oracle.moment_stats(ref_pv)
+    h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"])
+    pv = h.moments_ex(N, R, 13, flags=kpm.KPM_PER_VECTOR)
+    mean, sem = kpm.kpm_moment_stats(pv)
+    assert rel(mean, h.moments(N, R, 13)) < 1e-13
+    assert rel(mean, rm) < 1e-10
+    assert sem[0] < 1e-15 and rel(sem, rs) < 1e-7
