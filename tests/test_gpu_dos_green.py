@@ -175,3 +175,24 @@ def test_moment_stats_of_gpu_per_vector_moments(kpm, L, R, N):
     assert rel(mean, h.moments(N, R, 13)) < 1e-13
     assert rel(mean, rm) < 1e-10
     assert sem[0] < 1e-15 and rel(sem, rs) < 1e-7
+
+
+def test_moment_stats_over_a_vector_partition(kpm):
+    """Error bars under KPM_PART_VECTORS: the per-vector moments of a 3-way vector split,
+    concatenated in rank order, are the global vectors' moments, so their statistics match
+    the oracle's on all R vectors."""
+    lat = lat_of(2, (48, 20), W=1.0)
+    N, R = 40, 20
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    _, ref_pv = oracle.moments_doubling(H, a, b, ki.rademacher(9, R, lat["D"]), N, per_vector=True)
+    parts = []
+    for rank in range(3):
+        h = kpm.kpm_create_stencil(2, lat["L"], -1.0, a, b, onsite=lat["onsite"],
+                                   dist=(kpm.KPM_PART_VECTORS, rank, 3))
+        parts.append(h.moments_ex(N, R, 9, flags=kpm.KPM_PER_VECTOR))
+    pv = np.concatenate(parts)
+    assert pv.shape == (R, N)
+    mean, sem = kpm.kpm_moment_stats(pv)
+    rm, rs = oracle.moment_stats(ref_pv)
+    assert rel(mean, rm) < 1e-10 and rel(sem, rs) < 1e-7
