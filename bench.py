@@ -131,14 +131,15 @@ def measure_dgemm_tflops(dev, D, R, reps=10):
 
 def oracle_sample(cfg, lat, a, b, target_s=15.0, dense=False):
     """The oracle as it stands, on a bounded sample of the workload: full D, R' vectors
-    (one per host thread, fewer for huge D), and the first N' <= N moments chosen from a
-    short calibration run so the sample takes ~target_s.  Returns D*N'*R'/s.  dense: H is
+    (one per host thread, fewer for huge D; more, up to R, when all N moments take well under
+    target_s), and the first N' <= N moments chosen from a short calibration run so the sample
+    takes ~target_s.  Returns D*N'*R'/s.  dense: H is
     handed to the oracle with all D^2 entries (the dense variant's arithmetic)."""
     import oracle
     H = oracle.csr_from_dense(ki.lattice_dense(lat), keep_zeros=True) if dense else oracle.lattice_csr(lat)
     threads = oracle.num_threads()
     D = lat["D"]
-    Rs = threads if D <= (1 << 24) else max(1, min(threads, 4))
+    Rs = min(cfg["R"], threads if D <= (1 << 24) else max(1, min(threads, 4)))
     r = ki.rademacher(cfg["seed"], Rs, D)
     t0 = time.perf_counter()
     oracle.moments_doubling(H, a, b, r, 4)                    # 2 products per vector
@@ -150,10 +151,25 @@ def oracle_sample(cfg, lat, a, b, target_s=15.0, dense=False):
     t0 = time.perf_counter()
     oracle.moments_doubling(H, a, b, r, Ns)
     dt = time.perf_counter() - t0
-    value = D * Ns * Rs / dt
+    if Ns == cfg["N"] and dt < target_s / 3 and Rs < cfg["R"]:  # all N moments fit: widen to more vectors
+        Rs = int(min(cfg["R"], Rs * max(1, int(target_s / max(dt, 1e-9)))))
+        r = ki.rademacher(cfg["seed"], Rs, D)
+        t0 = time.perf_counter()
+        oracle.moments_doubling(H, a, b, r, Ns)
+        dt = time.perf_counter() - t0
+    reps = 1
+    for _ in range(3):  # the whole workload is small: repeat it until the sample is long enough
+        if not (Ns == cfg["N"] and Rs == cfg["R"] and dt < target_s / 3) or reps >= 100000:
+            break
+        reps = int(min(100000, reps * max(2, target_s / max(dt, 1e-6))))
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            oracle.moments_doubling(H, a, b, r, Ns)
+        dt = time.perf_counter() - t0
+    value = D * Ns * Rs * reps / dt
     cores = min(threads, Rs)
     sample = (f"{Rs} of {cfg['R']} vectors (global 0..{Rs - 1}), full D={D}, first {Ns} of N={cfg['N']} moments "
-              f"({Ns // 2} products per vector); {dt:.2f} s wall on {cores} OpenMP threads; CSR build excluded")
+              f"({Ns // 2} products per vector){f", whole workload x{reps}" if reps > 1 else ""}; {dt:.2f} s wall on {cores} OpenMP threads; CSR build excluded")
     return value, cores, sample, dt
 
 
