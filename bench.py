@@ -353,7 +353,8 @@ def main():
     # roofline of the dominant kernel: the fused recursion step
     peak, peak_kind = peak_hbm()
     plan = h.plan_info(N, R) if args.format != "dense" else {"dense": 1, "tile": "64x64x32 DMMA m8n8k4"}
-    kname = ("kpm_step_kernel<EllOp> (ELL SpMM over the vector block + recursion + reductions)"
+    kname = ("kpm_ell_step_kernel (ELL SpMM over the vector block, cp.async-staged row entries, + recursion + "
+             "reductions; kpm_step_kernel<EllOp> for K > 16 or KPM_ELL_GENERIC)"
              if args.format == "csr" else
              "kpm_dense_step_kernel (DMMA fp64 GEMM H~ a_n + fused recursion and moment sums)"
              if args.format == "dense" else
