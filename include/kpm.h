@@ -55,8 +55,11 @@ enum {
     KPM_ERR_OOM = 2,         /* device allocation failed or workspace too small */
     KPM_ERR_CUDA = 3,        /* CUDA runtime error (sticky) */
     KPM_ERR_UNSUPPORTED = 4, /* valid request this build does not implement */
-    KPM_ERR_SPECTRUM = 5     /* |mu_n| > mu_0 (1 + 1e-8) or non-finite: [b-a, b+a] does not
+    KPM_ERR_SPECTRUM = 5,    /* |mu_n| > mu_0 (1 + 1e-8) or non-finite: [b-a, b+a] does not
                                 enclose the spectrum (Eq 8 requires it).  Output still written. */
+    KPM_ERR_NCCL = 6         /* an NCCL call of the handle failed, or ncclCommGetAsyncError reported an
+                                asynchronous error (a peer died, a network fault).  The communicator
+                                has been aborted; the handle is unusable except for kpm_destroy. */
 };
 
 /* Element type of H and of the vector block. */
@@ -104,10 +107,17 @@ typedef struct {
 
 /* Partition of the work across ranks (one process per GPU).  NULL = one GPU. */
 enum { KPM_PART_NONE = 0, KPM_PART_VECTORS = 1, KPM_PART_ROWS = 2 };
-/* How row-partitioned ranks exchange halo planes and combine moment sums. */
+/* How the ranks of a partition combine moment sums (and, for KPM_PART_ROWS, exchange halos). */
 enum {
-    KPM_COMM_SELF = 0,  /* world == 1 (the slab is the whole lattice; halos are local copies) */
-    KPM_COMM_NCCL = 1,  /* one process per GPU: NCCL send/recv of halo planes, all-reduce of sums */
+    KPM_COMM_SELF = 0,  /* no library collective.  KPM_PART_ROWS: world == 1 (the slab is the whole
+                           lattice; halos are local copies).  KPM_PART_VECTORS: with world > 1 the
+                           caller combines the ranks' raw sums (KPM_RAW_SUMS, its own all-reduce,
+                           kpm_assemble) -- kpm_moments then fails with KPM_ERR_INVALID_ARG */
+    KPM_COMM_NCCL = 1,  /* one process per GPU; the handle owns an NCCL communicator made from
+                           nccl_id.  KPM_PART_VECTORS: ONE ncclAllReduce of the raw sums S[N] after
+                           the recursion (Eq 16 is a sum over the ranks' vectors; PAPER.md:120-128,
+                           Fig 3 step (3) PAPER.md:179), so kpm_moments returns mu on every rank.
+                           KPM_PART_ROWS: NCCL send/recv of halo planes + the same all-reduce. */
     KPM_COMM_LOCAL = 2  /* all ranks' handles in this process, driven by kpm_moments_group */
 };
 typedef struct {
@@ -123,9 +133,12 @@ typedef struct {
                           every step (kpm_csr_partition gives the lists). */
     int32_t rank;
     int32_t world;
-    int32_t comm;            /* KPM_COMM_* (row partition only) */
+    int32_t comm;            /* KPM_COMM_* (see above) */
     const void* nccl_id;     /* KPM_COMM_NCCL: the 128-byte ncclUniqueId from kpm_nccl_unique_id on
-                                rank 0, the same on every rank */
+                                rank 0, the same on every rank.  Handles created from the same id (and
+                                rank, world, device) share one communicator, which lives while any of
+                                them does; their calls are collective and must be issued in the same
+                                order on every rank. */
     int32_t vrank, vworld;   /* KPM_PART_ROWS only -- hybrid rows x vectors:
                                 with vworld > 1 this row group runs only the global vectors
                                 kpm_vector_range(R, vrank, vworld) (0 / 0 = all vectors).  The moment
@@ -196,6 +209,38 @@ kpm_status kpm_gershgorin_dense(int64_t D, const void* H, int32_t dtype, double 
 
 /* ---- execution ------------------------------------------------------------------- */
 
+/* Kernel-plan options of one handle.  All-zero = the default plan (the fastest measured kernel
+ * for the problem shape).  The fields only restrict or pin the planner's choice -- for A/B
+ * measurements and for tests that must reach one specific kernel; the moments are the same
+ * (to rounding) under every plan.  They are per handle: the library reads no environment. */
+typedef struct {
+    int32_t no_small;      /* 1: never the single-launch shared-memory kernel (kpm_small.cuh) */
+    int32_t no_tma;        /* 1: no TMA march kernels: generic grid-stride step kernel only */
+    int32_t no_two_step;   /* 1: no two-steps-per-launch kernel (temporal blocking): single steps */
+    int32_t no_box3;       /* 1: 3D lattices: the generic TMA march, not the dense-box kernel */
+    int32_t tma_lanes;     /* lanes per tile site of the TMA march (0 = automatic); must divide the
+                              lanes per site, else the automatic choice is kept */
+    int32_t halo_warp;     /* two-step kernel: 0 = automatic, 1 = a ninth warp for the halo sites,
+                              2 = no halo warp */
+    int32_t ell_generic;   /* 1: ELL steps through the generic kernel, not kpm_ell_step_kernel */
+    int32_t no_overlap;    /* 1: row partition: halo exchange after each step, not overlapped */
+    int32_t no_fused_halo; /* 1: in-process slab groups: plane copies, not fused peer stores */
+    int32_t contiguous;    /* 1: 3D march: contiguous plane ranges, not round-robin columns */
+    int32_t no_graph;      /* 1: launch the recursion step by step instead of replaying a captured
+                              CUDA graph of the step loop */
+    int32_t experimental;  /* experimental kernels, compiled only into libkpm_exp.so (the default
+                              libkpm.so answers KPM_ERR_UNSUPPORTED): 1 = 3D two-step kernel
+                              (exp_param = tile shape 0..3), 2 = KS-steps-per-launch 2D kernel
+                              (exp_param = KS, 3 or 4), 3 = persistent L2-resident kernel */
+    int32_t exp_param;
+    int32_t reserved[7];   /* must be 0 */
+} kpm_plan_opts;
+
+/* Set (opts != NULL) or reset to the default (opts == NULL) the plan options of h.
+ * KPM_ERR_INVALID_ARG for negative fields or non-zero reserved words; KPM_ERR_UNSUPPORTED for
+ * an experimental kernel this build does not contain. */
+kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* opts);
+
 /* Use this CUDA stream (a cudaStream_t; NULL = legacy default stream). */
 kpm_status kpm_set_stream(kpm_handle h, void* stream);
 
@@ -206,15 +251,20 @@ kpm_status kpm_workspace_size(kpm_handle h, int32_t N, int64_t R, uint32_t flags
  * The caller keeps it alive until kpm_destroy or the next kpm_set_workspace. NULL = own. */
 kpm_status kpm_set_workspace(kpm_handle h, void* dev_ptr, size_t bytes);
 
-/* mu[0..N-1] (host) from R random vectors drawn from `seed`.  One GPU only
- * (with KPM_PART_VECTORS and world > 1 use kpm_moments_ex + KPM_RAW_SUMS). */
+/* mu[0..N-1] (host) from R random vectors drawn from `seed` (R = the GLOBAL number of vectors).
+ * Partitions: KPM_PART_VECTORS with KPM_COMM_NCCL and KPM_PART_ROWS with KPM_COMM_NCCL return the
+ * same mu on every rank (all ranks call collectively); KPM_PART_VECTORS with world > 1 and
+ * KPM_COMM_SELF fails with KPM_ERR_INVALID_ARG (use kpm_moments_ex + KPM_RAW_SUMS + kpm_assemble). */
 kpm_status kpm_moments(kpm_handle h, int32_t N, int64_t R, uint64_t seed, double* mu);
 
 /* General form.  R is the GLOBAL number of vectors; this rank runs its share R_local.
  * r0: NULL = generate (see conventions); else this rank's start vectors, vector-major
  *     [R_local][D] of real doubles (host, or device with KPM_DEVICE_IN).
- * out: mu[N]; or [R_local][N] with KPM_PER_VECTOR; or S[N] with KPM_RAW_SUMS
- *      (host, or device with KPM_DEVICE_OUT). */
+ * out: mu[N] (all ranks' vectors, as kpm_moments); or [R_local][N] with KPM_PER_VECTOR (this
+ *      rank's vectors, no collective); or S[N] with KPM_RAW_SUMS (sums over THIS rank's vectors,
+ *      before any collective, for callers that bring their own all-reduce); host, or device with
+ *      KPM_DEVICE_OUT (then the call returns without synchronising the stream).
+ * Errors: KPM_ERR_NCCL if the handle's collective failed (see KPM_ERR_NCCL). */
 kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, const void* r0,
                           uint32_t flags, void* out);
 
@@ -301,11 +351,16 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
  * straight into the neighbours' ghost planes (fused halo, in-process slab groups). */
 kpm_status kpm_last_stats(kpm_handle h, int64_t stats[4]);
 
-/* Algorithmic HBM bytes moved by the recursion-step launches of the last kpm_moments_ex
- * call: 3 D R s per single step (read a_n, read a_{n-1}, write
- * a_{n+1}), 4 D R s per two-step launch, plus 8 D per launch for an on-site array and
- * K D (4 + s) per launch for ELL.  Divide by kpm_last_timing's steps_ms. */
+/* Algorithmic HBM bytes of the recursion steps of the last kpm_moments_ex call, SURVEY.md 8(d):
+ * per recursion step 3 D R s (read a_n, read a_{n-1}, write a_{n+1}; s = 8 fp64, 16 complex128)
+ * + 8 D for a stored on-site array + K D (4 + s) for ELL -- whatever kernel ran (a two-step
+ * launch counts two steps).  Divide by kpm_last_timing's steps_ms. */
 kpm_status kpm_step_bytes(kpm_handle h, double* bytes);
+
+/* bytes[0] = kpm_step_bytes; bytes[1] = the compulsory DRAM bytes of the kernels that ran: every
+ * vector block, on-site array and ELL array a launch touches counted once per launch (a two-step
+ * launch reads a_n, a_{n-1} and writes a_{n+1}, a_{n+2}: 4 D R s for two steps). */
+kpm_status kpm_step_traffic(kpm_handle h, double bytes[2]);
 
 void kpm_destroy(kpm_handle h); /* NULL-safe */
 const char* kpm_last_error(void);

@@ -8,9 +8,12 @@
  *
  * Plain, slow, obviously correct: CSR storage built here from the lattice
  * description, one vector at a time, fp64 throughout.  OpenMP parallelises
- * over the random vectors only (the paper's own decomposition: "the total
- * number of threads ... is SR"); per-vector results are summed
- * in the fixed order r = 0..R-1, so the result does not depend on threads.
+ * over the random vectors (the paper's own decomposition: "the total number
+ * of threads ... is SR"); per-vector results are summed in the
+ * fixed order r = 0..R-1.  With fewer vectors than threads the vectors run in
+ * turn and each row loop / inner product is split over the threads instead
+ * (SURVEY.md 8(d)); only then does the inner-product summation order depend on
+ * the thread count (reading X18).
  *
  * Functions and the passage each follows:
  *   oracle_build_lattice_csr   O1: H of the periodic nearest-neighbour lattice
@@ -134,8 +137,16 @@ typedef struct {
     double a, b;
 } csr_t;
 
+/* Parallel decomposition: OpenMP over the R vectors (the paper's own
+ * decomposition); when there are fewer vectors than threads, the vectors run one
+ * after the other and each row loop / inner product below is split over the threads instead
+ * ("rows" below = 1).  Only the summation order of the inner products changes with it (reading
+ * X18: rounding order is free; X17's tolerance covers it). */
+static int rows = 0;
+
 /* y = H~ x = (H x - b x) / a, real H (Eq 8). */
 static void apply_Ht_real(const csr_t *H, const double *x, double *y) {
+#pragma omp parallel for schedule(static) if (rows)
     for (int64_t i = 0; i < H->D; i++) {
         double s = 0.0;
         for (int64_t k = H->rowptr[i]; k < H->rowptr[i + 1]; k++) s += H->val_re[k] * x[H->col[k]];
@@ -145,6 +156,7 @@ static void apply_Ht_real(const csr_t *H, const double *x, double *y) {
 
 /* y = H~ x = (H x - b x) / a, complex H (Eq 8). */
 static void apply_Ht_cplx(const csr_t *H, const double complex *x, double complex *y) {
+#pragma omp parallel for schedule(static) if (rows)
     for (int64_t i = 0; i < H->D; i++) {
         double complex s = 0.0;
         for (int64_t k = H->rowptr[i]; k < H->rowptr[i + 1]; k++)
@@ -155,13 +167,25 @@ static void apply_Ht_cplx(const csr_t *H, const double complex *x, double comple
 
 static double dot_real(int64_t D, const double *u, const double *v) {
     double s = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : s) if (rows)
     for (int64_t i = 0; i < D; i++) s += u[i] * v[i];
     return s;
+}
+
+/* nx = 2 nx - p (Eq 18), real and complex */
+static void recur_real(int64_t D, double *nx, const double *p) {
+#pragma omp parallel for schedule(static) if (rows)
+    for (int64_t i = 0; i < D; i++) nx[i] = 2.0 * nx[i] - p[i];
+}
+static void recur_cplx(int64_t D, double complex *nx, const double complex *p) {
+#pragma omp parallel for schedule(static) if (rows)
+    for (int64_t i = 0; i < D; i++) nx[i] = 2.0 * nx[i] - p[i];
 }
 
 /* Re <u|v> = Re sum_i conj(u_i) v_i */
 static double redot_cplx(int64_t D, const double complex *u, const double complex *v) {
     double s = 0.0;
+#pragma omp parallel for schedule(static) reduction(+ : s) if (rows)
     for (int64_t i = 0; i < D; i++) s += creal(conj(u[i]) * v[i]);
     return s;
 }
@@ -188,7 +212,8 @@ int oracle_moments_direct(int64_t D, const int64_t *rowptr, const int32_t *col,
     csr_t H = {D, rowptr, col, val_re, val_im, a, b};
     double *m = calloc((size_t)(R * N), sizeof(double));
     if (!m) return 2;
-#pragma omp parallel for schedule(dynamic, 1)
+    rows = R < omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) if (!rows)
     for (int64_t q = 0; q < R; q++) {
         const double *rv = r + q * D;
         double *mq = m + q * N;
@@ -203,7 +228,7 @@ int oracle_moments_direct(int64_t D, const int64_t *rowptr, const int32_t *col,
             }
             for (int n = 2; n < N; n++) {
                 apply_Ht_real(&H, u1, u2);                /* (Eq 18) */
-                for (int64_t i = 0; i < D; i++) u2[i] = 2.0 * u2[i] - u0[i];
+                recur_real(D, u2, u0);
                 mq[n] = dot_real(D, rv, u2);              /* <r_0|r_n> (Eq 19) */
                 double *tmp = u0; u0 = u1; u1 = u2; u2 = tmp;
             }
@@ -222,7 +247,7 @@ int oracle_moments_direct(int64_t D, const int64_t *rowptr, const int32_t *col,
             }
             for (int n = 2; n < N; n++) {
                 apply_Ht_cplx(&H, u1, u2);
-                for (int64_t i = 0; i < D; i++) u2[i] = 2.0 * u2[i] - u0[i];
+                recur_cplx(D, u2, u0);
                 mq[n] = redot_cplx(D, rc, u2);
                 double complex *tmp = u0; u0 = u1; u1 = u2; u2 = tmp;
             }
@@ -250,7 +275,8 @@ int oracle_moments_doubling(int64_t D, const int64_t *rowptr, const int32_t *col
     csr_t H = {D, rowptr, col, val_re, val_im, a, b};
     double *m = calloc((size_t)(R * N), sizeof(double));
     if (!m) return 2;
-#pragma omp parallel for schedule(dynamic, 1)
+    rows = R < omp_get_max_threads();
+#pragma omp parallel for schedule(dynamic, 1) if (!rows)
     for (int64_t q = 0; q < R; q++) {
         const double *rv = r + q * D;
         double *mq = m + q * N;
@@ -268,7 +294,7 @@ int oracle_moments_doubling(int64_t D, const int64_t *rowptr, const int32_t *col
                     mq[2 * n] = 2.0 * dot_real(D, c, c) - s0;
                     if (2 * n + 1 >= N) break;
                     apply_Ht_real(&H, c, nx);
-                    for (int64_t i = 0; i < D; i++) nx[i] = 2.0 * nx[i] - p[i];
+                    recur_real(D, nx, p);
                     mq[2 * n + 1] = 2.0 * dot_real(D, c, nx) - s1;
                     double *tmp = p; p = c; c = nx; nx = tmp;
                 }
@@ -289,7 +315,7 @@ int oracle_moments_doubling(int64_t D, const int64_t *rowptr, const int32_t *col
                     mq[2 * n] = 2.0 * redot_cplx(D, c, c) - s0;
                     if (2 * n + 1 >= N) break;
                     apply_Ht_cplx(&H, c, nx);
-                    for (int64_t i = 0; i < D; i++) nx[i] = 2.0 * nx[i] - p[i];
+                    recur_cplx(D, nx, p);
                     mq[2 * n + 1] = 2.0 * redot_cplx(D, c, nx) - s1;
                     double complex *tmp = p; p = c; c = nx; nx = tmp;
                 }

@@ -1,4 +1,9 @@
-"""Build libkpm.so (the C-ABI library, include/kpm.h) in-tree for sm_100a with nvcc."""
+"""Build libkpm.so (the C-ABI library, include/kpm.h) in-tree for sm_100a with nvcc.
+
+Two artefacts from the same sources: libkpm.so (the product) and libkpm_exp.so (-DKPM_EXPERIMENTAL:
+the same library plus the kernels that are parity-green but measured slower than the default plan,
+reachable only through kpm_plan_opts.experimental; tests and A/B measurements load it explicitly).
+Both compile in parallel."""
 from __future__ import annotations
 
 import glob
@@ -8,6 +13,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libkpm.so")
+LIB_EXP = os.path.join(HERE, "libkpm_exp.so")
 NVCC_FLAGS = ["-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
               "-Xcompiler", "-fPIC", "-Xcompiler", "-O2", "-shared", "-Xptxas", "-warn-spills"]
 
@@ -29,19 +35,27 @@ def nccl_dir() -> str:
     raise RuntimeError("nccl.h not found (nvidia-nccl wheel)")
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    newest = max(os.path.getmtime(p) for p in sources())
-    if not force and os.path.exists(LIB) and os.path.getmtime(LIB) >= newest:
-        return LIB
+def _cmd(out, extra=()):
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
     nd = nccl_dir()
-    cmd = [nvcc, *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-           "-o", LIB + ".tmp", os.path.join(HERE, "csrc", "kpm_capi.cu"), "-lcudart",
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
-    if verbose:
-        print(" ".join(cmd))
-    subprocess.check_call(cmd)
-    os.replace(LIB + ".tmp", LIB)
+    return [nvcc, *NVCC_FLAGS, *extra, "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+            "-o", out + ".tmp", os.path.join(HERE, "csrc", "kpm_capi.cu"), "-lcudart",
+            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    newest = max(os.path.getmtime(p) for p in sources())
+    jobs = []
+    for out, extra in ((LIB, ()), (LIB_EXP, ("-DKPM_EXPERIMENTAL",))):
+        if force or not os.path.exists(out) or os.path.getmtime(out) < newest:
+            cmd = _cmd(out, extra)
+            if verbose:
+                print(" ".join(cmd))
+            jobs.append((out, subprocess.Popen(cmd)))
+    for out, pr in jobs:
+        if pr.wait() != 0:
+            raise subprocess.CalledProcessError(pr.returncode, "nvcc -> " + os.path.basename(out))
+        os.replace(out + ".tmp", out)
     return LIB
 
 

@@ -11,20 +11,28 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
+#include <thread>
+#include <utility>
 #include <vector>
 
 #include "../../include/kpm.h"
 #include "kpm_kernels.cuh"
 #include "kpm_tma.cuh"
 #include "kpm_tma2.cuh"
-#include "kpm_tmak.cuh"
 #include "kpm_tma3.cuh"
+// Kernels that are parity-green but measured slower than the default plan:
+// their templates are instantiated (launched) only under KPM_EXPERIMENTAL, i.e. in libkpm_exp.so,
+// and reached through kpm_plan_opts.experimental.  The default libkpm.so contains none of them.
+#include "kpm_tmak.cuh"
 #include "kpm_tma32.cuh"
 #include "kpm_persist.cuh"
 #include "kpm_ell.cuh"
@@ -120,7 +128,11 @@ struct kpm_handle_s {
     cudaEvent_t ev_bnd = nullptr, ev_comm = nullptr;
     int step_launches = 0, total_launches = 0;
     int halo_copies = 0, fused_halo_launches = 0;  // row partition: plane copies / launches storing into peers
-    double steps_bytes = 0.0;  // algorithmic HBM bytes of the recursion-step launches of the last call
+    double steps_bytes = 0.0;   // SURVEY.md 8(d) algorithmic bytes of the recursion steps of the last call
+    double design_bytes = 0.0;  // compulsory DRAM bytes of the kernels that ran (each array once per launch)
+    int smem_optin = 227 * 1024;  // cudaDevAttrMaxSharedMemoryPerBlockOptin
+    kpm_plan_opts opts{};         // kpm_set_plan_opts (zero = default plan)
+    bool dead = false;            // an NCCL failure aborted the communicator
 };
 
 namespace {
@@ -167,16 +179,116 @@ struct Plan {
 
 bool is_cplx(const kpm_handle_s* h) { return h->dtype == KPM_COMPLEX128; }
 
-bool env_on(const char* name) {
-    const char* e = getenv(name);
-    return e && e[0] && e[0] != '0';
-}
-bool tma_disabled() { return env_on("KPM_NO_TMA"); }
-int env_int(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return (e && e[0]) ? atoi(e) : dflt;
+// ---- NCCL: the handle's communicator (KPM_COMM_NCCL), failures -> KPM_ERR_NCCL
+//
+// Communicators are shared: handles created from the same (ncclUniqueId, rank, world, device)
+// reuse one ncclComm_t (reference counted), so creating a handle per call -- the end-to-end
+// pattern, H uploaded every time -- does not pay ncclCommInitRank every time.
+struct CommEntry {
+    ncclComm_t comm = nullptr;
+    int refs = 0;
+    bool aborted = false;
+};
+std::mutex g_comm_mu;
+std::map<std::string, CommEntry> g_comms;  // key: id bytes + rank/world/device
+std::map<ncclComm_t, std::string> g_comm_key;
+
+void comm_release(ncclComm_t c, bool abort) {
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    auto k = g_comm_key.find(c);
+    if (k == g_comm_key.end()) return;
+    CommEntry& e = g_comms[k->second];
+    if (abort && !e.aborted) {
+        ncclCommAbort(c);  // release the peers that wait on this rank
+        e.aborted = true;
+    }
+    if (--e.refs == 0) {
+        if (!e.aborted) ncclCommDestroy(c);
+        g_comms.erase(k->second);
+        g_comm_key.erase(k);
+    }
 }
 
+kpm_status nccl_fail(kpm_handle_s* h, ncclResult_t e, const char* what) {
+    if (h->nccl) comm_release(h->nccl, true);
+    h->nccl = nullptr;
+    h->dead = true;
+    return fail(KPM_ERR_NCCL, "%s: %s", what, ncclGetErrorString(e));
+}
+#define KPM_NCCL(h, call, what)                                  \
+    do {                                                         \
+        ncclResult_t e_ = (call);                                \
+        if (e_ != ncclSuccess) return nccl_fail((h), e_, (what)); \
+    } while (0)
+
+// Asynchronous errors (a peer that died, a transport fault) surface only through
+// ncclCommGetAsyncError; an in-flight collective would otherwise block the stream forever.
+kpm_status nccl_poll(kpm_handle_s* h) {
+    if (!h->nccl) return KPM_OK;
+    ncclResult_t ae = ncclSuccess;
+    KPM_NCCL(h, ncclCommGetAsyncError(h->nccl, &ae), "ncclCommGetAsyncError");
+    if (ae != ncclSuccess && ae != ncclInProgress) return nccl_fail(h, ae, "asynchronous NCCL error");
+    return KPM_OK;
+}
+
+// Wait for the handle's stream; with a communicator, poll its error state while waiting.
+kpm_status sync_stream(kpm_handle_s* h) {
+    if (!h->nccl) {
+        KPM_CUDA(cudaStreamSynchronize(h->stream));
+        return KPM_OK;
+    }
+    for (;;) {
+        const cudaError_t q = cudaStreamQuery(h->stream);
+        if (q == cudaSuccess) break;
+        if (q != cudaErrorNotReady) KPM_CUDA(q);
+        KPM_TRY(nccl_poll(h));
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
+    return nccl_poll(h);
+}
+
+// Communicator of a KPM_COMM_NCCL partition, from the caller's broadcast ncclUniqueId (shared
+// with earlier handles of the same id, rank, world and device).
+kpm_status init_comm(kpm_handle_s* h, const kpm_dist* dist) {
+    if (!dist || dist->partition == KPM_PART_NONE || dist->comm != KPM_COMM_NCCL) return KPM_OK;
+    ncclUniqueId id;
+    memcpy(&id, dist->nccl_id, sizeof id);
+    std::string key(reinterpret_cast<const char*>(&id), sizeof id);
+    char tail[64];
+    snprintf(tail, sizeof tail, "/%d/%d/%d", dist->rank, dist->world, h->device);
+    key += tail;
+    KPM_CUDA(cudaSetDevice(h->device));
+    std::lock_guard<std::mutex> lk(g_comm_mu);
+    CommEntry& e = g_comms[key];
+    if (e.aborted) return fail(KPM_ERR_NCCL, "the communicator of this nccl_id was aborted by an earlier failure");
+    if (!e.comm) {
+        const ncclResult_t r = ncclCommInitRank(&e.comm, dist->world, id, dist->rank);
+        if (r != ncclSuccess) {
+            g_comms.erase(key);
+            return fail(KPM_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
+        }
+        g_comm_key[e.comm] = key;
+    }
+    e.refs++;
+    h->nccl = e.comm;
+    return KPM_OK;
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) is a per-device setting: remember, per (kernel,
+// device), the largest size already set.  Thread-safe (handles may live on several threads/devices).
+std::mutex g_attr_mu;
+std::map<std::pair<const void*, int>, size_t> g_attr;
+kpm_status set_smem(const void* kern, size_t smem, int device) {
+    if (smem <= 48 * 1024) return KPM_OK;
+    std::lock_guard<std::mutex> lk(g_attr_mu);
+    size_t& done = g_attr[{kern, device}];
+    if (done >= smem) return KPM_OK;
+    KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    done = smem;
+    return KPM_OK;
+}
+
+#ifdef KPM_EXPERIMENTAL
 // Shared memory of the instantiated KS-step kernels (0 = not instantiated).
 size_t stepk_smem(int ks, int tl, bool onsite, int RP) {
     using namespace kpm;
@@ -189,7 +301,6 @@ size_t stepk_smem(int ks, int tl, bool onsite, int RP) {
 
 // Shared memory of the instantiated 3D two-step kernels (0 = not instantiated); KA, KP ring depths.
 constexpr int kKA32 = 5, kKP32 = 4;
-int nt32() { return env_int("KPM_TMA32_NT", 256) == 512 ? 512 : 256; }  // experiment: threads per CTA
 size_t step32_smem(int tx, int ty, int tl, bool onsite, int RP) {
     using namespace kpm;
     constexpr int NT = 512, KA = kKA32, KP = kKP32;  // (NT only sizes the reduction scratch)
@@ -208,13 +319,13 @@ size_t step32_smem(int tx, int ty, int tl, bool onsite, int RP) {
 // dividing the lattice, 4 vector blocks (the caller falls back to single steps otherwise).
 void plan_tma32(const kpm_handle_s* h, Plan* p) {
     p->use_tma32 = false;
-    // Opt-in (KPM_TMA32=1): correct (GPU parity tests) but measured slower than the single-step
-    // dense-box kernel on c3 (2.64 ms per launch = 1.32 ms per step vs 1.02 ms).
-    if (!env_on("KPM_TMA32")) return;
-    if (h->ndim != 3 || p->no_fused || h->rows || is_cplx(h) || env_on("KPM_NO_TMA32")) return;
+    // Experimental (opts.experimental = 1): correct (GPU parity tests) but measured slower than the
+    // single-step dense-box kernel on c3 (2.64 ms per launch = 1.32 ms per step vs 1.02 ms).
+    if (h->opts.experimental != 1) return;
+    if (h->ndim != 3 || p->no_fused || h->rows || is_cplx(h)) return;
     const int RG = p->RG;
     int TX = 8, TY = 8, TL = 8;
-    const int shape = env_int("KPM_TMA32_SHAPE", 0);  // experiment: 1 = 16x4x8, 2 = 8x4x16
+    const int shape = h->opts.exp_param;  // 1 = 16x4x8, 2 = 8x4x16, 3 = 16x8x8
     if (shape == 1) { TX = 16; TY = 4; TL = 8; }
     if (shape == 2) { TX = 8; TY = 4; TL = 16; }
     if (shape == 3) { TX = 16; TY = 8; TL = 8; }
@@ -227,16 +338,17 @@ void plan_tma32(const kpm_handle_s* h, Plan* p) {
     p->TL32 = TL;
     p->tma32_smem = sm;
     // whole columns round-robin when there are enough of them (in-plane halos then hit L2)
-    p->tma32_rr = (cols >= 4LL * h->num_sms && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
+    p->tma32_rr = (cols >= 4LL * h->num_sms && !h->opts.contiguous) ? 1 : 0;
     p->tma32_grid = (int)std::min<long long>(p->tma32_rr ? cols : cols * h->L[2], (long long)h->num_sms);
     p->use_tma32 = true;
 }
+#endif
 
 // Tile choice for the TMA march: ~16 KB main tiles (TX*TY*TL = 1024 lanes), full passes
 // of the 256 consumer threads, tiles dividing the lattice, lane groups dividing RG.
 void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     p->use_tma = false;
-    if (h->kind != KIND_STENCIL || h->ndim < 2 || (flags & KPM_DIRECT) || tma_disabled()) return;
+    if (h->kind != KIND_STENCIL || h->ndim < 2 || (flags & KPM_DIRECT) || h->opts.no_tma) return;
     const int RG = p->RG;
     int TL = 0;
     // 3D: 16 lanes (256 contiguous bytes per site) first -- c3 measured 1119 ms vs 1358 ms with 8 lanes
@@ -246,8 +358,8 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     const int cands2r[3] = {16, 32, 8}, cands2c[3] = {32, 16, 8}, cands3[3] = {16, 32, 8};
     for (int c : (h->ndim == 2 ? (is_cplx(h) ? cands2c : cands2r) : cands3))
         if (RG % c == 0) { TL = c; break; }
-    const int tl_env = env_int("KPM_TMA_TL", 0);  // experiment: lanes per tile site
-    if (tl_env && RG % tl_env == 0) TL = tl_env;
+    const int tl_opt = h->opts.tma_lanes;  // pinned lanes per tile site (A/B, tests)
+    if (tl_opt > 0 && RG % tl_opt == 0) TL = tl_opt;
     if (!TL) return;
     int TX, TY;
     if (h->ndim == 2) {
@@ -276,7 +388,7 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     p->TY = TY;
     p->tma_grid = (int)std::min<long long>(W, h->num_sms);
     p->use_tma3 = false;
-    if (h->ndim == 3 && !env_on("KPM_NO_TMA3")) {
+    if (h->ndim == 3 && !h->opts.no_box3) {
         const bool on = h->d_eps != nullptr;
         size_t sm3 = 0;
         if (TX == 16 && TY == 8 && TL == 8) sm3 = on ? kpm::step3_smem_bytes<16, 8, 8, true>(p->RP) : kpm::step3_smem_bytes<16, 8, 8, false>(p->RP);
@@ -289,13 +401,13 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     }
     // 3D: whole columns round-robin when there are enough of them (in-plane halos then hit L2)
     const long long cols = W / Lm;
-    p->tma_rr = (h->ndim == 3 && cols >= 4LL * p->tma_grid && !getenv("KPM_TMA_CONTIGUOUS")) ? 1 : 0;
+    p->tma_rr = (h->ndim == 3 && cols >= 4LL * p->tma_grid && !h->opts.contiguous) ? 1 : 0;
     p->use_tma = true;
     // two-step kernel: 2D lattices with L0 >= 4, same tiles, shared memory permitting
     // One CTA per SM with TX*TL = 1024 lanes per row tile (measured on c2: two co-resident
     // CTAs with half-width tiles were 5% slower).
     p->use_tma2 = false;
-    if (h->ndim == 2 && !p->no_fused && !env_on("KPM_NO_TMA2") && h->L[0] >= 4 && h->L[1] >= 4) {
+    if (h->ndim == 2 && !p->no_fused && !h->opts.no_two_step && h->L[0] >= 4 && h->L[1] >= 4) {
         const bool on = h->d_eps != nullptr;
         const int tx1 = 1024 / TL;
         const size_t sm1 = kpm::step2_smem_bytes(tx1, TL, on, p->RP);
@@ -313,9 +425,10 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     }
     // KS-step kernel: 2D lattices, row tiles of TXK * TLK = 512 lanes (kpm_tmak.cuh)
     p->use_tmak = false;
-    // Opt-in (KPM_TMAK_KS = 3 or 4): measured slower than the two-step kernel on c2 and c4
-    // ("deeper temporal blocking"), so the default plan does not use it.
-    const int ks = env_on("KPM_NO_TMAK") ? 0 : env_int("KPM_TMAK_KS", 0);
+#ifdef KPM_EXPERIMENTAL
+    // Experimental (opts.experimental = 2, exp_param = KS = 3 or 4): measured slower than the
+    // two-step kernel on c2 and c4 ("deeper temporal blocking").
+    const int ks = h->opts.experimental == 2 ? h->opts.exp_param : 0;
     if (h->ndim == 2 && !p->no_fused && ks >= 2) {
         const bool on = h->d_eps != nullptr;
         const int tlk = RG % 16 == 0 ? 16 : (RG % 8 == 0 ? 8 : 0);
@@ -332,6 +445,7 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
         }
     }
     plan_tma32(h, p);
+#endif
 }
 
 kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags, bool with_r0, Plan* p,
@@ -365,7 +479,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->use_tma) p->gx = p->tma_grid;
     if (h->kind == KIND_DENSE) p->gx = (int)(h->Dp / kpm::kDBM);  // partial rows = M tiles
     p->small_smem = 2 * (size_t)h->D * p->TR * sizeof(double2);
-    p->use_small = !h->rows && !(flags & KPM_DIRECT) && p->small_smem <= kpm::kSmallSmemMax && !env_on("KPM_NO_SMALL") &&
+    p->use_small = !h->rows && !(flags & KPM_DIRECT) && p->small_smem <= kpm::kSmallSmemMax && !h->opts.no_small &&
                    h->kind != KIND_DENSE;
     if (p->use_small) {
         p->use_tma = p->use_tma2 = p->use_tma32 = false;
@@ -378,7 +492,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->nslots = N;
     if (h->rows) p->use_tma2 = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
     p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL && !(flags & KPM_DIRECT) &&
-                 !env_on("KPM_NO_OVERLAP");
+                 !h->opts.no_overlap;
     if (p->overlap) p->gx = 3 * p->tma_grid;
     if (p->use_tmak && p->M - 1 < p->KSK) p->use_tmak = false;
     p->xpad = (h->kind == KIND_STENCIL && h->ndim == 3) ? 2 : 0;
@@ -390,19 +504,21 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
                              : p->xpad ? (size_t)(h->plane / h->L[0]) * (h->L[0] + 2 * p->xpad) : (size_t)h->plane;
     p->ghost_lanes = plane_mem * p->RG;
     p->lane_bytes = (p->mem_sites * p->RG + 2 * p->ghost_lanes) * sizeof(double2);
-    // Persistent L2-resident mode (opt-in, KPM_PERSIST=1): the whole recursion in one cooperative
-    // launch, one 512-thread CTA per SM per lane-group row of the grid.  Measured on c2 with R = 8
-    // (2 x 16.8 MB, L2-resident): 7.85 ms vs 7.42 ms for the per-step launches -- the launch gaps
-    // it removes are smaller than what the grid barrier costs.
+    // Persistent L2-resident mode (experimental, opts.experimental = 3): the whole recursion in one
+    // cooperative launch, one 512-thread CTA per SM per lane-group row of the grid.  Measured on c2
+    // with R = 8 (2 x 16.8 MB, L2-resident): 7.85 ms vs 7.42 ms for the per-step launches of round 1
+    // -- the launch gaps it removes are smaller than what the grid barrier costs.
     p->use_persist = false;
+#ifdef KPM_EXPERIMENTAL
     if (!p->use_small && h->kind != KIND_DENSE && !h->rows && !(flags & KPM_DIRECT) && p->M >= 2 &&
-        !env_on("KPM_NO_PERSIST") && p->gy <= h->num_sms && env_on("KPM_PERSIST")) {
+        p->gy <= h->num_sms && h->opts.experimental == 3) {
         p->use_persist = true;
         p->use_tma = p->use_tma2 = p->use_tma32 = p->use_tmak = p->use_tma3 = false;
         p->overlap = false;
         const long long site_ctas = (h->D + p->TS - 1) / p->TS;
         p->gx = (int)std::max<long long>(1, std::min<long long>(site_ctas, h->num_sms / p->gy));
     }
+#endif
     size_t off = 0;
     p->off_P = off; off = align_up(off + p->lane_bytes);
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
@@ -486,11 +602,7 @@ kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, i
     dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
     const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX);
     auto kern = kpm::kpm_ell_step_kernel<CPLX>;
-    static size_t configured = 0;
-    if (configured < smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        configured = smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, smem, h->device));
     const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a};
     kern<<<grid, block, smem, h->stream>>>(op, v, tail);
     KPM_CUDA(cudaGetLastError());
@@ -502,11 +614,7 @@ template <bool CPLX, class OP>
 kpm_status launch_small_t(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int from_buf, int N,
                           double* part) {
     auto kern = kpm::kpm_small_kernel<OP, CPLX>;
-    static size_t configured = 0;
-    if (configured < p.small_smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.small_smem));
-        configured = p.small_smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, p.small_smem, h->device));
     kern<<<dim3(1, p.gy), dim3(p.TR, p.TS), p.small_smem, h->stream>>>(op, v, from_buf, N, part);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
@@ -535,6 +643,7 @@ kpm_status launch_small(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, i
     }
 }
 
+#ifdef KPM_EXPERIMENTAL
 template <class OP, bool CPLX>
 kpm_status launch_persist_t(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int first_buf, int N,
                             long long slot, double* part) {
@@ -559,10 +668,15 @@ kpm_status launch_persist_op(kpm_handle_s* h, const Plan& p, const OP& op, const
     return launch_persist_t<OP, CPLX>(h, p, op, v, first_buf, N, slot, part);
 }
 
+#endif
+
 // Dispatch on the operator type of the handle.
 kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& v, int tail) {
     using namespace kpm;
-    if (h->kind == KIND_ELL && mode == STEP && h->K > 0 && h->K <= kEllKMax && !env_on("KPM_ELL_GENERIC"))
+    // the staged ELL kernel when its tile (index + value panels of TS * kEllSPW rows, double
+    // buffered) fits the device's opt-in shared memory; else the generic kernel
+    if (h->kind == KIND_ELL && mode == STEP && h->K > 0 && h->K <= kEllKMax && !h->opts.ell_generic &&
+        ell_smem_bytes(kThreads, p.TS, h->K, is_cplx(h)) <= (size_t)h->smem_optin)
         return is_cplx(h) ? launch_ell_t<true>(h, p, v, tail) : launch_ell_t<false>(h, p, v, tail);
     if (h->kind == KIND_ELL) {
         if (is_cplx(h)) return launch_mode<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a}, mode, v, tail);
@@ -584,6 +698,7 @@ kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& 
     }
 }
 
+#ifdef KPM_EXPERIMENTAL
 kpm_status launch_persist(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int first_buf, int N, long long slot,
                           double* part) {
     using namespace kpm;
@@ -609,6 +724,11 @@ kpm_status launch_persist(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v,
         default: return launch_persist_op<false>(h, p, StencilOp<3, true, false>{g}, v, first_buf, N, slot, part);
     }
 }
+#else
+kpm_status launch_persist(kpm_handle_s*, const Plan&, const kpm::VecArgs&, int, int, long long, double*) {
+    return fail(KPM_ERR_UNSUPPORTED, "persistent kernel: experimental build only (libkpm_exp.so)");
+}
+#endif
 
 using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
 
@@ -714,11 +834,7 @@ template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB, int XW>
 kpm_status launch_tma2_x(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
     auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS, MINB, XW>;
-    static size_t configured = 0;
-    if (configured < p.tma2_smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma2_smem));
-        configured = p.tma2_smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, p.tma2_smem, h->device));
     kern<<<p.tma2_grid, kpm::Threads2<XW>::N, p.tma2_smem, h->stream>>>(A.A2, A.Col2, P.A2, P.Col, E, E2, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
@@ -727,11 +843,12 @@ kpm_status launch_tma2_x(kpm_handle_s* h, const Plan& p, const BufMaps& A, const
 
 // Halo warp (XW = 1, kpm_tma2.cuh) for complex128 (Peierls) lattices: c4 3178 vs 3387 ms per call;
 // real lattices keep XW = 0 (c2 26.8 vs 25.9 ms: the 168-register cap of nine warps spills there).
-// KPM_TMA2_XW=0/1 overrides.
+// opts.halo_warp = 1 / 2 pins it on / off.
 template <int TL, int TX, bool ONSITE, bool PEIERLS, int MINB>
 kpm_status launch_tma2_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
-    if (env_int("KPM_TMA2_XW", PEIERLS ? 1 : 0)) return launch_tma2_x<TL, TX, ONSITE, PEIERLS, MINB, 1>(h, p, A, P, E, E2, g, tail);
+    const bool xw = h->opts.halo_warp == 1 || (h->opts.halo_warp == 0 && PEIERLS);
+    if (xw) return launch_tma2_x<TL, TX, ONSITE, PEIERLS, MINB, 1>(h, p, A, P, E, E2, g, tail);
     return launch_tma2_x<TL, TX, ONSITE, PEIERLS, MINB, 0>(h, p, A, P, E, E2, g, tail);
 }
 
@@ -757,15 +874,12 @@ kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX2);
 }
 
+#ifdef KPM_EXPERIMENTAL
 template <int KS, int TL, int TX, bool ONSITE, bool PEIERLS>
 kpm_status launch_tmak_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& EH, const kpm::TmaKGeom& g, int tail) {
     auto kern = kpm::kpm_stepk_tma_kernel<KS, TL, TX, ONSITE, PEIERLS>;
-    static size_t configured = 0;
-    if (configured < p.tmak_smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tmak_smem));
-        configured = p.tmak_smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, p.tmak_smem, h->device));
     kern<<<p.tmak_grid, kpm::StepKThreads<KS, TL, TX>::NT, p.tmak_smem, h->stream>>>(A.AK, A.AKH, P.AK, P.AKH1, E, EH, g,
                                                                                      tail);
     KPM_CUDA(cudaGetLastError());
@@ -794,6 +908,12 @@ kpm_status launch_tmak(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     if (p.KSK == 3 && p.TLK == 8) return launch_tmak_s<3, 8, 64>(h, p, A, P, E, EH, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no KS-step kernel for KS=%d TL=%d", p.KSK, p.TLK);
 }
+#else
+kpm_status launch_tmak(kpm_handle_s*, const Plan&, const BufMaps&, const BufMaps&, const CUtensorMap&, const CUtensorMap&,
+                       const kpm::TmaKGeom&, int) {
+    return fail(KPM_ERR_UNSUPPORTED, "KS-step kernel: experimental build only (libkpm_exp.so)");
+}
+#endif
 
 // eps~ in the x-row frame layout [L2][L1][L0+4] with a box of bx x by sites (3D two-step kernel)
 kpm_status make_epsf_map(const kpm_handle_s* h, int bx, int by, CUtensorMap* m) {
@@ -810,15 +930,12 @@ kpm_status make_epsf_map(const kpm_handle_s* h, int bx, int by, CUtensorMap* m) 
     return KPM_OK;
 }
 
+#ifdef KPM_EXPERIMENTAL
 template <int TX, int TY, int TL, bool ONSITE, int NT, int KA = kKA32, int KP = kKP32>
 kpm_status launch_tma32_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                           const CUtensorMap& E1, const kpm::Tma32Geom& g, int tail) {
     auto kern = kpm::kpm_step32_tma_kernel<TX, TY, TL, ONSITE, NT, KA, KP>;
-    static size_t configured = 0;
-    if (configured < p.tma32_smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma32_smem));
-        configured = p.tma32_smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, p.tma32_smem, h->device));
     kern<<<p.tma32_grid, NT, p.tma32_smem, h->stream>>>(A.A32, A.A32r, P.P32, P.P32r, E, E1, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
@@ -830,9 +947,6 @@ kpm_status launch_tma32(kpm_handle_s* h, const Plan& p, const BufMaps& A, const 
                         const CUtensorMap& E1, const kpm::Tma32Geom& g, int tail) {
     const bool on = h->d_eps != nullptr;
     if (p.TX32 == 8 && p.TY32 == 8 && p.TL32 == 8) {
-        if (nt32() == 512)
-            return on ? launch_tma32_t<8, 8, 8, true, 512>(h, p, A, P, E, E1, g, tail)
-                      : launch_tma32_t<8, 8, 8, false, 512>(h, p, A, P, E, E1, g, tail);
         return on ? launch_tma32_t<8, 8, 8, true, 256>(h, p, A, P, E, E1, g, tail)
                   : launch_tma32_t<8, 8, 8, false, 256>(h, p, A, P, E, E1, g, tail);
     }
@@ -845,16 +959,18 @@ kpm_status launch_tma32(kpm_handle_s* h, const Plan& p, const BufMaps& A, const 
                   : launch_tma32_t<16, 8, 8, false, 256, 3, 2>(h, p, A, P, E, E1, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no 3D two-step kernel for %dx%dx%d", p.TX32, p.TY32, p.TL32);
 }
+#else
+kpm_status launch_tma32(kpm_handle_s*, const Plan&, const BufMaps&, const BufMaps&, const CUtensorMap&, const CUtensorMap&,
+                        const kpm::Tma32Geom&, int) {
+    return fail(KPM_ERR_UNSUPPORTED, "3D two-step kernel: experimental build only (libkpm_exp.so)");
+}
+#endif
 
 template <int TX, int TY, int TL, bool ONSITE>
 kpm_status launch_tma3_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
                          const kpm::TmaGeom& g, int tail, int grid) {
     auto kern = kpm::kpm_step3_tma_kernel<TX, TY, TL, ONSITE>;
-    static size_t configured = 0;
-    if (configured < p.tma_smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma_smem));
-        configured = p.tma_smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, p.tma_smem, h->device));
     kern<<<grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.Box3, cur.Row3, prev.P, E, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
@@ -865,11 +981,7 @@ template <int NDIM, bool ONSITE, bool PEIERLS>
 kpm_status launch_tma_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
                         const kpm::TmaGeom& g, int tail, int grid) {
     auto kern = kpm::kpm_step_tma_kernel<NDIM, ONSITE, PEIERLS>;
-    static size_t configured = 0;
-    if (configured < p.tma_smem) {
-        KPM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.tma_smem));
-        configured = p.tma_smem;
-    }
+    KPM_TRY(set_smem((const void*)kern, p.tma_smem, h->device));
     kern<<<grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.A, cur.Col, cur.Row, prev.P, E, g, tail);
     KPM_CUDA(cudaGetLastError());
     h->total_launches++;
@@ -908,13 +1020,15 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
             return fail(KPM_ERR_UNSUPPORTED, "partition %d not supported", dist->partition);
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
             return fail(KPM_ERR_INVALID_ARG, "bad rank %d / world %d", dist->rank, dist->world);
-        if (dist->partition == KPM_PART_ROWS) {
+        if (dist->partition != KPM_PART_NONE) {
             if (dist->comm != KPM_COMM_SELF && dist->comm != KPM_COMM_NCCL && dist->comm != KPM_COMM_LOCAL)
                 return fail(KPM_ERR_INVALID_ARG, "bad comm %d", dist->comm);
-            if (dist->comm == KPM_COMM_SELF && dist->world != 1)
-                return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_SELF needs world == 1");
             if (dist->comm == KPM_COMM_NCCL && !dist->nccl_id)
                 return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_NCCL needs nccl_id");
+        }
+        if (dist->partition == KPM_PART_ROWS) {
+            if (dist->comm == KPM_COMM_SELF && dist->world != 1)
+                return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_SELF needs world == 1");
             if (dist->vworld > 1 && (dist->vrank < 0 || dist->vrank >= dist->vworld))
                 return fail(KPM_ERR_INVALID_ARG, "bad vector group %d of %d", dist->vrank, dist->vworld);
         }
@@ -929,6 +1043,7 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
     h->dist.nccl_id = nullptr;  // not kept
     cudaDeviceGetAttribute(&h->num_sms, cudaDevAttrMultiProcessorCount, device);
     cudaDeviceGetAttribute(&h->l2_bytes, cudaDevAttrL2CacheSize, device);
+    cudaDeviceGetAttribute(&h->smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     cudaMemPool_t pool;
     if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
         uint64_t keep = UINT64_MAX;  // keep freed workspace in the pool for the next handle
@@ -1064,6 +1179,7 @@ struct Run {
         h->halo_copies = 0;
         h->fused_halo_launches = 0;
         h->steps_bytes = 0.0;
+        h->design_bytes = 0.0;
 
         v.P = P;
         v.C = C;
@@ -1108,6 +1224,7 @@ struct Run {
             const double vb = (double)h->D * (double)p.R_loc * s_el;
             const double mb = h->kind == KIND_ELL ? (double)h->K * (double)h->D * (4.0 + s_el) : 0.0;
             h->steps_bytes = 2.0 * vb + (p.M - 1) * (3.0 * vb + (h->d_eps ? 8.0 * (double)h->D : 0.0) + mb);
+            h->design_bytes = h->steps_bytes;
             nsteps = 0;
             n = 1;
             return KPM_OK;
@@ -1221,8 +1338,8 @@ struct Run {
                 tg32.rr = p.tma32_rr;
                 tg32.W = p.tma32_rr ? cols : cols * tg32.L2;
                 tg32.rows_total = p.gx;
-                tg32.pfirst = env_int("KPM_TMA32_PFIRST", 1);  // measured: evict-first a_{n-1} 5.3 GB vs 6.2 GB DRAM reads
-                tg32.lg_fast = env_int("KPM_TMA32_LGFAST", 0);
+                tg32.pfirst = 1;   // measured: evict-first a_{n-1} 5.3 GB vs 6.2 GB DRAM reads
+                tg32.lg_fast = 0;
                 tg32.t = tg.t;
                 tg32.shift = tg.shift;
             }
@@ -1277,14 +1394,8 @@ struct Run {
         g.red1 = r1_;
         g.red2 = r2_;
         dim3 grid(p.RP / kpm::kDBN, (unsigned)(h->Dp / kpm::kDBM));
-        static bool configured = false;
-        if (!configured) {
-            KPM_CUDA(cudaFuncSetAttribute(kpm::kpm_dense_step_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)kpm::kDenseSmem));
-            KPM_CUDA(cudaFuncSetAttribute(kpm::kpm_dense_step_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          (int)kpm::kDenseSmem));
-            configured = true;
-        }
+        KPM_TRY(set_smem((const void*)kpm::kpm_dense_step_kernel<true>, kpm::kDenseSmem, h->device));
+        KPM_TRY(set_smem((const void*)kpm::kpm_dense_step_kernel<false>, kpm::kDenseSmem, h->device));
         if (first) kpm::kpm_dense_step_kernel<true><<<grid, kpm::kDThreads, kpm::kDenseSmem, h->stream>>>(g, tail);
         else kpm::kpm_dense_step_kernel<false><<<grid, kpm::kDThreads, kpm::kDenseSmem, h->stream>>>(g, tail);
         KPM_CUDA(cudaGetLastError());
@@ -1369,13 +1480,17 @@ struct Run {
                 e = ncclRecv(X + (h->D + h->roff[q]) * p.RG, h->rcnt[q] * lb, ncclUint8, q, h->nccl, st);
         }
         ncclResult_t e2 = ncclGroupEnd();
-        if (e != ncclSuccess || e2 != ncclSuccess)
-            return fail(KPM_ERR_UNSUPPORTED, "NCCL ghost exchange: %s", ncclGetErrorString(e != ncclSuccess ? e : e2));
-        return KPM_OK;
+        if (e != ncclSuccess || e2 != ncclSuccess) return nccl_fail(h, e != ncclSuccess ? e : e2, "NCCL ghost exchange");
+        return nccl_poll(h);
     }
     kpm_status (*exchange_hook)(Run*) = nullptr;
 
     bool more() const { return n <= nsteps; }
+    // the vector partition's all-reduce of S runs inside the library (KPM_COMM_NCCL)
+    bool vector_collective() const {
+        return !h->rows && h->dist.partition == KPM_PART_VECTORS && h->dist.comm == KPM_COMM_NCCL && h->nccl &&
+               !(flags & (KPM_RAW_SUMS | KPM_PER_VECTOR));
+    }
     double2* fresh() const { return cur; }
 
     kpm_status launch_next() {
@@ -1384,6 +1499,7 @@ struct Run {
             KPM_TRY(launch_dense(false, cur, prev, part + (size_t)(2 * n) * slot, part + (size_t)(2 * n + 1) * slot,
                                  tail ? part + (size_t)(2 * n + 2) * slot : nullptr, tail));
             h->steps_bytes += 3.0 * vbytes + mbytes;
+            h->design_bytes += 3.0 * vbytes + mbytes;
             h->step_launches++;
             std::swap(cur, prev);
             ++n;
@@ -1403,7 +1519,8 @@ struct Run {
             prev = spare0;
             spare0 = oc;
             spare1 = op;
-            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->steps_bytes += KS * (3.0 * vbytes + ebytes);  // KS steps
+            h->design_bytes += 4.0 * vbytes + ebytes;
             h->step_launches++;
             n += KS;
             return KPM_OK;
@@ -1422,7 +1539,8 @@ struct Run {
             prev = spare0;
             spare0 = oc;
             spare1 = op;
-            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->steps_bytes += 2.0 * (3.0 * vbytes + ebytes);  // two steps
+            h->design_bytes += 4.0 * vbytes + ebytes;        // a_n, a_{n-1} read, a_{n+1}, a_{n+2} written once
             h->step_launches++;
             n += 2;
             return KPM_OK;
@@ -1442,7 +1560,8 @@ struct Run {
             prev = spare0;
             spare0 = oc;
             spare1 = op;
-            h->steps_bytes += 4.0 * vbytes + ebytes;
+            h->steps_bytes += 2.0 * (3.0 * vbytes + ebytes);  // two steps
+            h->design_bytes += 4.0 * vbytes + ebytes;        // a_n, a_{n-1} read, a_{n+1}, a_{n+2} written once
             h->step_launches++;
             n += 2;
             return KPM_OK;
@@ -1454,6 +1573,7 @@ struct Run {
             v.red1 = v.red2 = nullptr;
             KPM_TRY(launch(h, p, r0 ? kpm::DIRECT_BUF : kpm::DIRECT_GEN, v, 0));
             h->steps_bytes += 3.0 * vbytes + ebytes + mbytes + (r0 ? vbytes : 0.0);
+            h->design_bytes += 3.0 * vbytes + ebytes + mbytes + (r0 ? vbytes : 0.0);
         } else {
             v.red0 = part + (size_t)(2 * n) * slot;      // <a_n|a_n>     -> mu_{2n}
             v.red1 = part + (size_t)(2 * n + 1) * slot;  // <a_n|a_{n+1}> -> mu_{2n+1}
@@ -1475,6 +1595,7 @@ struct Run {
                 KPM_TRY(launch(h, p, kpm::STEP, v, tail));
             }
             h->steps_bytes += 3.0 * vbytes + ebytes + mbytes;
+            h->design_bytes += 3.0 * vbytes + ebytes + mbytes;
         }
         h->step_launches++;
         std::swap(cur, prev);
@@ -1508,18 +1629,21 @@ struct Run {
             src = dout;
             out_bytes = (size_t)ne * sizeof(double);
         } else {
-            if (h->dist.partition == KPM_PART_VECTORS && h->dist.world > 1)
-                return fail(KPM_ERR_INVALID_ARG, "multi-rank: use KPM_RAW_SUMS, all-reduce, then kpm_assemble");
-            kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, 1.0 / ((double)h->D_total * (double)p.R_loc),
-                                                                         direct, dout);
+            const bool multi = h->dist.partition == KPM_PART_VECTORS && h->dist.world > 1;
+            if (multi && !vector_collective())
+                return fail(KPM_ERR_INVALID_ARG,
+                            "multi-rank vector partition without KPM_COMM_NCCL: use KPM_RAW_SUMS, all-reduce, then kpm_assemble");
+            // S holds the sums over all R vectors after the all-reduce, else over this rank's R_loc = R
+            const double Rn = multi ? (double)R : (double)p.R_loc;
+            kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, 1.0 / ((double)h->D_total * Rn), direct, dout);
             KPM_CUDA(cudaGetLastError());
             h->total_launches++;
             src = dout;
             out_bytes = (size_t)N * sizeof(double);
         }
         KPM_CUDA(cudaMemcpyAsync(out, src, out_bytes, dev_out ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->stream));
-        if (dev_out) return KPM_OK;
-        KPM_CUDA(cudaStreamSynchronize(h->stream));
+        if (dev_out) return nccl_poll(h);
+        KPM_TRY(sync_stream(h));
         if (!(flags & KPM_RAW_SUMS)) {
             const long long rows = (flags & KPM_PER_VECTOR) ? p.R_loc : 1;
             KPM_TRY(spectrum_guard(static_cast<const double*>(out), rows, N));
@@ -1566,9 +1690,8 @@ kpm_status Run::exchange_on(double2* X, cudaStream_t st) {
     if (e == ncclSuccess) e = ncclSend(last_plane(X), pb, ncclUint8, hi, h->nccl, st);
     if (e == ncclSuccess) e = ncclRecv(ghost_lo(X), pb, ncclUint8, lo, h->nccl, st);
     ncclResult_t e2 = ncclGroupEnd();
-    if (e != ncclSuccess || e2 != ncclSuccess)
-        return fail(KPM_ERR_UNSUPPORTED, "NCCL halo exchange: %s", ncclGetErrorString(e != ncclSuccess ? e : e2));
-    return KPM_OK;
+    if (e != ncclSuccess || e2 != ncclSuccess) return nccl_fail(h, e != ncclSuccess ? e : e2, "NCCL halo exchange");
+    return nccl_poll(h);
 }
 
 // Halo exchange of a single row-partitioned handle (world 1: a local wrap copy; NCCL:
@@ -1620,6 +1743,42 @@ kpm_status exchange_group(std::vector<Run>& runs, std::vector<cudaEvent_t>& evs)
     return KPM_OK;
 }
 
+// Random-vector partition over in-process handles (KPM_COMM_LOCAL): every rank's recursion is
+// enqueued on its own stream (interleaved launch by launch, so the ranks progress together), then
+// the raw sums are added on the host in rank order -- the in-process form of the one all-reduce
+// of SURVEY.md 8(e) P1 -- and assembled with the global R.
+kpm_status moments_group_vectors(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, uint64_t seed, double* mu) {
+    for (int i = 0; i < nh; ++i)
+        if (!hs[i] || hs[i]->dist.partition != KPM_PART_VECTORS || hs[i]->dist.comm != KPM_COMM_LOCAL ||
+            hs[i]->dist.rank != i || hs[i]->dist.world != nh)
+            return fail(KPM_ERR_INVALID_ARG, "handle %d is not rank %d of a KPM_COMM_LOCAL vector partition of %d", i, i, nh);
+    std::vector<Run> runs(nh);
+    for (int i = 0; i < nh; ++i) KPM_TRY(runs[i].begin(hs[i], N, R, seed, nullptr, 0u));
+    bool any = true;
+    while (any) {
+        any = false;
+        for (int i = 0; i < nh; ++i)
+            if (runs[i].more()) {
+                KPM_CUDA(cudaSetDevice(hs[i]->device));
+                KPM_TRY(runs[i].launch_next());
+                any = true;
+            }
+    }
+    std::vector<double> Ssum(N, 0.0), Si(N);
+    for (int i = 0; i < nh; ++i) {
+        KPM_CUDA(cudaSetDevice(hs[i]->device));
+        KPM_TRY(runs[i].collect());
+    }
+    for (int i = 0; i < nh; ++i) {
+        KPM_CUDA(cudaSetDevice(hs[i]->device));
+        KPM_CUDA(cudaMemcpyAsync(Si.data(), runs[i].S, N * sizeof(double), cudaMemcpyDeviceToHost, hs[i]->stream));
+        KPM_CUDA(cudaStreamSynchronize(hs[i]->stream));
+        for (int k = 0; k < N; ++k) Ssum[k] += Si[k];  // fixed rank order
+    }
+    KPM_TRY(kpm_assemble(nullptr, Ssum.data(), N, hs[0]->D_total, R, 0u, mu));
+    return Run::spectrum_guard(mu, 1, N);
+}
+
 }  // namespace
 
 extern "C" {
@@ -1641,7 +1800,7 @@ void kpm_destroy(kpm_handle h) {
     cudaFree(h->d_ghost_src);
     cudaFree(h->d_send);
     cudaFree(h->d_dense);
-    if (h->nccl) ncclCommDestroy(h->nccl);
+    if (h->nccl) comm_release(h->nccl, false);
     if (h->ev_begin) cudaEventDestroy(h->ev_begin);
     if (h->ev_end) cudaEventDestroy(h->ev_end);
     if (h->ev_bnd) cudaEventDestroy(h->ev_bnd);
@@ -1723,12 +1882,6 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
         h->L[h->slow] = h->nloc;
         h->D = h->plane * h->nloc;
         site0 = h->z0 * h->plane;
-        if (st == KPM_OK && dist->comm == KPM_COMM_NCCL) {
-            ncclUniqueId id;
-            memcpy(&id, dist->nccl_id, sizeof id);
-            ncclResult_t nr = ncclCommInitRank(&h->nccl, dist->world, id, dist->rank);
-            if (nr != ncclSuccess) st = fail(KPM_ERR_UNSUPPORTED, "ncclCommInitRank: %s", ncclGetErrorString(nr));
-        }
     }
     if (st == KPM_OK && d->onsite) {
         std::vector<double> e(h->D);
@@ -1736,6 +1889,7 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
         cudaError_t ce = cudaMalloc(&h->d_eps, h->D * sizeof(double));
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_eps, e.data(), h->D * sizeof(double), cudaMemcpyHostToDevice);
         if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site upload: %s", cudaGetErrorString(ce));
+#ifdef KPM_EXPERIMENTAL
         if (st == KPM_OK && h->ndim == 3 && !h->rows) {
             // x-row frame copy for the 3D two-step kernel: row pitch L0 + 4, two periodic images per side
             const size_t L0 = (size_t)h->L[0], rowsN = (size_t)(h->L[1] * h->L[2]), pf = (L0 + 4) * 8;
@@ -1750,6 +1904,7 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
             }
             if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site frame: %s", cudaGetErrorString(ce));
         }
+#endif
     }
     if (st == KPM_OK && d->flux != 0.0) {
         std::vector<double2> ph(h->L[0]);
@@ -1762,6 +1917,7 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_phase, ph.data(), h->L[0] * sizeof(double2), cudaMemcpyHostToDevice);
         if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "phase upload: %s", cudaGetErrorString(ce));
     }
+    if (st == KPM_OK) st = init_comm(h, dist);
     if (st != KPM_OK) {
         kpm_destroy(h);
         return st;
@@ -1883,12 +2039,6 @@ kpm_status ell_rows_setup(kpm_handle_s* h, const kpm_dist* dist, std::vector<int
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_send, send.data(), send.size() * sizeof(int32_t), cudaMemcpyHostToDevice);
     }
     if (ce != cudaSuccess) return fail(KPM_ERR_CUDA, "row-partition lists: %s", cudaGetErrorString(ce));
-    if (dist->comm == KPM_COMM_NCCL) {
-        ncclUniqueId id;
-        memcpy(&id, dist->nccl_id, sizeof id);
-        ncclResult_t nr = ncclCommInitRank(&h->nccl, W, id, g);
-        if (nr != ncclSuccess) return fail(KPM_ERR_UNSUPPORTED, "ncclCommInitRank: %s", ncclGetErrorString(nr));
-    }
     return KPM_OK;
 }
 
@@ -1931,6 +2081,7 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_val, v.data(), v.size() * sizeof(double), cudaMemcpyHostToDevice);
         if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "ELL upload: %s", cudaGetErrorString(ce));
     }
+    if (st == KPM_OK) st = init_comm(h, dist);
     if (st != KPM_OK) {
         kpm_destroy(h);
         return st;
@@ -1984,6 +2135,11 @@ kpm_status kpm_create_dense(int64_t D, const void* H, int32_t dtype, double a, d
     if (ce != cudaSuccess) {
         kpm_destroy(h);
         return fail(KPM_ERR_CUDA, "dense upload: %s", cudaGetErrorString(ce));
+    }
+    const kpm_status st = init_comm(h, dist);
+    if (st != KPM_OK) {
+        kpm_destroy(h);
+        return st;
     }
     *out = h;
     return KPM_OK;
@@ -2052,10 +2208,9 @@ kpm_status kpm_csr_partition(int64_t D, const int64_t* rowptr, const int32_t* co
 kpm_status kpm_set_stream(kpm_handle h, void* stream) {
     if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
     KPM_CUDA(cudaSetDevice(h->device));
-    if (h->own_stream && h->stream) {
-        cudaStreamSynchronize(h->stream);
-        cudaStreamDestroy(h->stream);
-    }
+    // work already queued on the outgoing stream (the workspace may be freed or reused on the new one)
+    KPM_CUDA(cudaStreamSynchronize(h->stream));
+    if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
     h->stream = static_cast<cudaStream_t>(stream);
     h->own_stream = false;
     return KPM_OK;
@@ -2086,6 +2241,7 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
                           void* out) {
     if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
     if (!out) return fail(KPM_ERR_INVALID_ARG, "NULL output");
+    if (h->dead) return fail(KPM_ERR_NCCL, "the handle's communicator was aborted by an earlier NCCL failure");
     if (h->rows && h->dist.comm == KPM_COMM_LOCAL)
         return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL slab handles run through kpm_moments_group");
     Run run;
@@ -2099,16 +2255,20 @@ kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, con
     KPM_TRY(run.collect());
     if (h->rows && h->dist.comm == KPM_COMM_NCCL) {
         // moment sums over all slabs: one all-reduce of S (and the per-vector Sv) over NCCL
-        ncclResult_t e = ncclAllReduce(run.S, run.S, N, ncclFloat64, ncclSum, h->nccl, h->stream);
-        if (e == ncclSuccess)
-            e = ncclAllReduce(run.Sv, run.Sv, (size_t)N * run.p.R_loc, ncclFloat64, ncclSum, h->nccl, h->stream);
-        if (e != ncclSuccess) return fail(KPM_ERR_UNSUPPORTED, "NCCL all-reduce: %s", ncclGetErrorString(e));
+        KPM_NCCL(h, ncclAllReduce(run.S, run.S, N, ncclFloat64, ncclSum, h->nccl, h->stream), "ncclAllReduce (S)");
+        KPM_NCCL(h, ncclAllReduce(run.Sv, run.Sv, (size_t)N * run.p.R_loc, ncclFloat64, ncclSum, h->nccl, h->stream),
+                 "ncclAllReduce (Sv)");
+    } else if (run.vector_collective()) {
+        // random-vector partition: the ONE collective of the method -- S[N]
+        // summed over the ranks' vectors (Eq 16; Fig 3 step (3))
+        KPM_NCCL(h, ncclAllReduce(run.S, run.S, N, ncclFloat64, ncclSum, h->nccl, h->stream), "ncclAllReduce (S)");
     }
     return run.output(out);
 }
 
 kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, uint64_t seed, double* mu) {
     if (!hs || nh < 1 || !mu) return fail(KPM_ERR_INVALID_ARG, "bad kpm_moments_group arguments");
+    if (hs[0] && hs[0]->dist.partition == KPM_PART_VECTORS) return moments_group_vectors(hs, nh, N, R, seed, mu);
     for (int i = 0; i < nh; ++i) {
         if (!hs[i] || !hs[i]->rows || hs[i]->dist.comm != KPM_COMM_LOCAL || hs[i]->dist.rank != i ||
             hs[i]->dist.world != nh)
@@ -2133,8 +2293,8 @@ kpm_status kpm_moments_group(kpm_handle* hs, int32_t nh, int32_t N, int64_t R, u
     // boundary planes straight into the neighbours' ghost planes of the same block (peer memory),
     // so between launches only stream ordering remains -- each rank's next launch waits for its two
     // neighbours' current one (their ghost writes into it, and their reads of the ghosts it
-    // overwrites next).  KPM_NO_FUSED_HALO=1 keeps the copy exchange.
-    bool fused = st == KPM_OK && !env_on("KPM_NO_FUSED_HALO");
+    // overwrites next).  opts.no_fused_halo = 1 (on hs[0]) keeps the copy exchange.
+    bool fused = st == KPM_OK && !hs[0]->opts.no_fused_halo;
     for (int i = 0; i < nh && fused; ++i)
         fused = hs[i]->kind == KIND_STENCIL && runs[i].p.use_tma && !runs[i].p.overlap;
     // slabs on different GPUs: the kernels store into the neighbours' memory over NVLink, which
@@ -2207,7 +2367,7 @@ kpm_status kpm_nccl_unique_id(void* out128) {
     if (!out128) return fail(KPM_ERR_INVALID_ARG, "NULL output");
     ncclUniqueId id;
     ncclResult_t e = ncclGetUniqueId(&id);
-    if (e != ncclSuccess) return fail(KPM_ERR_UNSUPPORTED, "ncclGetUniqueId: %s", ncclGetErrorString(e));
+    if (e != ncclSuccess) return fail(KPM_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(e));
     memcpy(out128, &id, sizeof id);
     return KPM_OK;
 }
@@ -2391,6 +2551,34 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
 kpm_status kpm_step_bytes(kpm_handle h, double* bytes) {
     if (!h || !bytes) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
     *bytes = h->steps_bytes;
+    return KPM_OK;
+}
+
+kpm_status kpm_step_traffic(kpm_handle h, double bytes[2]) {
+    if (!h || !bytes) return fail(KPM_ERR_INVALID_ARG, "NULL argument");
+    bytes[0] = h->steps_bytes;
+    bytes[1] = h->design_bytes;
+    return KPM_OK;
+}
+
+kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
+    if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
+    if (!o) {
+        h->opts = kpm_plan_opts{};
+        return KPM_OK;
+    }
+    const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
+                         o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
+                         o->no_graph,  o->experimental, o->exp_param};
+    for (int32_t x : f)
+        if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
+    for (int32_t x : o->reserved)
+        if (x != 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: reserved words must be 0");
+    if (o->halo_warp > 2 || o->experimental > 3) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: value out of range");
+#ifndef KPM_EXPERIMENTAL
+    if (o->experimental) return fail(KPM_ERR_UNSUPPORTED, "experimental kernels are built into libkpm_exp.so only");
+#endif
+    h->opts = *o;
     return KPM_OK;
 }
 

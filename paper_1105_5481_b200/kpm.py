@@ -18,12 +18,12 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libkpm.so")
+LIB_EXP_PATH = os.path.join(_HERE, "libkpm_exp.so")  # + the experimental (slower) kernels
 if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                       "g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
-_lib = ctypes.CDLL(LIB_PATH)
 
-KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM_ERR_SPECTRUM = range(6)
+KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM_ERR_SPECTRUM, KPM_ERR_NCCL = range(7)
 KPM_REAL64, KPM_COMPLEX128 = 0, 1
 KPM_KERNEL_JACKSON, KPM_KERNEL_NONE, KPM_KERNEL_LORENTZ, KPM_KERNEL_FEJER = 0, 1, 2, 3
 KPM_LORENTZ_DEFAULT_LAMBDA = 4.0
@@ -36,13 +36,23 @@ EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershg
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
            "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moment_stats", "kpm_moments_local", "kpm_create_dense",
-           "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_last_stats", "kpm_destroy",
-           "kpm_last_error", "kpm_version"]
+           "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_last_stats", "kpm_set_plan_opts",
+           "kpm_step_traffic", "kpm_destroy", "kpm_last_error", "kpm_version"]
 
 
 class kpm_stencil_desc(ctypes.Structure):
     _fields_ = [("ndim", ctypes.c_int32), ("L", ctypes.c_int64 * 3), ("t", ctypes.c_double),
                 ("onsite", ctypes.c_void_p), ("flux", ctypes.c_double)]
+
+
+class kpm_plan_opts(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int32) for n in (
+        "no_small", "no_tma", "no_two_step", "no_box3", "tma_lanes", "halo_warp", "ell_generic", "no_overlap",
+        "no_fused_halo", "contiguous", "no_graph", "experimental", "exp_param")] + [("reserved", ctypes.c_int32 * 7)]
+
+
+PLAN_OPTS = [f[0] for f in kpm_plan_opts._fields_ if f[0] != "reserved"]
+EXP_3D_TWO_STEP, EXP_KSTEP, EXP_PERSIST = 1, 2, 3  # kpm_plan_opts.experimental
 
 
 class kpm_dist(ctypes.Structure):
@@ -82,15 +92,42 @@ _SIG = {
     "kpm_slab_range": [_i64, _i32, _i32, _P, _P],
     "kpm_nccl_unique_id": [_P],
     "kpm_moments_group": [_P, _i32, _i32, _i64, _u64, _P],
+    "kpm_set_plan_opts": [_P, ctypes.POINTER(kpm_plan_opts)],
+    "kpm_step_traffic": [_P, _P],
 }
-for _name, _args in _SIG.items():
-    _fn = getattr(_lib, _name)
-    _fn.argtypes = _args
-    _fn.restype = ctypes.c_int32
-_lib.kpm_destroy.argtypes = [_P]
-_lib.kpm_destroy.restype = None
-_lib.kpm_last_error.restype = ctypes.c_char_p
-_lib.kpm_version.restype = ctypes.c_char_p
+
+
+def _load(path):
+    lib = ctypes.CDLL(path)
+    for name, args in _SIG.items():
+        fn = getattr(lib, name)
+        fn.argtypes = args
+        fn.restype = ctypes.c_int32
+    lib.kpm_destroy.argtypes = [_P]
+    lib.kpm_destroy.restype = None
+    lib.kpm_last_error.restype = ctypes.c_char_p
+    lib.kpm_version.restype = ctypes.c_char_p
+    return lib
+
+
+_lib = _load(LIB_PATH)
+_lib_default = _lib
+_lib_exp = None
+
+
+def use_experimental(on: bool = True):
+    """Route the handles created from now on to libkpm_exp.so (the same library plus the
+    experimental kernels of kpm_plan_opts.experimental), or back to libkpm.so.  A handle keeps
+    the library it was created with."""
+    global _lib, _lib_exp
+    if on:
+        if _lib_exp is None:
+            if not os.path.exists(LIB_EXP_PATH):
+                raise ImportError(f"{LIB_EXP_PATH} is missing (built by __graft_entry__.build())")
+            _lib_exp = _load(LIB_EXP_PATH)
+        _lib = _lib_exp
+    else:
+        _lib = _lib_default
 
 
 class KPMError(RuntimeError):
@@ -99,9 +136,9 @@ class KPMError(RuntimeError):
         self.status = status
 
 
-def _check(st):
+def _check(st, lib=None):
     if st != KPM_OK:
-        raise KPMError(st, _lib.kpm_last_error().decode())
+        raise KPMError(st, (lib or _lib).kpm_last_error().decode())
 
 
 def _ptr(a):
@@ -168,6 +205,7 @@ class Handle:
     """Owns one kpm_handle (one GPU, one process)."""
 
     def __init__(self, raw, D, R_of=None, dist=None):
+        self._lib = _lib         # the library that created it (libkpm.so or libkpm_exp.so)
         self._h = raw
         self.D = int(D)          # global number of sites
         self.D_local = int(D)    # sites on this rank (row partition: its slab)
@@ -176,9 +214,31 @@ class Handle:
     def __del__(self):
         self.close()
 
+    def _ck(self, st):
+        _check(st, self._lib)
+
+    def set_plan_opts(self, **opts):
+        """kpm_set_plan_opts: keyword fields of kpm_plan_opts (no_small=1, tma_lanes=8, ...);
+        no keywords = the default plan."""
+        unknown = set(opts) - set(PLAN_OPTS)
+        if unknown:
+            raise ValueError(f"unknown plan options {sorted(unknown)}")
+        if not opts:
+            self._ck(self._lib.kpm_set_plan_opts(self._h, None))
+            return
+        o = kpm_plan_opts(**{k: int(v) for k, v in opts.items()})
+        self._ck(self._lib.kpm_set_plan_opts(self._h, ctypes.byref(o)))
+
+    def step_traffic(self):
+        """(SURVEY 8(d) algorithmic bytes, compulsory DRAM bytes of the kernels that ran) of the
+        recursion steps of the last call."""
+        b = (ctypes.c_double * 2)()
+        self._ck(self._lib.kpm_step_traffic(self._h, b))
+        return b[0], b[1]
+
     def close(self):
         if getattr(self, "_h", None):
-            _lib.kpm_destroy(self._h)
+            self._lib.kpm_destroy(self._h)
             self._h = None
 
     @property
@@ -186,15 +246,15 @@ class Handle:
         return self._h
 
     def set_stream(self, stream_ptr: int):
-        _check(_lib.kpm_set_stream(self._h, ctypes.c_void_p(int(stream_ptr))))
+        self._ck(self._lib.kpm_set_stream(self._h, ctypes.c_void_p(int(stream_ptr))))
 
     def workspace_size(self, N, R, flags=0):
         n = ctypes.c_size_t()
-        _check(_lib.kpm_workspace_size(self._h, int(N), int(R), int(flags), ctypes.byref(n)))
+        self._ck(self._lib.kpm_workspace_size(self._h, int(N), int(R), int(flags), ctypes.byref(n)))
         return n.value
 
     def set_workspace(self, dev_ptr: int, nbytes: int):
-        _check(_lib.kpm_set_workspace(self._h, ctypes.c_void_p(int(dev_ptr)) if dev_ptr else None, int(nbytes)))
+        self._ck(self._lib.kpm_set_workspace(self._h, ctypes.c_void_p(int(dev_ptr)) if dev_ptr else None, int(nbytes)))
 
     def r_local(self, R):
         if self.dist is not None and self.dist[0] == KPM_PART_ROWS and len(self.dist) > 6 and self.dist[6] > 1:
@@ -206,7 +266,7 @@ class Handle:
 
     def moments(self, N, R, seed):
         mu = np.zeros(int(N), dtype=np.float64)
-        _check(_lib.kpm_moments(self._h, int(N), int(R), int(seed), _ptr(mu)))
+        self._ck(self._lib.kpm_moments(self._h, int(N), int(R), int(seed), _ptr(mu)))
         return mu
 
     def moments_ex(self, N, R, seed, r0=None, flags=0, out=None):
@@ -229,37 +289,37 @@ class Handle:
             assert keep.shape == (R_loc, self.D_local), (keep.shape, (R_loc, self.D_local))
             r0p = _ptr(keep)
         if isinstance(out, (int, np.integer)):
-            _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags),
+            self._ck(self._lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags),
                                        ctypes.c_void_p(int(out))))
             return None
         shape = (R_loc, int(N)) if flags & (KPM_PER_VECTOR | KPM_LOCAL) else (int(N),)
         res = np.zeros(shape, dtype=np.float64)
-        _check(_lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags), _ptr(res)))
+        self._ck(self._lib.kpm_moments_ex(self._h, int(N), int(R), int(seed), r0p, int(flags), _ptr(res)))
         return res
 
     def moments_local(self, N, sites):
         sites = np.ascontiguousarray(sites, dtype=np.int64)
         _, n_loc = self.r_local(len(sites))
         res = np.zeros((n_loc, int(N)), dtype=np.float64)
-        _check(_lib.kpm_moments_local(self._h, int(N), _ptr(sites), len(sites), _ptr(res)))
+        self._ck(self._lib.kpm_moments_local(self._h, int(N), _ptr(sites), len(sites), _ptr(res)))
         return res
 
     def assemble(self, S, N, R, flags=0, out=None):
         """Raw sums -> moments (kpm_assemble); S: host array, or int device pointer with out."""
         if isinstance(S, (int, np.integer)):
-            _check(_lib.kpm_assemble(self._h, ctypes.c_void_p(int(S)), int(N), self.D, int(R),
+            self._ck(self._lib.kpm_assemble(self._h, ctypes.c_void_p(int(S)), int(N), self.D, int(R),
                                      int(flags) | KPM_DEVICE_OUT, ctypes.c_void_p(int(out))))
             return None
         return kpm_assemble_host(S, N, self.D, R, flags)
 
     def last_timing(self):
         ms, sl, tl = ctypes.c_double(), ctypes.c_int32(), ctypes.c_int32()
-        _check(_lib.kpm_last_timing(self._h, ctypes.byref(ms), ctypes.byref(sl), ctypes.byref(tl)))
+        self._ck(self._lib.kpm_last_timing(self._h, ctypes.byref(ms), ctypes.byref(sl), ctypes.byref(tl)))
         return ms.value, sl.value, tl.value
 
     def plan_info(self, N, R, flags=0):
         info = np.zeros(12, dtype=np.int64)
-        _check(_lib.kpm_plan_info(self._h, int(N), int(R), int(flags), _ptr(info)))
+        self._ck(self._lib.kpm_plan_info(self._h, int(N), int(R), int(flags), _ptr(info)))
         keys = ["tma", "TL", "TX", "TY", "ctas", "smem", "lanes", "_", "TX2", "ctas_per_sm2", "grid2"]
         d = {k: int(v) for k, v in zip(keys, info) if k != "_"}
         d["round_robin"] = int(info[7] & 1)
@@ -274,13 +334,13 @@ class Handle:
     def last_stats(self):
         """step launches, all launches, halo plane copies, fused-halo launches of the last call"""
         st = np.zeros(4, dtype=np.int64)
-        _check(_lib.kpm_last_stats(self._h, _ptr(st)))
+        self._ck(self._lib.kpm_last_stats(self._h, _ptr(st)))
         return dict(step_launches=int(st[0]), launches=int(st[1]), halo_copies=int(st[2]), fused_halo=int(st[3]))
 
     def step_bytes(self):
         """Algorithmic HBM bytes of the recursion-step launches of the last call."""
         b = ctypes.c_double()
-        _check(_lib.kpm_step_bytes(self._h, ctypes.byref(b)))
+        self._ck(self._lib.kpm_step_bytes(self._h, ctypes.byref(b)))
         return b.value
 
 
@@ -398,10 +458,12 @@ def kpm_nccl_unique_id() -> bytes:
 
 
 def kpm_moments_group(handles, N, R, seed):
-    """KPM_COMM_LOCAL row partition: all slab handles of this process in lock step."""
+    """KPM_COMM_LOCAL partitions: all rank handles of this process (row partition: slabs in lock
+    step with halo exchange; vector partition: every rank's share, sums combined in rank order)."""
     arr = (ctypes.c_void_p * len(handles))(*[h.raw for h in handles])
     mu = np.zeros(int(N), dtype=np.float64)
-    _check(_lib.kpm_moments_group(arr, len(handles), int(N), int(R), int(seed), _ptr(mu)))
+    lib = handles[0]._lib
+    _check(lib.kpm_moments_group(arr, len(handles), int(N), int(R), int(seed), _ptr(mu)), lib)
     return mu
 
 
@@ -483,12 +545,18 @@ def kpm_destroy(h: Handle):
 
 
 def moments_distributed(h, N, R, seed, group=None, flags=0, device=None):
-    """Random-vector partition across ranks (one process per GPU): each rank runs its
-    share of the R vectors (global vector indices, so the vector set does not depend on
-    the number of ranks), the raw sums S[N] are summed over ranks with ONE all-reduce
-    (torch.distributed; NCCL over NVLink on GPUs), then assembled into mu.
-    device: torch device for the sums (default: the current CUDA device; a CPU device
-    uses host sums, e.g. with the gloo backend)."""
+    """Random-vector partition across ranks (one process per GPU).
+
+    A handle created with dist = (KPM_PART_VECTORS, rank, world, KPM_COMM_NCCL, nccl_id) owns
+    the collective: kpm_moments runs this rank's share of the R vectors and the library's one
+    ncclAllReduce of the sums, and returns mu on every rank -- this function only marshals.
+    A handle without a library communicator (KPM_COMM_SELF, e.g. ranks that share one GPU,
+    where NCCL refuses duplicate devices) gets the caller-owned form of the same collective:
+    raw sums (KPM_RAW_SUMS), one torch.distributed all-reduce (gloo or NCCL), kpm_assemble.
+    device: torch device for the sums in that form (default: the current CUDA device)."""
+    d = getattr(h, "dist", None)
+    if d is not None and len(d) > 3 and d[3] == KPM_COMM_NCCL and not flags:
+        return h.moments(N, R, seed)
     import torch
     import torch.distributed as dist
     if device is None:

@@ -33,7 +33,7 @@ hs = [kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["
                              device=rk % ndev, dist=(kpm.KPM_PART_ROWS, rk, G, kpm.KPM_COMM_LOCAL)) for rk in range(G)]
 res = {}
 for mode in ("0", "1"):
-    os.environ["KPM_NO_FUSED_HALO"] = mode
+    hs[0].set_plan_opts(no_fused_halo=int(mode))
     t, mu = timed(lambda: kpm.kpm_moments_group(hs, N, R, seed))
     res["fused" if mode == "0" else "copies"] = (t, float(abs(mu - mu_whole).max()), hs[0].last_stats())
 print({"config": sys.argv[1] if len(sys.argv) > 1 else "c3", "slabs": G, "devices": ndev, "whole_ms": t_whole, **res})

@@ -83,16 +83,15 @@ LOCAL_CASES = {
 
 @pytest.mark.parametrize("path", ["default", "no_small"])
 @pytest.mark.parametrize("case", sorted(LOCAL_CASES))
-def test_local_moments_match_oracle(kpm, case, path, monkeypatch):
+def test_local_moments_match_oracle(kpm, case, path):
     """KPM_LOCAL: unit start vectors e_i generated on the GPU; every launch path (single-launch
     smem, first step + TMA march / two-step / generic step kernels)."""
-    if path == "no_small":
-        monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat, N, sites = LOCAL_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
     ref = oracle.local_moments(H, a, b, sites, N)
     h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"])
+    h.set_plan_opts(no_small=int(path == "no_small"))
     lm = h.moments_local(N, sites)
     assert lm.shape == (len(sites), N)
     assert rel(lm, ref) < 1e-10

@@ -2,8 +2,6 @@
 seeded inputs.  Bar (X17): normwise max_n |mu_gpu - mu_orc| <= 1e-10 *
 max_n |mu_orc|; bitwise for config c1 (every a_n is integer-valued, Q4) and for the
 Rademacher generator (integer work)."""
-import os
-
 import numpy as np
 import pytest
 
@@ -26,13 +24,18 @@ def normwise(a, b):
     return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(b).max(), 1e-300)
 
 
-def make(kpm, lat, a, b, form="stencil"):
+def make(kpm, lat, a, b, form="stencil", **opts):
+    """A handle for lattice lat (stencil descriptor or the same H as CSR) with plan options opts
+    (kpm_plan_opts fields, e.g. no_small=1)."""
     if form == "stencil":
-        return kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"],
-                                      flux=lat["flux"])
-    H = oracle.lattice_csr(lat)
-    val = H.val_re + 1j * H.val_im if H.is_complex else H.val_re
-    return kpm.kpm_create_csr(H.D, H.rowptr, H.col, val, a, b)
+        h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"])
+    else:
+        H = oracle.lattice_csr(lat)
+        val = H.val_re + 1j * H.val_im if H.is_complex else H.val_re
+        h = kpm.kpm_create_csr(H.D, H.rowptr, H.col, val, a, b)
+    if opts:
+        h.set_plan_opts(**opts)
+    return h
 
 
 def lat_of(ndim, L, t=-1.0, W=0.0, flux=0.0, dseed=5):
@@ -57,11 +60,9 @@ CASES = {
 @pytest.mark.parametrize("path", ["default", "no_small"])
 @pytest.mark.parametrize("form", ["stencil", "csr"])
 @pytest.mark.parametrize("case", sorted(CASES))
-def test_moments_match_oracle(kpm, case, form, path, monkeypatch):
+def test_moments_match_oracle(kpm, case, form, path):
     """default: these sizes run the single-launch shared-memory path (kpm_small.cuh);
     no_small: the per-step launch path (first-step + generic/ELL step kernels)."""
-    if path == "no_small":
-        monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat, N, R = CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -69,7 +70,7 @@ def test_moments_match_oracle(kpm, case, form, path, monkeypatch):
     a *= 1.06
     r = ki.rademacher(11, R, lat["D"])
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b, form)
+    h = make(kpm, lat, a, b, form, no_small=int(path == "no_small"))
     mu = h.moments(N, R, 11)
     assert normwise(mu, ref) < TOL
     mu_r0 = h.moments_ex(N, R, 11, r0=r)
@@ -95,8 +96,7 @@ TMA_CASES = {
 
 
 @pytest.mark.parametrize("case", sorted(TMA_CASES))
-def test_tma_march_matches_oracle(kpm, case, monkeypatch):
-    monkeypatch.setenv("KPM_NO_SMALL", "1")  # some of these fit the single-launch smem path
+def test_tma_march_matches_oracle(kpm, case):
     lat, N, R = TMA_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
@@ -104,13 +104,13 @@ def test_tma_march_matches_oracle(kpm, case, monkeypatch):
     a *= 1.05
     r = ki.rademacher(21, R, lat["D"])
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b)
+    h = make(kpm, lat, a, b, no_small=1)  # some of these fit the single-launch smem path
     info = h.plan_info(N, R)
     assert info["tma"] == 1, info
     assert info["round_robin"] == (case == "3d_round_robin"), info
     if lat["ndim"] == 2:
         assert info["two_step"] == (lat["L"][0] % (1024 // info["TL"]) == 0), info
-    else:  # the 3D two-step kernel (kpm_tma32.cuh) is opt-in
+    else:  # the 3D two-step kernel (kpm_tma32.cuh) is experimental (libkpm_exp.so)
         assert info["two_step"] == info["two_step3d"] == 0, info
     mu = h.moments(N, R, 21)
     assert normwise(mu, ref) < TOL
@@ -120,28 +120,21 @@ def test_tma_march_matches_oracle(kpm, case, monkeypatch):
     assert np.array_equal(h.moments_ex(N, R, 21, r0=r), mu)
     if lat["ndim"] == 3:  # dense-box kernel (kpm_tma3.cuh) vs the generic-tile march kernel
         assert info["box3"] == ((info["TX"], info["TY"], info["TL"]) in [(16, 8, 8), (8, 8, 16), (4, 8, 32)]), info
-        monkeypatch.setenv("KPM_TMA32", "1")  # opt-in 3D two-step kernel
-        assert h.plan_info(N, R)["two_step3d"] == 1
-        assert normwise(h.moments(N, R, 21), ref) < TOL
-        monkeypatch.delenv("KPM_TMA32")
-        monkeypatch.setenv("KPM_NO_TMA3", "1")
+        h.set_plan_opts(no_small=1, no_box3=1)
         assert h.plan_info(N, R)["box3"] == 0
         assert normwise(h.moments(N, R, 21), ref) < TOL
 
 
 @pytest.mark.parametrize("tl", [8, 16, 32])
-def test_3d_box_kernel_every_tile_width(kpm, tl, monkeypatch):
+def test_3d_box_kernel_every_tile_width(kpm, tl):
     """The 3D dense-box kernel for each instantiated tile (TL = 8, 16, 32 lanes per site; the
-    plan's TL forced by KPM_TMA_TL), on-site disorder, round-robin columns, vs the oracle."""
-    monkeypatch.setenv("KPM_NO_SMALL", "1")
-    monkeypatch.setenv("KPM_TMA_TL", str(tl))
-    monkeypatch.setenv("KPM_NO_TMA32", "1")  # every step through the single-step kernel
+    plan's TL pinned by kpm_plan_opts.tma_lanes), on-site disorder, round-robin columns, vs the oracle."""
     lat = lat_of(3, (32, 24, 10), W=2.0)
     N, R = 23, 64
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
     ref = oracle.moments_doubling(H, a, b, ki.rademacher(6, R, lat["D"]), N)
-    h = make(kpm, lat, a, b)
+    h = make(kpm, lat, a, b, no_small=1, tma_lanes=tl)
     info = h.plan_info(N, R)
     assert info["TL"] == tl and info["box3"] == 1, info
     assert normwise(h.moments(N, R, 6), ref) < TOL
@@ -149,109 +142,24 @@ def test_3d_box_kernel_every_tile_width(kpm, tl, monkeypatch):
 
 @pytest.mark.parametrize("case", [c for c in sorted(TMA_CASES) if c.startswith("2d")])
 @pytest.mark.parametrize("N", [5, 6, 7, 8, 9])
-def test_two_step_pairs_and_single_steps(kpm, case, N, monkeypatch):
+def test_two_step_pairs_and_single_steps(kpm, case, N):
     """2D: the two-step kernel (temporal blocking) and the single-step kernel give the oracle's
     moments for every parity of the step count and of N (odd-N tail inside a pair)."""
-    monkeypatch.setenv("KPM_NO_SMALL", "1")
     lat, _, R = TMA_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
     ref = oracle.moments_doubling(H, a, b, ki.rademacher(5, R, lat["D"]), N)
-    h = make(kpm, lat, a, b)
+    h = make(kpm, lat, a, b, no_small=1)
     info = h.plan_info(N, R)
     assert info["two_step"] == (N // 2 - 1 >= 2 and lat["L"][0] % (1024 // info["TL"]) == 0)
     mu2 = h.moments(N, R, 5)
-    for xw in ("0", "1"):  # with and without the halo warp
-        monkeypatch.setenv("KPM_TMA2_XW", xw)
+    for xw in (1, 2):  # with and without the halo warp
+        h.set_plan_opts(no_small=1, halo_warp=xw)
         assert normwise(h.moments(N, R, 5), ref) < TOL
-    monkeypatch.setenv("KPM_NO_TMA2", "1")
+    h.set_plan_opts(no_small=1, no_two_step=1)
     assert h.plan_info(N, R)["two_step"] == 0
     mu1 = h.moments(N, R, 5)
     assert normwise(mu2, ref) < TOL and normwise(mu1, ref) < TOL
-
-
-THREE_D_TWO_STEP_CASES = {
-    "anderson_rr": (lat_of(3, (64, 32, 6), W=2.0), 64),          # 4 lane groups x 32 pencils: round-robin
-    "clean_rr": (lat_of(3, (64, 64, 5)), 48),                    # 3 lane groups, no on-site array
-    "anderson_contig": (lat_of(3, (16, 16, 10), W=2.0), 32),     # 8 columns -> contiguous plane ranges
-    "single_pencil_L2_2": (lat_of(3, (16, 8, 2), W=1.0), 16),    # z wraps onto itself, H = 1 segments
-    "one_pencil_wide_R": (lat_of(3, (8, 8, 9), W=1.0), 128),     # 8 lane groups of one pencil
-}
-
-
-@pytest.mark.parametrize("shape", [0, 1, 2, 3])
-@pytest.mark.parametrize("case", sorted(THREE_D_TWO_STEP_CASES))
-@pytest.mark.parametrize("N", [6, 7, 8, 9, 12, 15])
-def test_3d_two_step_kernel_matches_oracle(kpm, case, N, shape, monkeypatch):
-    """3D temporal blocking (kpm_tma32.cuh, opt-in KPM_TMA32=1) for every instantiated tile
-    (KPM_TMA32_SHAPE: 8x8 sites x 8 lanes, 16x4x8, 8x4x16, 16x8x8) and every parity of the step count and of N, vs
-    the oracle and vs the single-step dense-box kernel."""
-    monkeypatch.setenv("KPM_NO_SMALL", "1")
-    monkeypatch.setenv("KPM_TMA32", "1")  # opt-in kernel
-    monkeypatch.setenv("KPM_TMA32_SHAPE", str(shape))
-    lat, R = THREE_D_TWO_STEP_CASES[case]
-    H = oracle.lattice_csr(lat)
-    a, b = oracle.gershgorin(H)
-    b += 0.02 * a
-    a *= 1.03
-    r = ki.rademacher(8, R, lat["D"])
-    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b)
-    info = h.plan_info(N, R)
-    tx, ty, tl = {0: (8, 8, 8), 1: (16, 4, 8), 2: (8, 4, 16), 3: (16, 8, 8)}[shape]
-    fits = (lat["L"][0] % tx == 0 and lat["L"][1] % ty == 0 and ((R + 1) // 2) % tl == 0)
-    assert info["two_step3d"] == int(N // 2 - 1 >= 2 and fits), info
-    mu = h.moments(N, R, 8)
-    assert normwise(mu, ref) < TOL
-    pv = h.moments_ex(N, R, 8, flags=kpm.KPM_PER_VECTOR)
-    assert normwise(pv, ref_pv) < TOL
-    assert np.array_equal(h.moments(N, R, 8), mu), "not deterministic"
-    assert np.array_equal(h.moments_ex(N, R, 8, r0=r), mu)
-    monkeypatch.setenv("KPM_NO_TMA32", "1")
-    assert normwise(h.moments(N, R, 8), ref) < TOL
-
-
-KSTEP_CASES = {
-    "2d_R64": (lat_of(2, (64, 200)), 64),                        # segments cross pencil columns
-    "2d_anderson_R16": (lat_of(2, (128, 24), W=2.0), 16),        # 8 lanes per site: TL 8, TX 64
-    "2d_peierls_R32": (lat_of(2, (64, 16), flux=1 / 8), 32),
-    "2d_peierls_anderson_R16": (lat_of(2, (32, 30), flux=1 / 4, W=1.0), 16),
-    "2d_one_row_per_cta": (lat_of(2, (32, 4)), 32),              # 8 output rows -> 8 CTAs, H = 1
-    "2d_L1_2": (lat_of(2, (64, 2), W=1.0), 48),                  # rows wrap around several times
-    "2d_R96_two_groups": (lat_of(2, (96, 40)), 96),              # 3 pencils x 3 lane groups
-}
-
-
-@pytest.mark.parametrize("ks", [3, 4])
-@pytest.mark.parametrize("case", sorted(KSTEP_CASES))
-@pytest.mark.parametrize("N", [10, 11, 12, 13, 16, 19, 26])
-def test_multi_step_kernel_matches_oracle(kpm, case, N, ks, monkeypatch):
-    """2D: the KS-step (default KS = 3) deep temporal-blocking kernel (kpm_tmak.cuh) mixed with two-step and
-    single-step launches for the remainder, every parity of N (odd-N tail in the last launch)."""
-    monkeypatch.setenv("KPM_NO_SMALL", "1")
-    monkeypatch.setenv("KPM_TMAK_KS", str(ks))  # opt-in kernel
-    lat, R = KSTEP_CASES[case]
-    H = oracle.lattice_csr(lat)
-    a, b = oracle.gershgorin(H)
-    b -= 0.02 * a
-    a *= 1.03
-    r = ki.rademacher(13, R, lat["D"])
-    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b)
-    info = h.plan_info(N, R)
-    assert info["ks"] == ks, info
-    mu = h.moments(N, R, 13)
-    assert normwise(mu, ref) < TOL
-    pv = h.moments_ex(N, R, 13, flags=kpm.KPM_PER_VECTOR)
-    assert normwise(pv, ref_pv) < TOL
-    assert np.array_equal(h.moments(N, R, 13), mu), "not deterministic"
-    _, launches, _ = h.last_timing()
-    M = N // 2
-    rem = (M - 1) % ks
-    assert launches == (M - 1) // ks + (rem // 2 + rem % 2 if info["two_step"] else rem), (launches, info)
-    monkeypatch.delenv("KPM_TMAK_KS")
-    assert h.plan_info(N, R)["ks"] == 0
-    assert normwise(h.moments(N, R, 13), ref) < TOL
 
 
 @pytest.mark.parametrize("case", ["2d", "3d_anderson", "peierls"])
@@ -281,14 +189,12 @@ def test_c1_bitwise(kpm):
 @pytest.mark.parametrize("path", ["default", "no_small"])
 @pytest.mark.parametrize("N", [1, 2, 3, 4, 5, 8, 9])
 @pytest.mark.parametrize("R", [1, 2, 3])
-def test_small_N_and_R_edges(kpm, N, R, path, monkeypatch):
-    if path == "no_small":
-        monkeypatch.setenv("KPM_NO_SMALL", "1")
+def test_small_N_and_R_edges(kpm, N, R, path):
     lat = lat_of(2, (9, 7), W=1.0)
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
     ref = oracle.moments_doubling(H, a, b, ki.rademacher(9, R, lat["D"]), N)
-    mu = make(kpm, lat, a, b).moments(N, R, 9)
+    mu = make(kpm, lat, a, b, no_small=int(path == "no_small")).moments(N, R, 9)
     assert mu.shape == (N,) and normwise(mu, ref) < TOL
 
 
@@ -362,7 +268,7 @@ ROW_CASES = {
 
 @pytest.mark.parametrize("comm", ["self", "nccl"])
 @pytest.mark.parametrize("case", sorted(ROW_CASES))
-def test_row_partition_world1_matches_oracle(kpm, case, comm, monkeypatch):
+def test_row_partition_world1_matches_oracle(kpm, case, comm):
     """KPM_PART_ROWS with one rank: slab + ghost planes refreshed after every step (a local
     copy, or NCCL send/recv to itself), moment sums through the NCCL all-reduce."""
     lat, N, R = ROW_CASES[case]
@@ -385,7 +291,7 @@ def test_row_partition_world1_matches_oracle(kpm, case, comm, monkeypatch):
     whole = make(kpm, lat, a, b).moments(N, R, 8)
     assert normwise(mu, whole) < 1e-13
     if info["overlap"]:  # boundary planes + exchange on the comm stream + interior, vs serialised
-        monkeypatch.setenv("KPM_NO_OVERLAP", "1")
+        h.set_plan_opts(no_overlap=1)
         assert h.plan_info(N, R)["overlap"] == 0
         assert normwise(h.moments(N, R, 8), mu) < 1e-13
 
@@ -393,18 +299,18 @@ def test_row_partition_world1_matches_oracle(kpm, case, comm, monkeypatch):
 @pytest.mark.parametrize("fused", ["1", "0"])
 @pytest.mark.parametrize("world", [1, 2, 3, 4])
 @pytest.mark.parametrize("case", ["1d", "2d_tma", "2d_peierls_tma", "3d_simple", "3d_tma"])
-def test_row_partition_local_group_matches_oracle(kpm, case, world, fused, monkeypatch):
+def test_row_partition_local_group_matches_oracle(kpm, case, world, fused):
     """KPM_COMM_LOCAL: `world` slab handles in one process (one GPU) exchange halo planes
     after every step; uneven slabs included.  Same global vectors as one whole lattice.
     fused = 1: the TMA march kernels store their boundary planes straight into the neighbours'
     ghost planes (peer memory, no copy step); fused = 0: plane copies between launches."""
-    monkeypatch.setenv("KPM_NO_FUSED_HALO", "0" if fused == "1" else "1")
     lat, N, R = ROW_CASES[case]
     H = oracle.lattice_csr(lat)
     a, b = oracle.gershgorin(H)
     ref = oracle.moments_doubling(H, a, b, ki.rademacher(8, R, lat["D"]), N)
     hs = [kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
                                  dist=(kpm.KPM_PART_ROWS, rk, world, kpm.KPM_COMM_LOCAL)) for rk in range(world)]
+    hs[0].set_plan_opts(no_fused_halo=int(fused == "0"))
     mu = kpm.kpm_moments_group(hs, N, R, 8)
     assert normwise(mu, ref) < TOL
     st = hs[0].last_stats()
@@ -412,34 +318,6 @@ def test_row_partition_local_group_matches_oracle(kpm, case, world, fused, monke
     on = fused == "1" and tma  # the fused halo needs the TMA march kernels
     assert st["fused_halo"] == (st["step_launches"] if on else 0), st
     assert st["halo_copies"] == (2 if on else 2 * (st["step_launches"] + 1)), st  # + the first step's copies
-
-
-PERSIST_CASES = dict(**{k: v for k, v in CASES.items()}, **{"tma_" + k: v for k, v in TMA_CASES.items()})
-
-
-@pytest.mark.parametrize("form", ["stencil", "csr"])
-@pytest.mark.parametrize("case", sorted(PERSIST_CASES))
-def test_persistent_kernel_matches_oracle(kpm, case, form, monkeypatch):
-    """The whole recursion in one cooperative launch with grid-wide barriers between steps
-    (kpm_persist.cuh, L2-resident blocks): same moments as the oracle, per vector too, with
-    generated and caller-supplied start vectors, deterministic."""
-    monkeypatch.delenv("KPM_NO_PERSIST", raising=False)
-    monkeypatch.setenv("KPM_PERSIST", "1")  # opt-in (any size that is co-resident)
-    monkeypatch.setenv("KPM_NO_SMALL", "1")
-    lat, N, R = PERSIST_CASES[case]
-    H = oracle.lattice_csr(lat)
-    a, b = oracle.gershgorin(H)
-    b -= 0.02 * a
-    a *= 1.04
-    r = ki.rademacher(12, R, lat["D"])
-    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b, form)
-    assert h.plan_info(N, R)["persist"] == int(N // 2 >= 2), h.plan_info(N, R)
-    mu = h.moments(N, R, 12)
-    assert normwise(mu, ref) < TOL
-    assert normwise(h.moments_ex(N, R, 12, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
-    assert np.array_equal(h.moments_ex(N, R, 12, r0=r), mu)
-    assert np.array_equal(h.moments(N, R, 12), mu), "not deterministic"
 
 
 def random_sparse_hermitian(D, deg, seed, cplx):
@@ -563,11 +441,9 @@ def test_randomized_shapes_sweep(kpm):
         R = int(rng.choice([1, 3, 8, 16, 32, 64]))
         N = int(rng.integers(1, 40))
         lat = lat_of(ndim, L, W=W, flux=flux, dseed=trial)
-        os.environ["KPM_NO_SMALL"] = "1" if trial % 2 else "0"  # both launch paths
         H = oracle.lattice_csr(lat)
         a, b = oracle.gershgorin(H)
         a *= 1.0 + 0.1 * rng.random()
         ref = oracle.moments_doubling(H, a, b, ki.rademacher(trial, R, lat["D"]), N)
-        mu = make(kpm, lat, a, b).moments(N, R, trial)
+        mu = make(kpm, lat, a, b, no_small=trial % 2).moments(N, R, trial)  # both launch paths
         assert normwise(mu, ref) < TOL, (trial, ndim, L, flux, W, R, N)
-    os.environ.pop("KPM_NO_SMALL", None)
