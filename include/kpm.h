@@ -233,7 +233,11 @@ typedef struct {
                               (exp_param = tile shape 0..3), 2 = KS-steps-per-launch 2D kernel
                               (exp_param = KS, 3 or 4), 3 = persistent L2-resident kernel */
     int32_t exp_param;
-    int32_t reserved[7];   /* must be 0 */
+    int32_t two_step_ctas; /* two-step kernel CTAs per SM (0 = automatic; 2 only for the 4-lane,
+                              64-site tile, else 1) */
+    int32_t no_pdl;        /* 1: plain stream-ordered launches instead of programmatic dependent
+                              launches (PDL: the next kernel's prologue overlaps this one's tail) */
+    int32_t reserved[5];   /* must be 0 */
 } kpm_plan_opts;
 
 /* Set (opts != NULL) or reset to the default (opts == NULL) the plan options of h.

@@ -247,6 +247,27 @@ kpm_status sync_stream(kpm_handle_s* h) {
     return nccl_poll(h);
 }
 
+// One kernel of the kpm_moments chain on stream st, with programmatic stream serialization (PDL)
+// unless the plan switches it off: the kernel may launch while its predecessor in the stream is
+// still running and waits for it in pdl_entry() (kpm_kernels.cuh) before touching global memory.
+template <class... Exp, class... Act>
+kpm_status launch_k(kpm_handle_s* h, cudaStream_t st, void (*kern)(Exp...), dim3 grid, dim3 block, size_t smem,
+                    Act&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = h->opts.no_pdl ? 0 : 1;
+    KPM_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Act>(args)...));
+    h->total_launches++;
+    return KPM_OK;
+}
+
 // Communicator of a KPM_COMM_NCCL partition, from the caller's broadcast ncclUniqueId (shared
 // with earlier handles of the same id, rank, world and device).
 kpm_status init_comm(kpm_handle_s* h, const kpm_dist* dist) {
@@ -355,9 +376,11 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     // (DRAM locality of the TMA box rows; with the dense-box kernel, kpm_tma3.cuh)
     // 2D real: 16 lanes first -- c2 25.35 vs 26.13 ms per call with 32 (same box, A/B); 2D complex:
     // 32 first -- c4 3114 vs 3166-3274 ms with 16
-    const int cands2r[3] = {16, 32, 8}, cands2c[3] = {32, 16, 8}, cands3[3] = {16, 32, 8};
+    // 2D: 4 lanes per site when RG is not a multiple of 8 (e.g. c2 at 8 GPUs: R = 8 real vectors per
+    // GPU, an L2-resident block -- SURVEY.md 8(e) P1 strong scaling)
+    const int cands2r[4] = {16, 32, 8, 4}, cands2c[4] = {32, 16, 8, 4}, cands3[4] = {16, 32, 8, 0};
     for (int c : (h->ndim == 2 ? (is_cplx(h) ? cands2c : cands2r) : cands3))
-        if (RG % c == 0) { TL = c; break; }
+        if (c && RG % c == 0) { TL = c; break; }
     const int tl_opt = h->opts.tma_lanes;  // pinned lanes per tile site (A/B, tests)
     if (tl_opt > 0 && RG % tl_opt == 0) TL = tl_opt;
     if (!TL) return;
@@ -409,12 +432,19 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     p->use_tma2 = false;
     if (h->ndim == 2 && !p->no_fused && !h->opts.no_two_step && h->L[0] >= 4 && h->L[1] >= 4) {
         const bool on = h->d_eps != nullptr;
-        const int tx1 = 1024 / TL;
+        int tx1 = 1024 / TL, minb = 1;
+        // 4 lanes per site: the 64-site tile (2 CTAs per SM) when the 256-site tile would leave a CTA
+        // fewer than 32 rows to march (per-segment pipeline fill dominates short segments)
+        if (TL == 4 && (h->L[0] % tx1 || (long long)(RG / TL) * (h->L[0] / tx1) * h->L[1] < 32LL * h->num_sms)) {
+            tx1 = 64;
+            minb = 2;
+        }
+        if (h->opts.two_step_ctas > 0) minb = std::min(h->opts.two_step_ctas, tx1 == 64 && TL == 4 ? 2 : 1);
         const size_t sm1 = kpm::step2_smem_bytes(tx1, TL, on, p->RP);
         const long long Lm2 = h->L[1];
         if (h->L[0] % tx1 == 0 && sm1 <= 227 * 1024) {
             p->TX2 = tx1;
-            p->tma2_minb = 1;
+            p->tma2_minb = minb;
             p->tma2_smem = sm1;
         }
         if (p->TX2) {
@@ -565,10 +595,7 @@ template <int MODE, bool CPLX, class OP>
 kpm_status launch_step(kpm_handle_s* h, const Plan& p, const OP& op, const kpm::VecArgs& v, int tail) {
     dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
     const size_t smem = 3 * (size_t)kThreads * sizeof(double2);
-    kpm::kpm_step_kernel<OP, MODE, CPLX><<<grid, block, smem, h->stream>>>(op, v, tail);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    return KPM_OK;
+    return launch_k(h, h->stream, kpm::kpm_step_kernel<OP, MODE, CPLX>, grid, block, smem, op, v, tail);
 }
 
 template <bool CPLX, class OP>
@@ -604,10 +631,7 @@ kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, i
     auto kern = kpm::kpm_ell_step_kernel<CPLX>;
     KPM_TRY(set_smem((const void*)kern, smem, h->device));
     const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a};
-    kern<<<grid, block, smem, h->stream>>>(op, v, tail);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    return KPM_OK;
+    return launch_k(h, h->stream, kern, grid, block, smem, op, v, tail);
 }
 
 template <bool CPLX, class OP>
@@ -615,10 +639,7 @@ kpm_status launch_small_t(kpm_handle_s* h, const Plan& p, const OP& op, const kp
                           double* part) {
     auto kern = kpm::kpm_small_kernel<OP, CPLX>;
     KPM_TRY(set_smem((const void*)kern, p.small_smem, h->device));
-    kern<<<dim3(1, p.gy), dim3(p.TR, p.TS), p.small_smem, h->stream>>>(op, v, from_buf, N, part);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    return KPM_OK;
+    return launch_k(h, h->stream, kern, dim3(1, p.gy), dim3(p.TR, p.TS), p.small_smem, op, v, from_buf, N, part);
 }
 
 kpm_status launch_small(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int from_buf, int N, double* part) {
@@ -835,10 +856,10 @@ kpm_status launch_tma2_x(kpm_handle_s* h, const Plan& p, const BufMaps& A, const
                          const CUtensorMap& E2, const kpm::Tma2Geom& g, int tail) {
     auto kern = kpm::kpm_step2_tma_kernel<TL, TX, ONSITE, PEIERLS, MINB, XW>;
     KPM_TRY(set_smem((const void*)kern, p.tma2_smem, h->device));
-    kern<<<p.tma2_grid, kpm::Threads2<XW>::N, p.tma2_smem, h->stream>>>(A.A2, A.Col2, P.A2, P.Col, E, E2, g, tail);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    return KPM_OK;
+    // a_{n-1} halo box: 1 site, or 2 when a site is under 128 bytes (kpm_tma2.cuh p_halo)
+    const CUtensorMap& Ph = kpm::p_halo(TL) == 2 ? P.Col2 : P.Col;
+    return launch_k(h, h->stream, kern, dim3(p.tma2_grid), dim3(kpm::Threads2<XW>::N), p.tma2_smem, A.A2, A.Col2, P.A2, Ph,
+                    E, E2, g, tail);
 }
 
 // Halo warp (XW = 1, kpm_tma2.cuh) for complex128 (Peierls) lattices: c4 3178 vs 3387 ms per call;
@@ -871,6 +892,8 @@ kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     if (p.TL == 32 && p.TX2 == 32) return launch_tma2_s<32, 32, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 16 && p.TX2 == 64) return launch_tma2_s<16, 64, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 8 && p.TX2 == 128) return launch_tma2_s<8, 128, 1>(h, p, A, P, E, E2, g, tail);
+    if (p.TL == 4 && p.TX2 == 256) return launch_tma2_s<4, 256, 1>(h, p, A, P, E, E2, g, tail);
+    if (p.TL == 4 && p.TX2 == 64) return launch_tma2_s<4, 64, 2>(h, p, A, P, E, E2, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX2);
 }
 
@@ -971,10 +994,8 @@ kpm_status launch_tma3_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, con
                          const kpm::TmaGeom& g, int tail, int grid) {
     auto kern = kpm::kpm_step3_tma_kernel<TX, TY, TL, ONSITE>;
     KPM_TRY(set_smem((const void*)kern, p.tma_smem, h->device));
-    kern<<<grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.Box3, cur.Row3, prev.P, E, g, tail);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    return KPM_OK;
+    return launch_k(h, h->stream, kern, dim3(grid), dim3(kpm::kTmaThreads), p.tma_smem, cur.Box3, cur.Row3, prev.P, E, g,
+                    tail);
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS>
@@ -982,10 +1003,8 @@ kpm_status launch_tma_t(kpm_handle_s* h, const Plan& p, const BufMaps& cur, cons
                         const kpm::TmaGeom& g, int tail, int grid) {
     auto kern = kpm::kpm_step_tma_kernel<NDIM, ONSITE, PEIERLS>;
     KPM_TRY(set_smem((const void*)kern, p.tma_smem, h->device));
-    kern<<<grid, kpm::kTmaThreads, p.tma_smem, h->stream>>>(cur.A, cur.Col, cur.Row, prev.P, E, g, tail);
-    KPM_CUDA(cudaGetLastError());
-    h->total_launches++;
-    return KPM_OK;
+    return launch_k(h, h->stream, kern, dim3(grid), dim3(kpm::kTmaThreads), p.tma_smem, cur.A, cur.Col, cur.Row, prev.P, E,
+                    g, tail);
 }
 
 kpm_status launch_tma(kpm_handle_s* h, const Plan& p, const BufMaps& cur, const BufMaps& prev, const CUtensorMap& E,
@@ -1207,10 +1226,9 @@ struct Run {
                                      (flags & KPM_DEVICE_IN) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, h->stream));
             const long long ne = h->D * (long long)p.RG;
             const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
-            if (cplx) kpm::load_r0_kernel<true><<<blocks, 256, 0, h->stream>>>(stage, P, v);
-            else kpm::load_r0_kernel<false><<<blocks, 256, 0, h->stream>>>(stage, P, v);
-            KPM_CUDA(cudaGetLastError());
-            h->total_launches++;
+            const double* cstage = stage;
+            if (cplx) KPM_TRY(launch_k(h, h->stream, kpm::load_r0_kernel<true>, dim3(blocks), dim3(256), 0, cstage, P, v));
+            else KPM_TRY(launch_k(h, h->stream, kpm::load_r0_kernel<false>, dim3(blocks), dim3(256), 0, cstage, P, v));
             if (direct) KPM_CUDA(cudaMemcpyAsync(Rb, P, p.mem_sites * p.RG * sizeof(double2), cudaMemcpyDeviceToDevice, h->stream));
             first_mode = kpm::FIRST_BUF;
         }
@@ -1364,9 +1382,7 @@ struct Run {
         if (first_mode != kpm::FIRST_BUF) {
             const long long ne = h->Dp * (long long)p.RG;
             const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
-            kpm::dense_gen_kernel<false><<<blocks, 256, 0, h->stream>>>(v, (int)h->Dp, P);
-            KPM_CUDA(cudaGetLastError());
-            h->total_launches++;
+            KPM_TRY(launch_k(h, h->stream, kpm::dense_gen_kernel<false>, dim3(blocks), dim3(256), 0, v, (int)h->Dp, P));
         }
         v.red0 = part;
         v.red1 = part + slot;  // the partial buffer has >= 3 slots (slot 1 unused when N = 1)
@@ -1396,11 +1412,8 @@ struct Run {
         dim3 grid(p.RP / kpm::kDBN, (unsigned)(h->Dp / kpm::kDBM));
         KPM_TRY(set_smem((const void*)kpm::kpm_dense_step_kernel<true>, kpm::kDenseSmem, h->device));
         KPM_TRY(set_smem((const void*)kpm::kpm_dense_step_kernel<false>, kpm::kDenseSmem, h->device));
-        if (first) kpm::kpm_dense_step_kernel<true><<<grid, kpm::kDThreads, kpm::kDenseSmem, h->stream>>>(g, tail);
-        else kpm::kpm_dense_step_kernel<false><<<grid, kpm::kDThreads, kpm::kDenseSmem, h->stream>>>(g, tail);
-        KPM_CUDA(cudaGetLastError());
-        h->total_launches++;
-        return KPM_OK;
+        if (first) return launch_k(h, h->stream, kpm::kpm_dense_step_kernel<true>, grid, dim3(kpm::kDThreads), kpm::kDenseSmem, g, tail);
+        return launch_k(h, h->stream, kpm::kpm_dense_step_kernel<false>, grid, dim3(kpm::kDThreads), kpm::kDenseSmem, g, tail);
     }
 
     // Row partition, one recursion step with the halo exchange overlapped:
@@ -1468,9 +1481,9 @@ struct Run {
         if (h->n_send) {
             const long long ne = h->n_send * (long long)p.RG;
             const int blocks = (int)std::min<long long>((ne + 255) / 256, 8LL * h->num_sms);
-            kpm::gather_lanes_kernel<<<blocks, 256, 0, st>>>(X, h->d_send, h->n_send, p.RG, sendbuf);
-            KPM_CUDA(cudaGetLastError());
-            h->total_launches++;
+            const double2* cX = X;
+            const int* cidx = h->d_send;
+            KPM_TRY(launch_k(h, st, kpm::gather_lanes_kernel, dim3(blocks), dim3(256), 0, cX, cidx, (long long)h->n_send, p.RG, sendbuf));
         }
         const size_t lb = (size_t)p.RG * sizeof(double2);
         ncclResult_t e = ncclGroupStart();
@@ -1607,10 +1620,8 @@ struct Run {
     kpm_status collect() {
         KPM_TRY(join_comm());
         KPM_CUDA(cudaEventRecord(h->ev_end, h->stream));
-        kpm::finish_kernel<<<N, 256, 0, h->stream>>>(part, p.gx, p.RP, p.R_loc, Sv, S);
-        KPM_CUDA(cudaGetLastError());
-        h->total_launches++;
-        return KPM_OK;
+        const double* cpart = part;
+        return launch_k(h, h->stream, kpm::finish_kernel, dim3(N), dim3(256), 0, cpart, p.gx, p.RP, p.R_loc, Sv, S);
     }
 
     kpm_status output(void* out) {
@@ -1622,10 +1633,9 @@ struct Run {
             out_bytes = (size_t)N * sizeof(double);
         } else if (flags & KPM_PER_VECTOR) {
             const long long ne = (long long)N * p.R_loc;
-            kpm::assemble_pervec_kernel<<<(unsigned)((ne + 255) / 256), 256, 0, h->stream>>>(
-                Sv, N, p.R_loc, local_sites ? 1.0 : 1.0 / (double)h->D_total, direct, dout);
-            KPM_CUDA(cudaGetLastError());
-            h->total_launches++;
+            const double* cSv = Sv;
+            KPM_TRY(launch_k(h, h->stream, kpm::assemble_pervec_kernel, dim3((unsigned)((ne + 255) / 256)), dim3(256), 0, cSv,
+                             N, p.R_loc, local_sites ? 1.0 : 1.0 / (double)h->D_total, (int)direct, dout));
             src = dout;
             out_bytes = (size_t)ne * sizeof(double);
         } else {
@@ -1635,9 +1645,9 @@ struct Run {
                             "multi-rank vector partition without KPM_COMM_NCCL: use KPM_RAW_SUMS, all-reduce, then kpm_assemble");
             // S holds the sums over all R vectors after the all-reduce, else over this rank's R_loc = R
             const double Rn = multi ? (double)R : (double)p.R_loc;
-            kpm::assemble_kernel<<<(N + 255) / 256, 256, 0, h->stream>>>(S, N, 1.0 / ((double)h->D_total * Rn), direct, dout);
-            KPM_CUDA(cudaGetLastError());
-            h->total_launches++;
+            const double* cS = S;
+            KPM_TRY(launch_k(h, h->stream, kpm::assemble_kernel, dim3((N + 255) / 256), dim3(256), 0, cS, N,
+                             1.0 / ((double)h->D_total * Rn), (int)direct, dout));
             src = dout;
             out_bytes = (size_t)N * sizeof(double);
         }
@@ -2569,12 +2579,13 @@ kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
     }
     const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
                          o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
-                         o->no_graph,  o->experimental, o->exp_param};
+                         o->no_graph,  o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl};
     for (int32_t x : f)
         if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
     for (int32_t x : o->reserved)
         if (x != 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: reserved words must be 0");
-    if (o->halo_warp > 2 || o->experimental > 3) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: value out of range");
+    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2)
+        return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: value out of range");
 #ifndef KPM_EXPERIMENTAL
     if (o->experimental) return fail(KPM_ERR_UNSUPPORTED, "experimental kernels are built into libkpm_exp.so only");
 #endif

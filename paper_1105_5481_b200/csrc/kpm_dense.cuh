@@ -60,6 +60,7 @@ struct DenseArgs {
 // FIRST = true: a_1 = H~ a_0 written to P (no recursion term); else Eq (18) in place over P.
 template <bool FIRST>
 __global__ void __launch_bounds__(kDThreads) kpm_dense_step_kernel(const DenseArgs g, const int tail) {
+    pdl_entry();
     extern __shared__ __align__(16) double dsm[];
     double* Hs = dsm;                                // [stage][64][36]
     double* As = dsm + kDStages * kDBM * kDHS;       // [stage][32][68]
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(kDThreads) kpm_dense_step_kernel(const DenseAr
 // RG = RP / 2, D = real number of sites).
 template <bool CPLX>
 __global__ void dense_gen_kernel(const VecArgs v, int Dp, double2* __restrict__ out) {
+    pdl_entry();
     const long long n = (long long)Dp * v.RG;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
         const int s = (int)(e / v.RG), rg = (int)(e % v.RG);

@@ -31,6 +31,7 @@ __host__ __device__ inline size_t ell_smem_bytes(int nthr, int TS, int K, bool c
 
 template <bool CPLX>
 __global__ void __launch_bounds__(512) kpm_ell_step_kernel(const EllOp<CPLX> op, const VecArgs v, const int tail) {
+    pdl_entry();
     const int TR = blockDim.x, TS = blockDim.y;
     const int nthr = TR * TS, tid = threadIdx.y * TR + threadIdx.x;
     const int rg = blockIdx.y * TR + threadIdx.x;

@@ -24,6 +24,17 @@
 
 namespace kpm {
 
+// ------------------------------------------------------------ programmatic dependent launch
+// Every kernel of a kpm_moments call is launched with programmatic stream serialization (PDL,
+// kpm_capi.cu launch_k): it lets the NEXT kernel of the chain launch as soon as every CTA of this
+// one has started (griddepcontrol.launch_dependents), and each kernel waits for its predecessor's
+// completion and memory flush (griddepcontrol.wait) before touching global memory.  The launch
+// latency of step n+1 thus overlaps step n.  Both are no-ops for a kernel launched without PDL.
+__device__ __forceinline__ void pdl_entry() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
 // ------------------------------------------------------------ lane arithmetic
 __device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 scale2(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
@@ -293,6 +304,7 @@ __device__ __forceinline__ void step_body(const OP& op, const VecArgs& v, const 
 
 template <class OP, int MODE, bool CPLX>
 __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArgs v, const int tail) {
+    pdl_entry();
     step_body<OP, MODE, CPLX>(op, v, tail);
 }
 
@@ -300,6 +312,7 @@ __global__ void __launch_bounds__(512) kpm_step_kernel(const OP op, const VecArg
 // Caller start vectors, vector-major [R_loc][D] real -> lane layout [D][RG] (memory sites of v).
 template <bool CPLX>
 __global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restrict__ out, const VecArgs v) {
+    pdl_entry();
     const int D = v.D, RG = v.RG;
     const long long R_loc = v.R_loc;
     const long long n = (long long)D * RG;
@@ -319,6 +332,7 @@ __global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restric
 // dst[k][l] = src[idx[k]][l] over n sites of RG 16-byte lanes (row-partition ghost exchange).
 __global__ void gather_lanes_kernel(const double2* __restrict__ src, const int* __restrict__ idx, long long n, int RG,
                                     double2* __restrict__ dst) {
+    pdl_entry();
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < n * RG; e += (long long)gridDim.x * blockDim.x) {
         const long long k = e / RG;
         dst[e] = src[(long long)__ldg(idx + k) * RG + (e - k * RG)];
@@ -327,25 +341,39 @@ __global__ void gather_lanes_kernel(const double2* __restrict__ src, const int* 
 
 // Sum the CTA partials of every moment slot in a fixed order:
 // Sv[m][v] = sum_c partial[m][c][v] (per vector), S[m] = sum_v Sv[m][v].
+// One block per slot m; its threads form CG groups x VB vector lanes (VB = the power of two >= R_loc,
+// at most 32): group g sums the CTA rows c = g, g + CG, ... of vectors v0 + lane, then the groups are
+// combined by a fixed shared-memory tree.  The partition depends only on (nCTA, R_loc), so repeated
+// calls give identical bits.  (One thread per vector summing all CTA rows serially took 90 us per
+// call at R_loc = 8 on c2.)
 __global__ void finish_kernel(const double* __restrict__ partial, int nCTA, int RP, long long R_loc,
                               double* __restrict__ Sv, double* __restrict__ S) {
+    pdl_entry();
     const int m = blockIdx.x;
     const double* base = partial + (size_t)m * nCTA * RP;
-    double local = 0.0;
-    for (long long v = threadIdx.x; v < R_loc; v += blockDim.x) {
+    int VB = 1;
+    while (VB < R_loc && VB < 32) VB <<= 1;
+    const int CG = blockDim.x / VB;
+    const int lane = threadIdx.x % VB, grp = threadIdx.x / VB;
+    __shared__ double red[256];
+    double total = 0.0;  // thread 0: sum over v in order of chunks
+    for (long long v0 = 0; v0 < R_loc; v0 += VB) {
+        const long long v = v0 + lane;
         double s = 0.0;
-        for (int c = 0; c < nCTA; ++c) s += base[(size_t)c * RP + v];
-        Sv[(size_t)m * R_loc + v] = s;
-        local += s;
-    }
-    __shared__ double red[1024];
-    red[threadIdx.x] = local;
-    __syncthreads();
-    for (int w = blockDim.x / 2; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        if (v < R_loc && grp < CG)
+            for (int c = grp; c < nCTA; c += CG) s += base[(size_t)c * RP + v];
+        red[threadIdx.x] = s;
+        __syncthreads();
+        for (int w = CG / 2; w > 0; w >>= 1) {  // fixed tree over the groups
+            if (grp < w) red[threadIdx.x] += red[threadIdx.x + w * VB];
+            __syncthreads();
+        }
+        if (threadIdx.x < VB && v < R_loc) Sv[(size_t)m * R_loc + v] = red[threadIdx.x];
+        if (threadIdx.x == 0)
+            for (int j = 0; j < VB && v0 + j < R_loc; ++j) total += red[j];
         __syncthreads();
     }
-    if (threadIdx.x == 0) S[m] = red[0];
+    if (threadIdx.x == 0) S[m] = total;
 }
 
 // Doubling transform + normalisation (north_star; Eq 19 for direct):
@@ -358,6 +386,7 @@ __device__ __forceinline__ double assemble_one(const double* S, long long stride
 }
 
 __global__ void assemble_kernel(const double* __restrict__ S, int N, double c, int direct, double* __restrict__ mu) {
+    pdl_entry();
     const int n = blockIdx.x * blockDim.x + threadIdx.x;
     if (n < N) mu[n] = assemble_one(S, 1, n, c, direct);
 }
@@ -365,6 +394,7 @@ __global__ void assemble_kernel(const double* __restrict__ S, int N, double c, i
 // Per-vector moments: pv[v][n] from Sv[n][v].
 __global__ void assemble_pervec_kernel(const double* __restrict__ Sv, int N, long long R_loc, double c, int direct,
                                        double* __restrict__ pv) {
+    pdl_entry();
     const long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (e >= (long long)N * R_loc) return;
     const long long v = e / N;

@@ -18,6 +18,7 @@ constexpr size_t kSmallSmemMax = 200 * 1024;
 template <class OP, bool CPLX>
 __global__ void __launch_bounds__(kSmallThreads, 1)
     kpm_small_kernel(const OP op, const VecArgs v, const int first_from_buf, const int N, double* __restrict__ part) {
+    pdl_entry();
     const int TR = blockDim.x, TS = blockDim.y;
     const int rg = blockIdx.y * TR + threadIdx.x;
     const bool active = rg < v.RG;

@@ -154,19 +154,22 @@ constexpr int kTmaThreads = (kTmaConsumerWarps + 1) * 32;
 constexpr int kSA = KPM_SA;  // a_n ring slots
 constexpr int kSP = KPM_SP;  // a_{n-1} ring slots
 
-// Shared-memory carve-up of one a_n slot: [main TY*TX][left TY][right TY][top TX][bottom TX][eps TX*TY doubles]
+// Shared-memory carve-up of one a_n slot: [main TY*TX][left TY][right TY][top TX][bottom TX][eps TX*TY doubles],
+// every region starting on a 128-byte boundary (TMA destinations; with TL = 4 lanes a 1-site halo
+// column is only 64 bytes).
 struct SlotLayout {
     int site_bytes, main_off, left_off, right_off, top_off, bot_off, eps_off, bytes;
+    __host__ __device__ static int up(int x) { return (x + 127) / 128 * 128; }
     __host__ __device__ SlotLayout(int NDIM, int TX, int TY, int TL, bool onsite) {
         site_bytes = TL * 16;
         main_off = 0;
-        left_off = main_off + TX * TY * site_bytes;
-        right_off = left_off + TY * site_bytes;
-        top_off = right_off + TY * site_bytes;
-        bot_off = top_off + (NDIM == 3 ? TX * site_bytes : 0);
-        eps_off = bot_off + (NDIM == 3 ? TX * site_bytes : 0);
+        left_off = up(main_off + TX * TY * site_bytes);
+        right_off = up(left_off + TY * site_bytes);
+        top_off = up(right_off + TY * site_bytes);
+        bot_off = up(top_off + (NDIM == 3 ? TX * site_bytes : 0));
+        eps_off = up(bot_off + (NDIM == 3 ? TX * site_bytes : 0));
         int end = eps_off + (onsite ? TX * TY * 8 : 0);
-        bytes = (end + 127) / 128 * 128;
+        bytes = up(end);
     }
 };
 
@@ -224,6 +227,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                         const __grid_constant__ CUtensorMap mapP,     // a_{n-1}: main box
                         const __grid_constant__ CUtensorMap mapE,     // eps~: tile box
                         const TmaGeom g, const int tail) {
+    pdl_entry();
     constexpr int CONS = kTmaConsumerWarps * 32;
     extern __shared__ __align__(128) unsigned char smem[];
     const SlotLayout SL(NDIM, g.TX, g.TY, g.TL, ONSITE);

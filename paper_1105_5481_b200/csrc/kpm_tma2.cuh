@@ -54,6 +54,10 @@ constexpr int kSB2 = 3;         // a_{n+1} ring (computed)
 
 // a_n slot: [2 halo sites][TX sites][2 halo sites] then eps~ as three 128-byte aligned
 // pieces (TMA destinations must be 128-byte aligned): [2 left][TX main][2 right].
+// a_{n-1} slot: [PH halo sites][TX sites][PH halo sites], PH = 1 when a site is >= 128 bytes
+// (TL >= 8 lanes), else 2 (TL = 4: the halo box is two sites wide so that the main box lands on
+// a 128-byte boundary; the outer halo site is loaded but not used).
+__host__ __device__ constexpr int p_halo(int TL) { return TL * 16 >= 128 ? 1 : 2; }
 struct Slot2Layout {
     int site, a_bytes, eps_l, eps_m, eps_r, p_bytes, b_bytes;
     __host__ __device__ constexpr Slot2Layout(int TX, int TL, bool onsite)
@@ -62,7 +66,7 @@ struct Slot2Layout {
           eps_l((TX + 4) * TL * 16),
           eps_m((TX + 4) * TL * 16 + 128),
           eps_r((TX + 4) * TL * 16 + 128 + (TX * 8 + 127) / 128 * 128),
-          p_bytes(((TX + 2) * TL * 16 + 127) / 128 * 128),
+          p_bytes(((TX + 2 * p_halo(TL)) * TL * 16 + 127) / 128 * 128),
           b_bytes(((TX + 2) * TL * 16 + 127) / 128 * 128) {}
     // eps~ at tile x index lx in [-2, TX+1]
     __device__ __forceinline__ double eps(const unsigned char* slot, int lx, int TX) const {
@@ -91,7 +95,7 @@ struct LoadCursor {
     int row, x0, xl, xr, c0;
     bool valid;
     template <class G>
-    __device__ void seg(const G& g, int extra) {
+    __device__ void seg(const G& g, int extra, int xh = -1) {
         valid = w < w_end;
         if (!valid) return;
         const long long col = w / g.L1;
@@ -103,26 +107,26 @@ struct LoadCursor {
         w = e;
         q = 0;
         nq = H + extra;
-        const int hw = extra / 2;
+        const int hw = extra / 2;  // halo rows per side
         row = m0 - hw;
         while (row < 0) row += g.L1;
         x0 = px * g.TX;
-        xl = x0 - hw;
+        xl = x0 - (xh < 0 ? hw : xh);  // halo sites per side along x
         while (xl < 0) xl += g.L0;
         xr = x0 + g.TX;
         while (xr >= g.L0) xr -= g.L0;
         c0 = 2 * lg * g.TL;
     }
     template <class G>
-    __device__ void init(const G& g, long long b, long long e, int extra) {
+    __device__ void init(const G& g, long long b, long long e, int extra, int xh = -1) {
         w = b;
         w_end = e;
-        seg(g, extra);
+        seg(g, extra, xh);
     }
     template <class G>
-    __device__ void next(const G& g, int extra) {
+    __device__ void next(const G& g, int extra, int xh = -1) {
         if (++row == g.L1) row = 0;
-        if (++q >= nq) seg(g, extra);
+        if (++q >= nq) seg(g, extra, xh);
     }
 };
 
@@ -140,14 +144,16 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     kpm_step2_tma_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
                          const __grid_constant__ CUtensorMap mapA2,   // a_n 2-site box {2TL, 2, 1}
                          const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
-                         const __grid_constant__ CUtensorMap mapP1,   // a_{n-1} 1-site box {2TL, 1, 1}
+                         const __grid_constant__ CUtensorMap mapP1,   // a_{n-1} PH-site box {2TL, PH, 1}
                          const __grid_constant__ CUtensorMap mapE,    // eps~ box {TX, 1}
                          const __grid_constant__ CUtensorMap mapE2,   // eps~ box {2, 1}
                          const Tma2Geom g, const int tail) {
+    pdl_entry();
     constexpr int CONS = kThreads2;
     constexpr int KSTEP = CONS / TL;              // tile sites per pass
     constexpr int NB = TX + 2;                    // a_{n+1} sites per row (with halo)
     constexpr int SITE = TL * 16;
+    constexpr int PH = p_halo(TL);                // a_{n-1} halo sites per side in the slot
     constexpr Slot2Layout SL(TX, TL, ONSITE);
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ringA = smem;
@@ -187,12 +193,12 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
         if (!cp.valid) return;
         const int row = cp.row, c0 = cp.c0, x0 = cp.x0, xl1 = cp.xl, xr1 = cp.xr;
         unsigned char* dst = ringP + slot * SL.p_bytes;
-        mbar_expect_tx(fullP + slot, (TX + 2) * SITE);
+        mbar_expect_tx(fullP + slot, (TX + 2 * PH) * SITE);
         const uint64_t pol = pol_smem;
         tma_load_hint(dst, &mapP1, fullP + slot, c0, xl1, row, pol);
-        tma_load_hint(dst + SITE, &mapP, fullP + slot, c0, x0, row, pol);
-        tma_load_hint(dst + (TX + 1) * SITE, &mapP1, fullP + slot, c0, xr1, row, pol);
-        cp.next(g, 2);
+        tma_load_hint(dst + PH * SITE, &mapP, fullP + slot, c0, x0, row, pol);
+        tma_load_hint(dst + (TX + PH) * SITE, &mapP1, fullP + slot, c0, xr1, row, pol);
+        cp.next(g, 2, PH);
     };
     if (t == 0) {
         for (int i = 0; i < kSA2; ++i) mbar_init(fullA + i, 1);
@@ -208,7 +214,7 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
         }
         pol_smem = policy_evict_first();
         ca.init(g, w_begin, w_end, 4);
-        cp.init(g, w_begin, w_end, 2);
+        cp.init(g, w_begin, w_end, 2, PH);
         for (int i = 0; i < kSA2; ++i) issueA(i);
         for (int i = 0; i < kSP2; ++i) issueP(i);
     }
@@ -315,7 +321,8 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
                 if (halo_warp) break;
                 const int lx = k0 + p * KSTEP;       // interior site
                 const int oa = (lx + 2) * SITE + lo;  // a_n slot index
-                const int ob = (lx + 1) * SITE + lo;  // a_{n+1} / a_{n-1} slot index
+                const int ob = (lx + 1) * SITE + lo;  // a_{n+1} slot index
+                const int op = (lx + PH) * SITE + lo; // a_{n-1} slot index
                 const double2 ph = PEIERLS ? sphase[lx + 1] : make_double2(0.0, 0.0);
                 if (q == 0) {
                     am[p] = ld(A0 + oa);
@@ -326,7 +333,7 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
                 // first step: a_{n+1}(row r, lx)
                 const double2 x = ac[p];
                 const double e1 = ONSITE ? reinterpret_cast<const double*>(A1 + SL.eps_m)[lx] : g.shift;
-                const double2 b = step_val(x, ld(A1 + oa - SITE), ld(A1 + oa + SITE), am[p], ap[p], e1, ph, ld(Pq + ob));
+                const double2 b = step_val(x, ld(A1 + oa - SITE), ld(A1 + oa + SITE), am[p], ap[p], e1, ph, ld(Pq + op));
                 *reinterpret_cast<double2*>(Bq + ob) = b;
                 if (own_b) {
                     __stcs(outB + p * gstep, b);
@@ -353,10 +360,11 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
             if (hs >= 0) {  // halo a_{n+1} site (recomputed here, owned by the neighbouring pencil)
                 const int oa = (hlx + 2) * SITE + lo;
                 const int ob = (hlx + 1) * SITE + lo;
+                const int op = (hlx + PH) * SITE + lo;
                 const double2 ph = PEIERLS ? sphase[hlx + 1] : make_double2(0.0, 0.0);
                 const double e1 = ONSITE ? SL.eps(A1, hlx, TX) : g.shift;
                 const double2 b = step_val(ld(A1 + oa), ld(A1 + oa - SITE), ld(A1 + oa + SITE), ld(A0 + oa), ld(A2 + oa), e1,
-                                           ph, ld(Pq + ob));
+                                           ph, ld(Pq + op));
                 *reinterpret_cast<double2*>(Bq + ob) = b;
             }
             if (halo_warp) {  // the two halo sites x0-1, x0+TX of a_{n+1}, all lanes
@@ -364,10 +372,11 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
                     const int hx = j < TL ? -1 : TX, hl = j % TL;
                     const int oa = (hx + 2) * SITE + hl * 16;
                     const int ob = (hx + 1) * SITE + hl * 16;
+                    const int op = (hx + PH) * SITE + hl * 16;
                     const double2 ph = PEIERLS ? sphase[hx + 1] : make_double2(0.0, 0.0);
                     const double e1 = ONSITE ? SL.eps(A1, hx, TX) : g.shift;
                     const double2 b = step_val(ld(A1 + oa), ld(A1 + oa - SITE), ld(A1 + oa + SITE), ld(A0 + oa),
-                                               ld(A2 + oa), e1, ph, ld(Pq + ob));
+                                               ld(A2 + oa), e1, ph, ld(Pq + op));
                     *reinterpret_cast<double2*>(Bq + ob) = b;
                 }
             }

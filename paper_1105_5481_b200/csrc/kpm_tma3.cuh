@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                          const __grid_constant__ CUtensorMap mapP,     // a_{n-1}: {2TL, TX, TY, 1}
                          const __grid_constant__ CUtensorMap mapE,     // eps~: {TX, TY, 1}
                          const TmaGeom g, const int tail) {
+    pdl_entry();
     using S = Slot3<TX, TY, TL, ONSITE>;
     constexpr int CONS = kTmaConsumerWarps * 32;
     constexpr int KSTEP = CONS / TL;                 // tile sites per pass

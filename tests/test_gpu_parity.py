@@ -92,7 +92,23 @@ TMA_CASES = {
     "3d_single_pencil": (lat_of(3, (16, 8, 6), W=1.0), 20, 16),
     "3d_anderson_R48": (lat_of(3, (32, 16, 12), W=2.0), 19, 48),
     "3d_round_robin": (lat_of(3, (256, 128, 4), W=2.0), 17, 64),  # 4 lane groups x 256 pencils
+    # 4 lanes per site (small R per GPU, e.g. c2's share at 8 GPUs): 64-site two-step tiles
+    "2d_R8_four_lanes": (lat_of(2, (128, 40)), 40, 8),
+    "2d_anderson_R8_four_lanes": (lat_of(2, (256, 20), W=2.0), 33, 8),
+    "2d_peierls_R4_four_lanes": (lat_of(2, (64, 16), flux=1 / 8), 41, 4),
 }
+
+
+def two_step_expected(lat, info, N=None):
+    """The planner's two-step rule: 2D, a tile width TX2 (1024 lanes per row, or 64 sites with 4
+    lanes per site) dividing L0, at least two recursion steps."""
+    L0 = lat["L"][0]
+    ok = lat["ndim"] == 2 and (L0 % (1024 // info["TL"]) == 0 or (info["TL"] == 4 and L0 % 64 == 0))
+    if N is not None:
+        ok = ok and N // 2 - 1 >= 2
+    if info["two_step"]:
+        assert L0 % info["TX2"] == 0 and info["TX2"] in (1024 // info["TL"], 64), info
+    return int(ok)
 
 
 @pytest.mark.parametrize("case", sorted(TMA_CASES))
@@ -109,7 +125,7 @@ def test_tma_march_matches_oracle(kpm, case):
     assert info["tma"] == 1, info
     assert info["round_robin"] == (case == "3d_round_robin"), info
     if lat["ndim"] == 2:
-        assert info["two_step"] == (lat["L"][0] % (1024 // info["TL"]) == 0), info
+        assert info["two_step"] == two_step_expected(lat, info), info
     else:  # the 3D two-step kernel (kpm_tma32.cuh) is experimental (libkpm_exp.so)
         assert info["two_step"] == info["two_step3d"] == 0, info
     mu = h.moments(N, R, 21)
@@ -151,7 +167,7 @@ def test_two_step_pairs_and_single_steps(kpm, case, N):
     ref = oracle.moments_doubling(H, a, b, ki.rademacher(5, R, lat["D"]), N)
     h = make(kpm, lat, a, b, no_small=1)
     info = h.plan_info(N, R)
-    assert info["two_step"] == (N // 2 - 1 >= 2 and lat["L"][0] % (1024 // info["TL"]) == 0)
+    assert info["two_step"] == two_step_expected(lat, info, N), info
     mu2 = h.moments(N, R, 5)
     for xw in (1, 2):  # with and without the halo warp
         h.set_plan_opts(no_small=1, halo_warp=xw)
