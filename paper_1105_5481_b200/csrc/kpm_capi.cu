@@ -628,7 +628,8 @@ template <bool CPLX>
 kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail) {
     dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
     const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX);
-    auto kern = kpm::kpm_ell_step_kernel<CPLX>;
+    auto kern = h->K <= 4 ? kpm::kpm_ell_step_kernel<CPLX, 4>
+                          : (h->K <= 8 ? kpm::kpm_ell_step_kernel<CPLX, 8> : kpm::kpm_ell_step_kernel<CPLX, 16>);
     KPM_TRY(set_smem((const void*)kern, smem, h->device));
     const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a};
     return launch_k(h, h->stream, kern, grid, block, smem, op, v, tail);

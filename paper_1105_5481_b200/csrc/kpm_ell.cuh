@@ -29,21 +29,31 @@ __host__ __device__ inline size_t ell_smem_bytes(int nthr, int TS, int K, bool c
     return 3 * (size_t)nthr * 16 + 2 * (size_t)K * tile * 4 + 16 + 2 * (size_t)K * tile * (cplx ? 16 : 8);
 }
 
-template <bool CPLX>
-__global__ void __launch_bounds__(512) kpm_ell_step_kernel(const EllOp<CPLX> op, const VecArgs v, const int tail) {
+// KMAX: compile-time bound on the entries per row (4, 8 or 16; the row's K <= KMAX entries are
+// unrolled, entries k >= K skipped by a CTA-uniform branch).  U rows per thread are processed
+// together -- all their gathers issued before any is consumed -- so a thread keeps up to
+// U (KMAX + 2) 16-byte loads in flight (ncu r01: the one-row-at-a-time loop with 8-entry padded
+// chunks issued 196 warp instructions per row and stalled on L1TEX latency at 39% DRAM).  One
+// 512-thread CTA per SM (128 registers hold the loads in flight).
+template <bool CPLX, int KMAX>
+__global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> op, const VecArgs v, const int tail) {
     pdl_entry();
+    constexpr int U = KMAX == 4 ? 4 : (KMAX == 8 ? 2 : 1);  // U (K + 2) double2 in flight: 24, 20, 18
+    static_assert(kEllSPW % U == 0, "rows per thread");
     const int TR = blockDim.x, TS = blockDim.y;
     const int nthr = TR * TS, tid = threadIdx.y * TR + threadIdx.x;
     const int rg = blockIdx.y * TR + threadIdx.x;
     const bool active = rg < v.RG;
-    const int K = op.K, D = op.D;
+    const int K = op.K, D = op.D, RG = v.RG;
     const int TILE = TS * kEllSPW;
     extern __shared__ double2 sred[];                                     // [3][nthr]
     int* scol = reinterpret_cast<int*>(sred + 3 * nthr);                 // [2][K][TILE]
     const size_t vofs = ((size_t)2 * K * TILE * 4 + 15) / 16 * 16;
     unsigned char* sval = reinterpret_cast<unsigned char*>(scol) + vofs; // [2][K][TILE] double or double2
-    const int vb = CPLX ? 16 : 8;
+    constexpr int vb = CPLX ? 16 : 8;
     const int ntiles = (D + TILE - 1) / TILE;
+    const double2* __restrict__ C = v.C;
+    double2* __restrict__ P = v.P;
 
     auto prefetch = [&](int tile, int buf) {
         for (int e = tid; e < K * TILE; e += nthr) {
@@ -71,33 +81,37 @@ __global__ void __launch_bounds__(512) kpm_ell_step_kernel(const EllOp<CPLX> op,
         const int* tc = scol + (size_t)buf * K * TILE;
         const unsigned char* tv = sval + (size_t)buf * K * TILE * vb;
 #pragma unroll 1
-        for (int u = 0; u < kEllSPW; ++u) {
-            const int i = threadIdx.y + u * TS;
-            const int s = tile * TILE + i;
-            if (s >= D) break;
-            const size_t idx = (size_t)s * v.RG + rg;
-            const double2 x = __ldg(v.C + idx);
-            const double2 p = __ldcs(v.P + idx);
-            double2 h = scale2(op.shift, x);
-            for (int k0 = 0; k0 < K; k0 += 8) {
-                double2 xj[8], vv[8];
+        for (int u0 = 0; u0 < kEllSPW; u0 += U) {
+            int ii[U];
+            bool ok[U];
+            double2 x[U], p[U], xj[U][KMAX];
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int k = k0 + q < K ? k0 + q : K - 1;
-                    const int j = tc[k * TILE + i];
-                    xj[q] = __ldg(v.C + (size_t)j * v.RG + rg);
-                    vv[q] = CPLX ? reinterpret_cast<const double2*>(tv)[k * TILE + i]
-                                 : make_double2(reinterpret_cast<const double*>(tv)[k * TILE + i], 0.0);
-                    if (k0 + q >= K) vv[q] = make_double2(0.0, 0.0);
-                }
+            for (int q = 0; q < U; ++q) {
+                ii[q] = threadIdx.y + (u0 + q) * TS;
+                ok[q] = tile * TILE + ii[q] < D;
+                const int s = ok[q] ? tile * TILE + ii[q] : tile * TILE;  // (a valid row; result unused)
+                x[q] = __ldg(C + (size_t)s * RG + rg);
+                p[q] = __ldcs(P + (size_t)s * RG + rg);
 #pragma unroll
-                for (int q = 0; q < 8; ++q) h = CPLX ? add2(h, cmul(vv[q], xj[q])) : fma2(vv[q].x, xj[q], h);
+                for (int k = 0; k < KMAX; ++k)
+                    if (k < K) xj[q][k] = __ldg(C + (size_t)tc[k * TILE + (ok[q] ? ii[q] : 0)] * RG + rg);
             }
-            const double2 y = make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));  // Eq 18
-            __stcs(v.P + idx, y);
-            dot_acc<CPLX>(acc0, x, x);
-            dot_acc<CPLX>(acc1, x, y);
-            if (tail) dot_acc<CPLX>(acc2, y, y);
+#pragma unroll
+            for (int q = 0; q < U; ++q) {
+                if (!ok[q]) continue;
+                double2 h = scale2(op.shift, x[q]);
+#pragma unroll
+                for (int k = 0; k < KMAX; ++k) {
+                    if (k >= K) break;
+                    if (CPLX) h = add2(h, cmul(reinterpret_cast<const double2*>(tv)[k * TILE + ii[q]], xj[q][k]));
+                    else h = fma2(reinterpret_cast<const double*>(tv)[k * TILE + ii[q]], xj[q][k], h);
+                }
+                const double2 y = make_double2(fma(2.0, h.x, -p[q].x), fma(2.0, h.y, -p[q].y));  // Eq 18
+                __stcs(P + (size_t)(tile * TILE + ii[q]) * RG + rg, y);
+                dot_acc<CPLX>(acc0, x[q], x[q]);
+                dot_acc<CPLX>(acc1, x[q], y);
+                if (tail) dot_acc<CPLX>(acc2, y, y);
+            }
         }
     }
     cp_async_wait_all();

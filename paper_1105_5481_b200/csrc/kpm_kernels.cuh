@@ -445,7 +445,10 @@ __global__ void moment_stats_kernel(const double* __restrict__ pv, long long R, 
     sem[n] = R > 1 ? sqrt(q / ((double)(R - 1) * (double)R)) : CUDART_NAN;
 }
 
-// rho(omega) = sum_n c_n T_n(x) / (pi a sqrt(1 - x^2)), x = (omega - b)/a; T_n by Eq (4)-(5).
+// rho(omega) = sum_n c_n T_n(x) / (pi a sqrt(1 - x^2)), x = (omega - b)/a, with
+// T_n(x) = cos(n theta), theta = arccos x (Eq 3) evaluated term by term.  (The three-term
+// recurrence, Eq 4-5, propagates a rounding error like n^2 eps near x = +-1 -- 1.8e-9 at
+// n = 4096 -- while cos(n theta) errs by about n theta eps; X27.)  One thread per energy.
 __global__ void dos_kernel(const double* __restrict__ c, int N, double a, double b, const double* __restrict__ omega,
                            long long K, double* __restrict__ rho) {
     const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -455,23 +458,17 @@ __global__ void dos_kernel(const double* __restrict__ c, int N, double a, double
         rho[k] = 0.0;
         return;
     }
-    double t0 = 1.0, t1 = x;
+    const double th = acos(x);
     double s = c[0];
-    if (N > 1) s = fma(c[1], t1, s);
-    for (int n = 2; n < N; ++n) {
-        const double t2 = fma(2.0 * x, t1, -t0);
-        s = fma(c[n], t2, s);
-        t0 = t1;
-        t1 = t2;
-    }
+    for (int n = 1; n < N; ++n) s = fma(c[n], cos((double)n * th), s);
     rho[k] = s / (CUDART_PI * a * sqrt(1.0 - x * x));
 }
 
-// Retarded G(omega) = G~(x)/a (X24).  Inside (|x| < 1), with
-// e^{-i n theta} = T_n(x) - i sin(theta) U_{n-1}(x):
-//   Re G~ = -sum_{n>=1} c_n U_{n-1}(x),   Im G~ = -sum_n c_n T_n(x) / sqrt(1 - x^2)
-// (T and U by the three-term recurrence, Eq 5).  Outside: G~ = sum_n c_n t^n / (sgn(x)
-// sqrt(x^2 - 1)), t = x - sgn(x) sqrt(x^2 - 1) (Horner).  |x| = 1: NaN.  G is [K][2] (re, im).
+// Retarded G(omega) = G~(x)/a (X24).  Inside (|x| < 1), theta = arccos x:
+//   G~ = -i sum_n c_n e^{-i n theta} / sin(theta)
+//   Re G~ = -sum_{n>=1} c_n sin(n theta) / sin(theta),  Im G~ = -sum_n c_n cos(n theta) / sin(theta)
+// (term by term, as dos_kernel).  Outside: G~ = sum_n c_n t^n / (sgn(x) sqrt(x^2 - 1)),
+// t = x - sgn(x) sqrt(x^2 - 1), |t| < 1 (Horner).  |x| = 1: NaN.  G is [K][2] (re, im).
 __global__ void green_kernel(const double* __restrict__ c, int N, double a, double b, const double* __restrict__ omega,
                              long long K, double* __restrict__ G) {
     const long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -479,24 +476,17 @@ __global__ void green_kernel(const double* __restrict__ c, int N, double a, doub
     const double x = (omega[k] - b) / a;
     double re, im;
     if (fabs(x) < 1.0) {
-        double t0 = 1.0, t1 = x, u0 = 1.0, u1 = 2.0 * x;  // T_0, T_1, U_0, U_1
-        double st = c[0], su = 0.0;
-        if (N > 1) {
-            st = fma(c[1], t1, st);
-            su = c[1] * u0;
+        const double th = acos(x);
+        double sc = c[0], ss = 0.0;
+        for (int n = 1; n < N; ++n) {
+            double sn, cn;
+            sincos((double)n * th, &sn, &cn);
+            sc = fma(c[n], cn, sc);
+            ss = fma(c[n], sn, ss);
         }
-        for (int n = 2; n < N; ++n) {
-            const double t2 = fma(2.0 * x, t1, -t0);
-            st = fma(c[n], t2, st);
-            su = fma(c[n], u1, su);  // U_{n-1}
-            const double u2 = fma(2.0 * x, u1, -u0);
-            t0 = t1;
-            t1 = t2;
-            u0 = u1;
-            u1 = u2;
-        }
-        re = -su;
-        im = -st / sqrt(1.0 - x * x);
+        const double st = sin(th);  // sin(arccos x), as the oracle
+        re = -ss / st;
+        im = -sc / st;
     } else if (fabs(x) > 1.0) {
         const double sg = x > 0 ? 1.0 : -1.0;
         const double sq = sqrt(x * x - 1.0);

@@ -48,9 +48,12 @@ struct Tma2Geom {
 };
 
 constexpr int kThreads2 = 256;  // 8 warps
-constexpr int kSA2 = 5;         // a_n ring
-constexpr int kSP2 = 3;         // a_{n-1} ring
 constexpr int kSB2 = 3;         // a_{n+1} ring (computed)
+// a_n / a_{n-1} ring depths: 5 / 3 slots for the 1024-lane row tiles (one CTA per SM, ~190 KB);
+// 12 / 8 for the small 4-lane x 64-site tile (two CTAs per SM, L2-resident blocks): rows are only
+// 4 KB there, and the deeper rings keep more TMA loads in flight per CTA.
+__host__ __device__ constexpr int ring2_a(int TL, int TX) { return TL * TX <= 256 ? 12 : 5; }
+__host__ __device__ constexpr int ring2_p(int TL, int TX) { return TL * TX <= 256 ? 8 : 3; }
 
 // a_n slot: [2 halo sites][TX sites][2 halo sites] then eps~ as three 128-byte aligned
 // pieces (TMA destinations must be 128-byte aligned): [2 left][TX main][2 right].
@@ -78,8 +81,9 @@ struct Slot2Layout {
 
 __host__ __device__ inline size_t step2_smem_bytes(int TX, int TL, bool onsite, int RP) {
     const Slot2Layout S(TX, TL, onsite);
-    return (size_t)kSA2 * S.a_bytes + (size_t)kSP2 * S.p_bytes + (size_t)kSB2 * S.b_bytes + 5 * (size_t)RP * 8 +
-           (size_t)kThreads2 * 16 + (size_t)(TX + 2) * 16 + (kSA2 + kSP2) * 8;
+    const int SA = ring2_a(TL, TX), SP = ring2_p(TL, TX);
+    return (size_t)SA * S.a_bytes + (size_t)SP * S.p_bytes + (size_t)kSB2 * S.b_bytes + 5 * (size_t)RP * 8 +
+           (size_t)kThreads2 * 16 + (size_t)(TX + 2) * 16 + (SA + SP) * 8;
 }
 
 // Walks one CTA's segments (lane group, pencil, rows [m0, m0+H)) and, within a segment,
@@ -155,6 +159,7 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     constexpr int SITE = TL * 16;
     constexpr int PH = p_halo(TL);                // a_{n-1} halo sites per side in the slot
     constexpr Slot2Layout SL(TX, TL, ONSITE);
+    constexpr int kSA2 = ring2_a(TL, TX), kSP2 = ring2_p(TL, TX);
     extern __shared__ __align__(128) unsigned char smem[];
     unsigned char* ringA = smem;
     unsigned char* ringP = ringA + kSA2 * SL.a_bytes;

@@ -2,9 +2,10 @@
 damping kernels (Eq 6-7 with the kernels of ref [10]), the DoS with every kernel, the
 retarded Green's function (reading X24), and local moments <i|T_n(H~)|i> from unit start
 vectors (KPM_LOCAL).  Tolerances: reading X17 (normwise 1e-10) for moments.  The expansions
-evaluate T_n (and U_n) by the three-term recurrence (Eq 5) on the GPU and by cos(n arccos x)
-in the oracle; the recurrence's rounding error grows like n^2 eps near x = +-1, so the bar is
-N^2 eps sum|c_n| / max|value| <~ 1e-10 for N <= 1000 (X27), written as 1e-10."""
+evaluate T_n = cos(n theta) (and sin(n theta)) term by term on both sides (theta = arccos x);
+the per-term difference is at most a few ulp of theta times n, so |drho(x)| <= eps sum_n |c_n|
+(2 + 4 n theta) / (pi a sin theta) pointwise (X27; 1.4e-12 relative to max|rho| at
+N = 4096), and the bar is 1e-10 relative to max|value|, at the configs' N = 1024-4096 too."""
 import numpy as np
 import pytest
 
@@ -69,7 +70,47 @@ def test_green_matches_oracle_inside_and_outside(kpm, name):
     # Im G = -pi rho (same kernel)
     ins = np.abs(om - b) < a
     rho = kpm.kpm_dos_ex(mu, a, b, om[ins], kernel=KERNELS[name], lam=4.0)
-    assert rel(-G.imag[ins] / np.pi, rho) < 1e-12  # same recurrence on both
+    assert rel(-G.imag[ins] / np.pi, rho) < 1e-12  # same terms on both
+
+
+# the configs' moment counts (BASELINE.json c2 N=1024, c3 N=2048, c4 N=4096), on lattices of the
+# same kinds (moments from the oracle; only the expansion is under test here)
+BIG_N = {
+    "c2_like_N1024": (lat_of(2, (40, 36)), 1024),
+    "c3_like_N2048": (lat_of(3, (12, 11, 10), W=2.0), 2048),
+    "c4_like_N4096": (lat_of(2, (32, 24), flux=1 / 8), 4096),
+}
+
+
+@pytest.mark.parametrize("name", ["jackson", "lorentz", "none"])
+@pytest.mark.parametrize("case", sorted(BIG_N))
+def test_dos_green_at_config_N(kpm, case, name):
+    """DoS and Green's function at N = 1024, 2048, 4096: normwise 1e-10 against the oracle and
+    the pointwise bound of reading X27, on a grid that reaches x = +-(1 - 1e-9) and on the N
+    Chebyshev nodes."""
+    lat, N = BIG_N[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    mu = oracle.moments_doubling(H, a, b, ki.rademacher(7, 3, lat["D"]), N)
+    x = np.concatenate([np.linspace(-1 + 1e-9, 1 - 1e-9, 2001), oracle.chebyshev_nodes(N),
+                        [-1 + 1e-12, 1 - 1e-12]])
+    om = b + a * x
+    rho = kpm.kpm_dos_ex(mu, a, b, om, kernel=KERNELS[name], lam=4.0)
+    ref = oracle.dos(mu, a, b, om, kernel=name, lam=4.0)
+    assert rel(rho, ref) < 1e-10
+    c = oracle.kernel_coeffs(N, name, 4.0) * mu
+    c[1:] *= 2
+    xs = (om - b) / a
+    th = np.arccos(np.clip(xs, -1, 1))
+    n = np.arange(N)
+    bound = np.finfo(float).eps * (np.abs(c)[None, :] * (2 + 4 * np.outer(th, n))).sum(axis=1) / (np.pi * a * np.sin(th))
+    assert np.all(np.abs(rho - ref) <= bound), np.max(np.abs(rho - ref) / bound)
+    G = kpm.kpm_green(mu, a, b, om, kernel=KERNELS[name], lam=4.0)
+    Gr = oracle.green(mu, a, b, om, kernel=name, lam=4.0)
+    assert rel(G.real, Gr.real) < 1e-10 and rel(G.imag, Gr.imag) < 1e-10
+    out = b + a * np.array([-2.0, -1.01, 1.01, 3.0])  # outside the band
+    Go = kpm.kpm_green(mu, a, b, out, kernel=KERNELS[name], lam=4.0)
+    assert rel(Go.real, oracle.green(mu, a, b, out, kernel=name, lam=4.0).real) < 1e-10
 
 
 LOCAL_CASES = {

@@ -15,9 +15,11 @@ import oracle
 
 pytestmark = pytest.mark.gpu
 
-# config -> (sampled vector indices, number of moments checked against the oracle)
-SAMPLES = {"c1": ([0, 3, 7], None), "c2": ([0, 63], None), "c3": ([0, 127], 256),
-           "c4": ([0, 255], 512), "c5": ([0, 31], 16)}
+# config -> (sampled vector indices, number of moments checked against the oracle; None = all N).
+# The oracle splits its rows over the host threads when it runs one vector (oracle/kpm_oracle.c),
+# so whole vectors at full N fit the test budget up to c4; c5 (D = 134M) checks 256 moments.
+SAMPLES = {"c1": ([0, 3, 7], None), "c2": ([0, 63], None), "c3": ([0, 127], None),
+           "c4": ([0, 255], None), "c5": ([0, 31], 256)}
 
 
 @pytest.fixture(scope="module")
