@@ -237,7 +237,9 @@ typedef struct {
                               64-site tile, else 1) */
     int32_t no_pdl;        /* 1: plain stream-ordered launches instead of programmatic dependent
                               launches (PDL: the next kernel's prologue overlaps this one's tail) */
-    int32_t reserved[5];   /* must be 0 */
+    int32_t no_first_tile; /* 1: first step by the generic grid-stride kernel (a_0 hashed per neighbour)
+                              instead of the plane-ring tile kernel (2D/3D stencils) */
+    int32_t reserved[4];   /* must be 0 */
 } kpm_plan_opts;
 
 /* Set (opts != NULL) or reset to the default (opts == NULL) the plan options of h.

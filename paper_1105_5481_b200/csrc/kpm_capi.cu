@@ -36,6 +36,7 @@
 #include "kpm_tma32.cuh"
 #include "kpm_persist.cuh"
 #include "kpm_ell.cuh"
+#include "kpm_first.cuh"
 #include "kpm_small.cuh"
 #include "kpm_dense.cuh"
 
@@ -628,8 +629,11 @@ template <bool CPLX>
 kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail) {
     dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
     const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX);
-    auto kern = h->K <= 4 ? kpm::kpm_ell_step_kernel<CPLX, 4>
-                          : (h->K <= 8 ? kpm::kpm_ell_step_kernel<CPLX, 8> : kpm::kpm_ell_step_kernel<CPLX, 16>);
+    const bool wide = (double)(h->D + h->n_ghost) * p.RG >= 2147483648.0;  // 32-bit element offsets otherwise
+    auto kern = wide ? (h->K <= 4 ? kpm::kpm_ell_step_kernel<CPLX, 4, true>
+                                  : (h->K <= 8 ? kpm::kpm_ell_step_kernel<CPLX, 8, true> : kpm::kpm_ell_step_kernel<CPLX, 16, true>))
+                     : (h->K <= 4 ? kpm::kpm_ell_step_kernel<CPLX, 4, false>
+                                  : (h->K <= 8 ? kpm::kpm_ell_step_kernel<CPLX, 8, false> : kpm::kpm_ell_step_kernel<CPLX, 16, false>));
     KPM_TRY(set_smem((const void*)kern, smem, h->device));
     const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a};
     return launch_k(h, h->stream, kern, grid, block, smem, op, v, tail);
@@ -718,6 +722,56 @@ kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& 
         case 6: return launch_mode<false>(h, p, StencilOp<3, false, false>{g}, mode, v, tail);
         default: return launch_mode<false>(h, p, StencilOp<3, true, false>{g}, mode, v, tail);
     }
+}
+
+// First step of a 2D/3D stencil with a_0 generated once per element (kpm_first.cuh).
+template <int NDIM, bool ONSITE, bool PEIERLS, bool CPLX>
+kpm_status launch_first_t(kpm_handle_s* h, const kpm::VecArgs& v, const kpm::FirstGeom& g, int grid, size_t smem, int tail) {
+    auto kern = kpm::kpm_first_tile_kernel<NDIM, ONSITE, PEIERLS, CPLX>;
+    KPM_TRY(set_smem((const void*)kern, smem, h->device));
+    return launch_k(h, h->stream, kern, dim3(grid), dim3(kpm::kFirstThreads), smem, v, g, tail);
+}
+
+kpm_status launch_first_tile(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail) {
+    kpm::FirstGeom g{};
+    const int nd = h->ndim;
+    g.L0 = (int)h->L[0];
+    g.L1 = (int)h->L[1];
+    g.TL = std::min(nd == 3 ? 8 : 16, p.RG);
+    g.TX = (int)std::min<int64_t>(nd == 3 ? 16 : 64, h->L[0]);
+    g.TY = nd == 3 ? (int)std::min<int64_t>(16, h->L[1]) : 1;
+    g.PX = (g.L0 + g.TX - 1) / g.TX;
+    g.PY = nd == 3 ? (g.L1 + g.TY - 1) / g.TY : 1;
+    g.G_L = (p.RG + g.TL - 1) / g.TL;
+    g.Lm = (int)h->L[nd - 1];  // (the slab's planes under KPM_PART_ROWS)
+    const long long cols = (long long)g.G_L * g.PX * g.PY;
+    const int rows = p.gx;     // partial-sum rows per slot of this plan
+    int nseg = cols >= 2LL * rows ? 1 : (int)((2LL * rows + cols - 1) / cols);
+    int seg = (g.Lm + nseg - 1) / nseg;
+    if (seg < 4) seg = std::min(4, g.Lm);
+    g.SEG = seg;
+    g.NSEG = (g.Lm + seg - 1) / seg;
+    g.items = cols * g.NSEG;
+    g.rows_total = rows;
+    g.ghost = h->rows ? 1 : 0;
+    g.t = h->t_scaled;
+    g.shift = -h->b / h->a;
+    g.eps = h->d_eps;
+    g.phase = h->d_phase;
+    const int grid = (int)std::min<long long>(g.items, rows);
+    const size_t smem = kpm::first_smem_bytes(nd, g.TX, g.TY, g.TL, p.RP);
+    if (smem > (size_t)h->smem_optin) return fail(KPM_ERR_UNSUPPORTED, "first-step tile does not fit shared memory");
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_first_t<2, true, true, true>(h, v, g, grid, smem, tail);
+        return launch_first_t<2, false, true, true>(h, v, g, grid, smem, tail);
+    }
+    if (nd == 2) {
+        if (on) return launch_first_t<2, true, false, false>(h, v, g, grid, smem, tail);
+        return launch_first_t<2, false, false, false>(h, v, g, grid, smem, tail);
+    }
+    if (on) return launch_first_t<3, true, false, false>(h, v, g, grid, smem, tail);
+    return launch_first_t<3, false, false, false>(h, v, g, grid, smem, tail);
 }
 
 #ifdef KPM_EXPERIMENTAL
@@ -1260,7 +1314,12 @@ struct Run {
         v.red0 = part;
         v.red1 = N > 1 ? part + slot : nullptr;
         v.red2 = (!direct && N == 3) ? part + 2 * slot : nullptr;
-        KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
+        // 2D/3D stencils: a_0 hashed once per element into a shared-memory plane ring
+        // (kpm_first.cuh); else the generic grid-stride kernel
+        if (first_mode == kpm::FIRST_GEN && h->kind == KIND_STENCIL && h->ndim >= 2 && !h->opts.no_first_tile)
+            KPM_TRY(launch_first_tile(h, p, v, v.red2 != nullptr));
+        else
+            KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
 
         // Recursion launches (Eq 18).  Single-step launches write a_{n+1} over a_{n-1} in place;
         // two-step launches (kpm_tma2.cuh) read (a_n, a_{n-1}) and write (a_{n+1}, a_{n+2}) into
@@ -2580,7 +2639,7 @@ kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
     }
     const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
                          o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
-                         o->no_graph,  o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl};
+                         o->no_graph,  o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile};
     for (int32_t x : f)
         if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
     for (int32_t x : o->reserved)

@@ -8,6 +8,8 @@
 // One warp row of threads owns the 16-byte vector lanes of a row (one matrix entry
 // serves all R vectors, BJ north_star); each thread keeps 8 gathers in flight.
 #pragma once
+#include <type_traits>
+
 #include "kpm_kernels.cuh"
 
 namespace kpm {
@@ -35,16 +37,19 @@ __host__ __device__ inline size_t ell_smem_bytes(int nthr, int TS, int K, bool c
 // U (KMAX + 2) 16-byte loads in flight (ncu r01: the one-row-at-a-time loop with 8-entry padded
 // chunks issued 196 warp instructions per row and stalled on L1TEX latency at 39% DRAM).  One
 // 512-thread CTA per SM (128 registers hold the loads in flight).
-template <bool CPLX, int KMAX>
+template <bool CPLX, int KMAX, bool WIDE>
 __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> op, const VecArgs v, const int tail) {
     pdl_entry();
     constexpr int U = KMAX == 4 ? 4 : (KMAX == 8 ? 2 : 1);  // U (K + 2) double2 in flight: 24, 20, 18
     static_assert(kEllSPW % U == 0, "rows per thread");
+    // element offsets j * RG + rg in 32 bits unless the extended block has 2^31 lanes or more (WIDE)
+    using off_t = typename std::conditional<WIDE, long long, unsigned>::type;
     const int TR = blockDim.x, TS = blockDim.y;
     const int nthr = TR * TS, tid = threadIdx.y * TR + threadIdx.x;
     const int rg = blockIdx.y * TR + threadIdx.x;
     const bool active = rg < v.RG;
-    const int K = op.K, D = op.D, RG = v.RG;
+    const int K = op.K, D = op.D;
+    const off_t RG = (off_t)v.RG;
     const int TILE = TS * kEllSPW;
     extern __shared__ double2 sred[];                                     // [3][nthr]
     int* scol = reinterpret_cast<int*>(sred + 3 * nthr);                 // [2][K][TILE]
@@ -52,8 +57,8 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
     unsigned char* sval = reinterpret_cast<unsigned char*>(scol) + vofs; // [2][K][TILE] double or double2
     constexpr int vb = CPLX ? 16 : 8;
     const int ntiles = (D + TILE - 1) / TILE;
-    const double2* __restrict__ C = v.C;
-    double2* __restrict__ P = v.P;
+    const double2* __restrict__ Cl = v.C + rg;  // this thread's lane of row 0
+    double2* __restrict__ Pl = v.P + rg;
 
     auto prefetch = [&](int tile, int buf) {
         for (int e = tid; e < K * TILE; e += nthr) {
@@ -80,25 +85,25 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
         if (!active) continue;
         const int* tc = scol + (size_t)buf * K * TILE;
         const unsigned char* tv = sval + (size_t)buf * K * TILE * vb;
+        const int nrow = min(TILE, D - tile * TILE);
 #pragma unroll 1
         for (int u0 = 0; u0 < kEllSPW; u0 += U) {
             int ii[U];
-            bool ok[U];
             double2 x[U], p[U], xj[U][KMAX];
 #pragma unroll
             for (int q = 0; q < U; ++q) {
-                ii[q] = threadIdx.y + (u0 + q) * TS;
-                ok[q] = tile * TILE + ii[q] < D;
-                const int s = ok[q] ? tile * TILE + ii[q] : tile * TILE;  // (a valid row; result unused)
-                x[q] = __ldg(C + (size_t)s * RG + rg);
-                p[q] = __ldcs(P + (size_t)s * RG + rg);
+                const int i = threadIdx.y + (u0 + q) * TS;
+                ii[q] = i < nrow ? i : 0;  // (ragged last tile: row 0's loads, result unused)
+                const off_t o = (off_t)(tile * TILE + ii[q]) * RG;
+                x[q] = __ldg(Cl + o);
+                p[q] = __ldcs(Pl + o);
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k)
-                    if (k < K) xj[q][k] = __ldg(C + (size_t)tc[k * TILE + (ok[q] ? ii[q] : 0)] * RG + rg);
+                    if (k < K) xj[q][k] = __ldg(Cl + (off_t)tc[k * TILE + ii[q]] * RG);
             }
 #pragma unroll
             for (int q = 0; q < U; ++q) {
-                if (!ok[q]) continue;
+                if (threadIdx.y + (u0 + q) * TS >= nrow) continue;
                 double2 h = scale2(op.shift, x[q]);
 #pragma unroll
                 for (int k = 0; k < KMAX; ++k) {
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
                     else h = fma2(reinterpret_cast<const double*>(tv)[k * TILE + ii[q]], xj[q][k], h);
                 }
                 const double2 y = make_double2(fma(2.0, h.x, -p[q].x), fma(2.0, h.y, -p[q].y));  // Eq 18
-                __stcs(P + (size_t)(tile * TILE + ii[q]) * RG + rg, y);
+                __stcs(Pl + (off_t)(tile * TILE + ii[q]) * RG, y);
                 dot_acc<CPLX>(acc0, x[q], x[q]);
                 dot_acc<CPLX>(acc1, x[q], y);
                 if (tail) dot_acc<CPLX>(acc2, y, y);

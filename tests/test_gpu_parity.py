@@ -463,3 +463,38 @@ def test_randomized_shapes_sweep(kpm):
         ref = oracle.moments_doubling(H, a, b, ki.rademacher(trial, R, lat["D"]), N)
         mu = make(kpm, lat, a, b, no_small=trial % 2).moments(N, R, trial)  # both launch paths
         assert normwise(mu, ref) < TOL, (trial, ndim, L, flux, W, R, N)
+
+
+FIRST_CASES = {
+    "2d_ragged_tile": (lat_of(2, (70, 9), W=1.0), 12, 6),          # L0 not a multiple of the 64-site tile
+    "2d_peierls_lanes_masked": (lat_of(2, (48, 12), flux=1 / 4), 9, 20),  # 20 lanes: 16-lane groups, masked
+    "3d_ragged": (lat_of(3, (20, 18, 7), W=2.0), 10, 5),            # 16 x 16 tiles, ragged in x and y
+    "3d_L2": (lat_of(3, (2, 3, 2)), 7, 3),                          # one tile, halos wrap onto the tile
+    "3d_lane_groups": (lat_of(3, (16, 16, 6)), 8, 40),              # 20 lanes: 8-lane groups, masked
+}
+
+
+@pytest.mark.parametrize("case", sorted(FIRST_CASES))
+@pytest.mark.parametrize("first_tile", [0, 1])
+def test_first_step_tile_kernel(kpm, case, first_tile):
+    """a_0 hashed once per element into a plane ring (kpm_first.cuh) vs the generic first step:
+    both equal the oracle; N = 3 puts the odd-N tail <a_1|a_1> into the first launch."""
+    lat, N, R = FIRST_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b += 0.03 * a
+    a *= 1.04
+    r = ki.rademacher(17, R, lat["D"])
+    for n in (N, 3, 2):
+        ref, ref_pv = oracle.moments_doubling(H, a, b, r, n, per_vector=True)
+        h = make(kpm, lat, a, b, no_small=1, no_first_tile=int(not first_tile))
+        assert normwise(h.moments(n, R, 17), ref) < TOL
+        assert normwise(h.moments_ex(n, R, 17, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
+    # local moments (unit start vectors) and a one-slab row partition through the same kernel
+    sites = [0, lat["D"] - 1, lat["D"] // 3]
+    h = make(kpm, lat, a, b, no_small=1, no_first_tile=int(not first_tile))
+    assert normwise(h.moments_local(N, sites), oracle.local_moments(H, a, b, sites, N)) < TOL
+    hr = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], a, b, onsite=lat["onsite"], flux=lat["flux"],
+                                dist=(kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_SELF))
+    hr.set_plan_opts(no_first_tile=int(not first_tile))
+    assert normwise(hr.moments(N, R, 17), oracle.moments_doubling(H, a, b, r, N)) < TOL
