@@ -226,8 +226,6 @@ typedef struct {
     int32_t no_overlap;    /* 1: row partition: halo exchange after each step, not overlapped */
     int32_t no_fused_halo; /* 1: in-process slab groups: plane copies, not fused peer stores */
     int32_t contiguous;    /* 1: 3D march: contiguous plane ranges, not round-robin columns */
-    int32_t no_graph;      /* 1: launch the recursion step by step instead of replaying a captured
-                              CUDA graph of the step loop */
     int32_t experimental;  /* experimental kernels, compiled only into libkpm_exp.so (the default
                               libkpm.so answers KPM_ERR_UNSUPPORTED): 1 = 3D two-step kernel
                               (exp_param = tile shape 0..3), 2 = KS-steps-per-launch 2D kernel
@@ -239,7 +237,7 @@ typedef struct {
                               launches (PDL: the next kernel's prologue overlaps this one's tail) */
     int32_t no_first_tile; /* 1: first step by the generic grid-stride kernel (a_0 hashed per neighbour)
                               instead of the plane-ring tile kernel (2D/3D stencils) */
-    int32_t reserved[4];   /* must be 0 */
+    int32_t reserved[5];   /* must be 0 */
 } kpm_plan_opts;
 
 /* Set (opts != NULL) or reset to the default (opts == NULL) the plan options of h.

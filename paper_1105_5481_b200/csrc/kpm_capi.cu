@@ -2639,7 +2639,7 @@ kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
     }
     const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
                          o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
-                         o->no_graph,  o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile};
+                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile};
     for (int32_t x : f)
         if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
     for (int32_t x : o->reserved)

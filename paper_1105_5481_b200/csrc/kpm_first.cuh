@@ -28,22 +28,27 @@ struct FirstGeom {
     const double2* phase;
 };
 
-constexpr int kFirstThreads = 256;
+constexpr int kFirstThreads = 512;  // 16 warps: one CTA per SM holds the whole partial-row budget of the plan
 
+// shared-memory carve-up: ring [3][PYs][PXs][TL] double2 | eps~ [3][TY][TX] | sacc [3][RP] | sred [3][threads]
+// double2, each region 16-byte aligned
+__host__ __device__ inline size_t first_a16(size_t x) { return (x + 15) / 16 * 16; }
 __host__ __device__ inline size_t first_smem_bytes(int ndim, int TX, int TY, int TL, int RP) {
     const int PXs = TX + 2, PYs = ndim == 3 ? TY + 2 : 1;
-    return 3 * (size_t)PXs * PYs * TL * 16 + 3 * (size_t)RP * 8 + 3 * (size_t)kFirstThreads * 16;
+    return 3 * (size_t)PXs * PYs * TL * 16 + first_a16(3 * (size_t)TX * TY * 8) + first_a16(3 * (size_t)RP * 8) +
+           3 * (size_t)kFirstThreads * 16;
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS, bool CPLX>
 __global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const VecArgs v, const FirstGeom g, const int tail) {
     pdl_entry();
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(128) unsigned char smem[];  // (every extern smem declaration of the TU must agree: TMA destinations need 128)
     const int PXs = g.TX + 2, PYs = NDIM == 3 ? g.TY + 2 : 1;
     const int plane_el = PXs * PYs * g.TL;
     double2* ring = reinterpret_cast<double2*>(smem);                  // [3][PYs][PXs][TL]
-    double* sacc = reinterpret_cast<double*>(ring + 3 * plane_el);    // [3][RP]
-    double2* sred = reinterpret_cast<double2*>(sacc + 3 * v.RP);      // [3][threads]
+    double* seps = reinterpret_cast<double*>(ring + 3 * plane_el);    // [3][TY][TX] eps~ of the planes
+    double* sacc = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(seps) + first_a16(3 * (size_t)g.TX * g.TY * 8));
+    double2* sred = reinterpret_cast<double2*>(reinterpret_cast<unsigned char*>(sacc) + first_a16(3 * (size_t)v.RP * 8));
     const int t = threadIdx.x, nthr = blockDim.x;
     for (int i = t; i < 3 * v.RP; i += nthr) sacc[i] = 0.0;
     const int l = t % g.TL, k0 = t / g.TL, kstep = nthr / g.TL;
@@ -63,25 +68,37 @@ __global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const Vec
         const int rg0 = lg * g.TL;
         // a_0 of plane m (march coordinate; m = -1 / Lm are the periodic images, or the ghost
         // planes of a slab) with its one-site in-plane halo, into ring slot `slot`
+        // (thread t always handles lane l of tile sites k0, k0 + kstep, ...: the site coordinates
+        // advance incrementally, no per-element division)
         auto gen = [&](int m, int slot) {
             double2* dst = ring + slot * plane_el;
             int mm = m;
             if (!g.ghost) mm = mm < 0 ? mm + g.Lm : (mm >= g.Lm ? mm - g.Lm : mm);
-            for (int e = t; e < plane_el; e += nthr) {
-                const int ll = e % g.TL, s = e / g.TL;
-                const int tx = s % PXs, ty = s / PXs;
+            const int rg = rg0 + l;
+            const int jm = NDIM == 3 ? g.L0 * g.L1 * mm : g.L0 * mm;  // first site of plane mm
+            int tx = k0 % PXs, ty = k0 / PXs;
+            const int dx = kstep % PXs, dy = kstep / PXs;
+            for (int s = k0; s < PXs * PYs; s += kstep) {
                 int x = x0 + tx - 1;
                 x = x < 0 ? x + g.L0 : (x >= g.L0 ? x - g.L0 : x);
-                int j;
+                int j = jm + x;
                 if (NDIM == 3) {
                     int y = y0 + ty - 1;
                     y = y < 0 ? y + g.L1 : (y >= g.L1 ? y - g.L1 : y);
-                    j = x + g.L0 * (y + g.L1 * mm);
-                } else {
-                    j = x + g.L0 * mm;
+                    j += g.L0 * y;
                 }
-                const int rg = rg0 + ll;
-                dst[e] = rg < v.RG ? gen_lane<CPLX>(v, j, rg) : make_double2(0.0, 0.0);
+                dst[s * g.TL + l] = rg < v.RG ? gen_lane<CPLX>(v, j, rg) : make_double2(0.0, 0.0);
+                // eps~ of the interior sites, staged with the plane (a dependent global load per
+                // element stalled the compute loop: ncu long-scoreboard on the a_1 FMA)
+                if (ONSITE && l == 0 && tx >= 1 && tx <= g.TX && ty >= (NDIM == 3 ? 1 : 0) &&
+                    ty < (NDIM == 3 ? g.TY + 1 : 1) && mm >= 0 && mm < g.Lm)
+                    seps[slot * g.TX * g.TY + (NDIM == 3 ? ty - 1 : 0) * g.TX + tx - 1] = __ldg(g.eps + j);
+                tx += dx;
+                ty += dy;
+                if (tx >= PXs) {
+                    tx -= PXs;
+                    ++ty;
+                }
             }
         };
         __syncthreads();  // the previous item is done with the ring
@@ -95,11 +112,19 @@ __global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const Vec
             const double2* P1 = ring + s1 * plane_el;  // plane m
             const double2* P2 = ring + s2 * plane_el;  // plane m+1
             const int rg = rg0 + l;
+            int lx = k0 % g.TX, ly = k0 / g.TX;
+            const int ex = kstep % g.TX, ey = kstep / g.TX;
             for (int k = k0; k < nsite && rg < v.RG; k += kstep) {
-                const int lx = k % g.TX, ly = k / g.TX;
                 const int x = x0 + lx, y = y0 + ly;
+                const int lx0 = lx, ly0 = ly;
+                lx += ex;
+                ly += ey;
+                if (lx >= g.TX) {
+                    lx -= g.TX;
+                    ++ly;
+                }
                 if (x >= g.L0 || (NDIM == 3 && y >= g.L1)) continue;  // ragged last tile
-                const int c = ((NDIM == 3 ? ly + 1 : 0) * PXs + lx + 1) * g.TL + l;
+                const int c = ((NDIM == 3 ? ly0 + 1 : 0) * PXs + lx0 + 1) * g.TL + l;
                 const double2 xc = P1[c];
                 double2 nb = add2(P1[c - g.TL], P1[c + g.TL]);
                 if (NDIM == 3) nb = add2(nb, add2(P1[c - PXs * g.TL], P1[c + PXs * g.TL]));
@@ -112,12 +137,24 @@ __global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const Vec
                 } else {
                     nb = add2(nb, add2(mprev, mnext));
                 }
-                s = NDIM == 3 ? x + g.L0 * (y + g.L1 * m) : x + g.L0 * m;
-                const double e = ONSITE ? __ldg(g.eps + s) : g.shift;
+                const int row = NDIM == 3 ? y + g.L1 * m : m;  // x-row of the site
+                s = x + g.L0 * row;
+                const double e = ONSITE ? seps[s1 * g.TX * g.TY + ly0 * g.TX + lx0] : g.shift;
                 const double2 a1 = fma2(e, xc, scale2(g.t, nb));  // a_1 = H~ a_0 (Eq 17)
-                const long long ms = v.mem(s);
-                store_site(v, v.P, s, ms, rg, xc, false);
-                store_site(v, v.C, s, ms, rg, a1, false);
+                // memory site: x-rows carry a frame of xpad periodic images per side (3D)
+                const long long ms = (long long)row * (g.L0 + 2 * v.xpad) + x + v.xpad;
+                double2* pa = v.P + ms * v.RG + rg;
+                double2* pc = v.C + ms * v.RG + rg;
+                *pa = xc;
+                *pc = a1;
+                if (x < v.xpad) {  // (both images when L0 < 2 xpad)
+                    pa[(long long)g.L0 * v.RG] = xc;
+                    pc[(long long)g.L0 * v.RG] = a1;
+                }
+                if (x >= g.L0 - v.xpad && v.xpad) {
+                    pa[-(long long)g.L0 * v.RG] = xc;
+                    pc[-(long long)g.L0 * v.RG] = a1;
+                }
                 dot_acc<CPLX>(acc0, xc, xc);
                 dot_acc<CPLX>(acc1, xc, a1);
                 if (tail) dot_acc<CPLX>(acc2, a1, a1);

@@ -461,7 +461,10 @@ __global__ void dos_kernel(const double* __restrict__ c, int N, double a, double
     const double th = acos(x);
     double s = c[0];
     for (int n = 1; n < N; ++n) s = fma(c[n], cos((double)n * th), s);
-    rho[k] = s / (CUDART_PI * a * sqrt(1.0 - x * x));
+    // x^2 explicitly rounded (no FMA contraction into 1 - x^2): the same bits as the oracle, whose
+    // numpy arithmetic rounds x * x first -- near |x| = 1 the two roundings of 1 - x^2 differ relatively
+    // by eps / (1 - x^2), far above the expansion's own error (X27)
+    rho[k] = s / (CUDART_PI * a * sqrt(1.0 - __dmul_rn(x, x)));
 }
 
 // Retarded G(omega) = G~(x)/a (X24).  Inside (|x| < 1), theta = arccos x:
@@ -489,7 +492,7 @@ __global__ void green_kernel(const double* __restrict__ c, int N, double a, doub
         im = -sc / st;
     } else if (fabs(x) > 1.0) {
         const double sg = x > 0 ? 1.0 : -1.0;
-        const double sq = sqrt(x * x - 1.0);
+        const double sq = sqrt(__dmul_rn(x, x) - 1.0);  // x^2 rounded first, as the oracle (see dos_kernel)
         const double t = x - sg * sq;
         double s = 0.0;
         for (int n = N - 1; n >= 0; --n) s = fma(s, t, c[n]);
