@@ -132,8 +132,8 @@ def profiled_traffic(config, kname, R_loc, fmt):
         return None, None
     key = config if fmt in (None, "stencil") else f"{config}_{fmt}"
     rec = recs.get(f"{key}_R{R_loc}") or recs.get(key)
-    if not rec or rec.get("R_loc", R_loc) != R_loc:
-        return None, None
+    if not rec or rec.get("R_loc") != R_loc:
+        return None, None  # no capture of this config at this R per GPU
     if kname.split(" ")[0] not in rec.get("kernel", ""):
         return None, None  # the committed capture is of another kernel: no traffic claim
     return rec["dram_bytes_per_launch"], rec.get("round")

@@ -29,6 +29,7 @@
 #include "kpm_tma.cuh"
 #include "kpm_tma2.cuh"
 #include "kpm_tma3.cuh"
+#include "kpm_tri.cuh"
 // Kernels that are parity-green but measured slower than the default plan:
 // their templates are instantiated (launched) only under KPM_EXPERIMENTAL, i.e. in libkpm_exp.so,
 // and reached through kpm_plan_opts.experimental.  The default libkpm.so contains none of them.
@@ -157,6 +158,9 @@ struct Plan {
     bool use_tma2 = false, no_fused = false;
     size_t tma2_smem = 0;
     int TX2 = 0, tma2_minb = 1, tma2_grid = 0;  // two-step tile width, CTAs per SM, grid
+    // three steps per launch (kpm_tri.cuh), same tile as the two-step kernel; needs 4 vector blocks
+    bool use_tri = false;
+    size_t tri_smem = 0;
     // two steps per launch for 3D lattices (kpm_tma32.cuh); needs 4 vector blocks
     bool use_tma32 = false;
     int TX32 = 0, TY32 = 0, TL32 = 0, tma32_grid = 0, tma32_rr = 0;
@@ -452,6 +456,11 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
             const long long W2 = (long long)(RG / TL) * (h->L[0] / p->TX2) * Lm2;
             p->tma2_grid = (int)std::min<long long>(W2, (long long)p->tma2_minb * h->num_sms);
             p->use_tma2 = true;
+            // three steps per launch: the same row tile, sites of >= 128 bytes (8+ lanes)
+            const size_t smt = kpm::tri_smem_bytes(p->TX2, TL, on, p->RP);
+            p->use_tri = h->opts.three_step == 1 && TL >= 8 && TL <= 32 && TL * p->TX2 == 1024 && h->L[0] >= 8 &&
+                         h->L[1] >= 6 && smt <= (size_t)h->smem_optin;
+            p->tri_smem = smt;
         }
     }
     // KS-step kernel: 2D lattices, row tiles of TXK * TLK = 512 lanes (kpm_tmak.cuh)
@@ -521,7 +530,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->use_tmak) p->gx = std::max(p->gx, p->tmak_grid);
     if (p->use_tma32) p->gx = std::max(p->gx, p->tma32_grid);
     p->nslots = N;
-    if (h->rows) p->use_tma2 = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
+    if (h->rows) p->use_tma2 = p->use_tri = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
     p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL && !(flags & KPM_DIRECT) &&
                  !h->opts.no_overlap;
     if (p->overlap) p->gx = 3 * p->tma_grid;
@@ -555,6 +564,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_C = off; off = align_up(off + std::max(p->lane_bytes, with_r0 ? (size_t)p->R_loc * h->D * sizeof(double) : 0));
     p->off_R = off;
     if ((flags & KPM_DIRECT) && with_r0) off = align_up(off + p->lane_bytes);
+    if (p->use_tri && (p->M - 1 < 3 || !p->use_tma2)) p->use_tri = false;
     if (p->use_tma2 && p->M - 1 < 2) p->use_tma2 = false;
     if (p->use_tma32 && p->M - 1 < 2) p->use_tma32 = false;
     if (p->use_tma2 || p->use_tmak || p->use_tma32) {  // out-of-place multi-step launches: two spare blocks
@@ -726,13 +736,14 @@ kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& 
 
 // First step of a 2D/3D stencil with a_0 generated once per element (kpm_first.cuh).
 template <int NDIM, bool ONSITE, bool PEIERLS, bool CPLX>
-kpm_status launch_first_t(kpm_handle_s* h, const kpm::VecArgs& v, const kpm::FirstGeom& g, int grid, size_t smem, int tail) {
+kpm_status launch_first_t(kpm_handle_s* h, const kpm::VecArgs& v, const kpm::FirstGeom& g, int grid, size_t smem, int tail,
+                          int from_buf) {
     auto kern = kpm::kpm_first_tile_kernel<NDIM, ONSITE, PEIERLS, CPLX>;
     KPM_TRY(set_smem((const void*)kern, smem, h->device));
-    return launch_k(h, h->stream, kern, dim3(grid), dim3(kpm::kFirstThreads), smem, v, g, tail);
+    return launch_k(h, h->stream, kern, dim3(grid), dim3(kpm::kFirstThreads), smem, v, g, tail, from_buf);
 }
 
-kpm_status launch_first_tile(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail) {
+kpm_status launch_first_tile(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail, int from_buf) {
     kpm::FirstGeom g{};
     const int nd = h->ndim;
     g.L0 = (int)h->L[0];
@@ -763,15 +774,15 @@ kpm_status launch_first_tile(kpm_handle_s* h, const Plan& p, const kpm::VecArgs&
     if (smem > (size_t)h->smem_optin) return fail(KPM_ERR_UNSUPPORTED, "first-step tile does not fit shared memory");
     const bool on = h->d_eps != nullptr;
     if (is_cplx(h)) {
-        if (on) return launch_first_t<2, true, true, true>(h, v, g, grid, smem, tail);
-        return launch_first_t<2, false, true, true>(h, v, g, grid, smem, tail);
+        if (on) return launch_first_t<2, true, true, true>(h, v, g, grid, smem, tail, from_buf);
+        return launch_first_t<2, false, true, true>(h, v, g, grid, smem, tail, from_buf);
     }
     if (nd == 2) {
-        if (on) return launch_first_t<2, true, false, false>(h, v, g, grid, smem, tail);
-        return launch_first_t<2, false, false, false>(h, v, g, grid, smem, tail);
+        if (on) return launch_first_t<2, true, false, false>(h, v, g, grid, smem, tail, from_buf);
+        return launch_first_t<2, false, false, false>(h, v, g, grid, smem, tail, from_buf);
     }
-    if (on) return launch_first_t<3, true, false, false>(h, v, g, grid, smem, tail);
-    return launch_first_t<3, false, false, false>(h, v, g, grid, smem, tail);
+    if (on) return launch_first_t<3, true, false, false>(h, v, g, grid, smem, tail, from_buf);
+    return launch_first_t<3, false, false, false>(h, v, g, grid, smem, tail, from_buf);
 }
 
 #ifdef KPM_EXPERIMENTAL
@@ -860,6 +871,7 @@ struct BufMaps {
     const void* base = nullptr;
     CUtensorMap A, Col, Row, P, Col2;  // main, 1-site column, row, (=main), 2-site column (2D)
     CUtensorMap A2;                    // main box of the two-step kernel (width TX2)
+    CUtensorMap A3;                    // 3-site box of the three-step kernel
     CUtensorMap AK, AKH, AKH1;         // KS-step kernel: main (TXK), KS-site and (KS-1)-site boxes, TLK lanes
     CUtensorMap Box3, Row3;            // 3D dense-box kernel: (TX+2) x TY box, (TX+2)-site row
     CUtensorMap A32, A32r, P32, P32r;  // 3D two-step kernel: (TX+4) x TY, (TX+4) x 2, (TX+2) x TY, (TX+2) x 1
@@ -872,6 +884,7 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     KPM_TRY(make_vec_map(h, p, base, p.TX, 1, 1, &bm->Row));
     if (h->ndim == 2) KPM_TRY(make_vec_map(h, p, base, 2, 1, 1, &bm->Col2));
     if (p.use_tma2) KPM_TRY(make_vec_map(h, p, base, p.TX2, 1, 1, &bm->A2));
+    if (p.use_tri) KPM_TRY(make_vec_map(h, p, base, 3, 1, 1, &bm->A3));
     if (p.use_tma3) {
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, p.TY, 1, &bm->Box3));
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, 1, 1, &bm->Row3));
@@ -950,6 +963,36 @@ kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
     if (p.TL == 4 && p.TX2 == 256) return launch_tma2_s<4, 256, 1>(h, p, A, P, E, E2, g, tail);
     if (p.TL == 4 && p.TX2 == 64) return launch_tma2_s<4, 64, 2>(h, p, A, P, E, E2, g, tail);
     return fail(KPM_ERR_UNSUPPORTED, "no two-step kernel for TL=%d TX=%d", p.TL, p.TX2);
+}
+
+template <int TL, int TX, bool ONSITE, bool PEIERLS>
+kpm_status launch_tri_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                        const CUtensorMap& E4, const kpm::TriGeom& g, int tail) {
+    auto kern = kpm::kpm_step_tri_kernel<TL, TX, ONSITE, PEIERLS>;
+    KPM_TRY(set_smem((const void*)kern, p.tri_smem, h->device));
+    return launch_k(h, h->stream, kern, dim3(p.tma2_grid), dim3(kpm::kThreadsTri), p.tri_smem, A.A2, A.A3, P.A2, P.Col2, E,
+                    E4, g, tail);
+}
+
+template <int TL, int TX>
+kpm_status launch_tri_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                        const CUtensorMap& E4, const kpm::TriGeom& g, int tail) {
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) {
+        if (on) return launch_tri_t<TL, TX, true, true>(h, p, A, P, E, E4, g, tail);
+        return launch_tri_t<TL, TX, false, true>(h, p, A, P, E, E4, g, tail);
+    }
+    if (on) return launch_tri_t<TL, TX, true, false>(h, p, A, P, E, E4, g, tail);
+    return launch_tri_t<TL, TX, false, false>(h, p, A, P, E, E4, g, tail);
+}
+
+// instantiated tile shapes of the three-step kernel (TX * TL = 1024 lanes per row tile)
+kpm_status launch_tri(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                      const CUtensorMap& E4, const kpm::TriGeom& g, int tail) {
+    if (p.TL == 32 && p.TX2 == 32) return launch_tri_s<32, 32>(h, p, A, P, E, E4, g, tail);
+    if (p.TL == 16 && p.TX2 == 64) return launch_tri_s<16, 64>(h, p, A, P, E, E4, g, tail);
+    if (p.TL == 8 && p.TX2 == 128) return launch_tri_s<8, 128>(h, p, A, P, E, E4, g, tail);
+    return fail(KPM_ERR_UNSUPPORTED, "no three-step kernel for TL=%d TX=%d", p.TL, p.TX2);
 }
 
 #ifdef KPM_EXPERIMENTAL
@@ -1186,6 +1229,8 @@ struct Run {
     CUtensorMap mapEK, mapEKH;       // eps~: KS-step main box (TXK), KS-site box
     kpm::TmaGeom tg{};
     kpm::Tma2Geom tg2{};
+    kpm::TriGeom tgt{};
+    CUtensorMap mapE4;               // eps~: 4-site box (three-step kernel)
     kpm::TmaKGeom tgk{};
     kpm::Tma32Geom tg32{};
     CUtensorMap mapE32, mapE32r;     // eps~ frame: (TX+4) x TY box, (TX+4) x 1 box (3D two-step kernel)
@@ -1316,8 +1361,9 @@ struct Run {
         v.red2 = (!direct && N == 3) ? part + 2 * slot : nullptr;
         // 2D/3D stencils: a_0 hashed once per element into a shared-memory plane ring
         // (kpm_first.cuh); else the generic grid-stride kernel
-        if (first_mode == kpm::FIRST_GEN && h->kind == KIND_STENCIL && h->ndim >= 2 && !h->opts.no_first_tile)
-            KPM_TRY(launch_first_tile(h, p, v, v.red2 != nullptr));
+        if ((first_mode == kpm::FIRST_GEN || first_mode == kpm::FIRST_BUF) && h->kind == KIND_STENCIL && h->ndim >= 2 &&
+            !h->opts.no_first_tile)
+            KPM_TRY(launch_first_tile(h, p, v, v.red2 != nullptr, first_mode == kpm::FIRST_BUF));
         else
             KPM_TRY(launch(h, p, first_mode, v, v.red2 != nullptr));
 
@@ -1327,6 +1373,7 @@ struct Run {
         nsteps = direct ? std::max(0, N - 2) : std::max(0, p.M - 1);
         memset(&mapE, 0, sizeof mapE);
         memset(&mapE2, 0, sizeof mapE2);
+        memset(&mapE4, 0, sizeof mapE4);
         memset(&mapEf, 0, sizeof mapEf);
         memset(&mapEK, 0, sizeof mapEK);
         memset(&mapEKH, 0, sizeof mapEKH);
@@ -1342,6 +1389,7 @@ struct Run {
                     KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
                     KPM_TRY(make_eps_map_w(h, p, p.TX2, &mapEf));
                 }
+                if (p.use_tri) KPM_TRY(make_eps_map_w(h, p, 4, &mapE4));
                 if (p.use_tma32) {
                     KPM_TRY(make_epsf_map(h, p.TX32 + 4, p.TY32, &mapE32));
                     KPM_TRY(make_epsf_map(h, p.TX32 + 4, 1, &mapE32r));
@@ -1389,6 +1437,19 @@ struct Run {
             tg2.t = tg.t;
             tg2.shift = tg.shift;
             tg2.phase = tg.phase;
+            tgt.L0 = tg2.L0;
+            tgt.L1 = tg2.L1;
+            tgt.TX = tg2.TX;
+            tgt.TL = tg2.TL;
+            tgt.RG = tg2.RG;
+            tgt.G_L = tg2.G_L;
+            tgt.PX = tg2.PX;
+            tgt.W = tg2.W;
+            tgt.RP = tg2.RP;
+            tgt.rows_total = p.gx;
+            tgt.t = tg.t;
+            tgt.shift = tg.shift;
+            tgt.phase = tg.phase;
             tgk.L0 = tg.L0;
             tgk.L1 = tg.L1;
             tgk.TX = p.TXK;
@@ -1618,7 +1679,31 @@ struct Run {
             n += 2;
             return KPM_OK;
         }
-        const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps && !(n == 1 && (nsteps & 1));
+        // three-step launches (kpm_tri.cuh): the remainder of the step count goes first as one pair
+        // or one single step, then every launch advances three steps
+        const int left = nsteps - n + 1;
+        if (!direct && p.use_tri && left >= 3 && left % 3 == 0) {
+            // steps n, n+1, n+2: slots 2n .. 2n+5 (+ odd-N tail 2n+6)
+            const bool tail = (N & 1) && n + 2 == nsteps;
+            for (int k = 0; k < 6; ++k) tgt.red[k] = part + (size_t)(2 * n + k) * slot;
+            tgt.red[6] = tail ? part + (size_t)(2 * n + 6) * slot : nullptr;
+            tgt.outB = spare0;
+            tgt.outC = spare1;
+            KPM_TRY(launch_tri(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapEf, mapE4, tgt, tail));
+            double2* oc = cur;
+            double2* op = prev;
+            cur = spare1;
+            prev = spare0;
+            spare0 = oc;
+            spare1 = op;
+            h->steps_bytes += 3.0 * (3.0 * vbytes + ebytes);  // three steps
+            h->design_bytes += 4.0 * vbytes + ebytes;         // a_n, a_{n-1} read, a_{n+2}, a_{n+3} written once
+            h->step_launches++;
+            n += 3;
+            return KPM_OK;
+        }
+        const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps &&
+                          (p.use_tri ? left % 3 == 2 : !(n == 1 && (nsteps & 1)));
         if (pair) {
             // steps n and n+1: slots 2n .. 2n+3 (+ odd-N tail 2n+4)
             const bool tail = (N & 1) && n + 1 == nsteps;
@@ -2613,7 +2698,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[8] = p.use_tma2 ? p.TX2 : (p.use_tma32 ? p.TX32 * 100 + p.TY32 : 0);
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;
-    info[11] = p.use_tmak ? p.KSK : 0;
+    info[11] = p.use_tmak ? p.KSK : (p.use_tri ? 3 : 0);
     if (p.use_persist) info[7] |= 32;
     return KPM_OK;
 }
@@ -2639,12 +2724,12 @@ kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
     }
     const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
                          o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
-                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile};
+                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile, o->three_step};
     for (int32_t x : f)
         if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
     for (int32_t x : o->reserved)
         if (x != 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: reserved words must be 0");
-    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2)
+    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2 || o->three_step > 1)
         return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: value out of range");
 #ifndef KPM_EXPERIMENTAL
     if (o->experimental) return fail(KPM_ERR_UNSUPPORTED, "experimental kernels are built into libkpm_exp.so only");

@@ -1,5 +1,6 @@
 // kpm_first.cuh -- the first recursion step for 2D/3D lattice stencils:
-//     a_0 = r (Rademacher, Eq 14-15, generated on the GPU as the paper does),
+//     a_0 = r (Rademacher, Eq 14-15, generated on the GPU as the paper does; or the
+//           caller's start block, from_buf = 1, read from the buffer -- the same summation order),
 //     a_1 = H~ a_0 (Eq 17),   S_0 = <a_0|a_0>,  S_1 = <a_0|a_1>  (+ the odd-N tail <a_1|a_1>).
 //
 // The generic grid-stride kernel regenerates the counter hash of a_0 for a site AND for each of
@@ -40,7 +41,8 @@ __host__ __device__ inline size_t first_smem_bytes(int ndim, int TX, int TY, int
 }
 
 template <int NDIM, bool ONSITE, bool PEIERLS, bool CPLX>
-__global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const VecArgs v, const FirstGeom g, const int tail) {
+__global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const VecArgs v, const FirstGeom g, const int tail,
+                                                                         const int from_buf) {
     pdl_entry();
     extern __shared__ __align__(128) unsigned char smem[];  // (every extern smem declaration of the TU must agree: TMA destinations need 128)
     const int PXs = g.TX + 2, PYs = NDIM == 3 ? g.TY + 2 : 1;
@@ -87,7 +89,16 @@ __global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const Vec
                     y = y < 0 ? y + g.L1 : (y >= g.L1 ? y - g.L1 : y);
                     j += g.L0 * y;
                 }
-                dst[s * g.TL + l] = rg < v.RG ? gen_lane<CPLX>(v, j, rg) : make_double2(0.0, 0.0);
+                double2 a0 = make_double2(0.0, 0.0);
+                if (rg < v.RG) {
+                    if (from_buf) {  // the caller's start block, already in lane layout in P
+                        const int row = j >= 0 ? j / g.L0 : -((-j + g.L0 - 1) / g.L0);
+                        a0 = v.P[((long long)row * (g.L0 + 2 * v.xpad) + x + v.xpad) * v.RG + rg];
+                    } else {
+                        a0 = gen_lane<CPLX>(v, j, rg);
+                    }
+                }
+                dst[s * g.TL + l] = a0;
                 // eps~ of the interior sites, staged with the plane (a dependent global load per
                 // element stalled the compute loop: ncu long-scoreboard on the a_1 FMA)
                 if (ONSITE && l == 0 && tx >= 1 && tx <= g.TX && ty >= (NDIM == 3 ? 1 : 0) &&
@@ -145,14 +156,14 @@ __global__ void __launch_bounds__(kFirstThreads) kpm_first_tile_kernel(const Vec
                 const long long ms = (long long)row * (g.L0 + 2 * v.xpad) + x + v.xpad;
                 double2* pa = v.P + ms * v.RG + rg;
                 double2* pc = v.C + ms * v.RG + rg;
-                *pa = xc;
+                if (!from_buf) *pa = xc;
                 *pc = a1;
                 if (x < v.xpad) {  // (both images when L0 < 2 xpad)
-                    pa[(long long)g.L0 * v.RG] = xc;
+                    if (!from_buf) pa[(long long)g.L0 * v.RG] = xc;
                     pc[(long long)g.L0 * v.RG] = a1;
                 }
                 if (x >= g.L0 - v.xpad && v.xpad) {
-                    pa[-(long long)g.L0 * v.RG] = xc;
+                    if (!from_buf) pa[-(long long)g.L0 * v.RG] = xc;
                     pc[-(long long)g.L0 * v.RG] = a1;
                 }
                 dot_acc<CPLX>(acc0, xc, xc);

@@ -1,0 +1,344 @@
+// kpm_tri.cuh -- THREE recursion steps per HBM pass (temporal blocking), 2D lattices.
+//
+// One launch advances the recursion by three steps (Eq 18 three times):
+//     a_{n+1} = 2 H~ a_n - a_{n-1},  a_{n+2} = 2 H~ a_{n+1} - a_n,  a_{n+3} = 2 H~ a_{n+2} - a_{n+1},
+// reading a_n and a_{n-1} from HBM once and writing a_{n+2} and a_{n+3} once: 4 D R s bytes per
+// three steps (the two-step kernel, kpm_tma2.cuh, moves 4 D R s per two; single steps 3 D R s per
+// one).  a_{n+1} and a_{n+2} live in shared-memory row rings.
+//
+// Same march as kpm_tma2.cuh (pencil of TX sites x TL lanes, rows of y), one level deeper:
+//   level 0  a_n      rows m0-3 .. m1+2, sites x0-3 .. x0+TX+2  (TMA: main box + two 3-site boxes)
+//   level -1 a_{n-1}  rows m0-2 .. m1+1, sites x0-2 .. x0+TX+1  (TMA: main box + two 2-site boxes)
+//   level 1  a_{n+1}  rows m0-2 .. m1+1, sites x0-2 .. x0+TX+1  (computed, 3-row ring B1)
+//   level 2  a_{n+2}  rows m0-1 .. m1,   sites x0-1 .. x0+TX    (computed, 2-row ring B2; rows m0..m1-1
+//                                                                of sites x0..x0+TX-1 stored)
+//   level 3  a_{n+3}  rows m0 .. m1-1,   sites x0 .. x0+TX-1    (stored)
+// Iteration q of a segment computes level 1 at row r1 = m0-2+q, level 2 at r1-1 and level 3 at
+// r1-2.  Interior sites: 8 warps, each thread NPI sites of a row; its level-1 and level-2 values
+// of the last rows roll in registers (the y-neighbours and the "- a_{n-1}" terms of the next
+// levels), x-neighbours and level 0 come from shared memory.  The halo sites (level 1: x0-2,
+// x0-1, x0+TX, x0+TX+1; level 2: x0-1, x0+TX) are spread over the first 4 TL threads: thread
+// t < 2 TL computes level 1 and then level 2 at x0-1 or x0+TX (its own level-1 value is the
+// level-2 y-neighbour, so no barrier between them), threads 2 TL .. 4 TL - 1 level 1 at x0-2 or
+// x0+TX+1.  (A ninth warp for the halo would cap registers at 168 -- 3 warps on one SM
+// sub-partition -- and spilled.)  The last thread issues the TMA refills.  One CTA barrier per row.
+//
+// Reductions: <a_n|a_n>, <a_n|a_{n+1}>, <a_{n+1}|a_{n+1}>, <a_{n+1}|a_{n+2}>, <a_{n+2}|a_{n+2}>,
+// <a_{n+2}|a_{n+3}> (and the odd-N tail <a_{n+3}|a_{n+3}>) over owned sites, per lane, fixed order.
+#pragma once
+#include "kpm_tma2.cuh"
+
+namespace kpm {
+
+struct TriGeom {
+    int L0, L1;          // lattice extents
+    int TX, TL, RG, G_L, PX;
+    long long W;         // output rows = G_L * PX * L1
+    int RP;
+    int rows_total;      // partial-sum rows per slot (>= gridDim.x; extra rows are zeroed)
+    double t, shift;
+    const double2* phase;
+    double* red[7];      // slots 2n .. 2n+5, (tail) 2n+6; red[6] nullable
+    double2* outB;       // a_{n+2}
+    double2* outC;       // a_{n+3}
+};
+
+constexpr int kThreadsTri = 256;       // 8 warps: two per SM sub-partition, up to 255 registers
+constexpr int kSAT = 4;                // a_n ring
+constexpr int kSPT = 2;                // a_{n-1} ring
+
+// a_n slot: [3 halo sites][TX][3 halo sites], then eps~ as three 128-byte aligned pieces
+// [4 left (x0-4 ..)][TX][4 right] (TMA boxes need 16-byte multiples); a_{n-1} slot
+// [2][TX][2]; B1 rows [2][TX][2] sites; B2 rows [1][TX][1].
+struct TriLayout {
+    int site, a_bytes, eps_l, eps_m, eps_r, p_bytes, b1_bytes, b2_bytes;
+    __host__ __device__ constexpr TriLayout(int TX, int TL, bool onsite)
+        : site(TL * 16),
+          a_bytes(onsite ? (TX + 6) * TL * 16 + 128 + (TX * 8 + 127) / 128 * 128 + 128 : (TX + 6) * TL * 16),
+          eps_l((TX + 6) * TL * 16),
+          eps_m((TX + 6) * TL * 16 + 128),
+          eps_r((TX + 6) * TL * 16 + 128 + (TX * 8 + 127) / 128 * 128),
+          p_bytes(((TX + 4) * TL * 16 + 127) / 128 * 128),
+          b1_bytes(((TX + 4) * TL * 16 + 127) / 128 * 128),
+          b2_bytes(((TX + 2) * TL * 16 + 127) / 128 * 128) {}
+    // eps~ at tile x index lx in [-4, TX+3]
+    __device__ __forceinline__ double eps(const unsigned char* slot, int lx, int TX) const {
+        return *reinterpret_cast<const double*>(
+            slot + (lx < 0 ? eps_l + (lx + 4) * 8 : (lx < TX ? eps_m + lx * 8 : eps_r + (lx - TX) * 8)));
+    }
+};
+
+__host__ __device__ inline size_t tri_smem_bytes(int TX, int TL, bool onsite, int RP) {
+    const TriLayout S(TX, TL, onsite);
+    return (size_t)kSAT * S.a_bytes + (size_t)kSPT * S.p_bytes + 3 * (size_t)S.b1_bytes + 2 * (size_t)S.b2_bytes +
+           7 * (size_t)RP * 8 + (size_t)kThreadsTri * 16 + (size_t)(TX + 6) * 16 + (kSAT + kSPT) * 8;
+}
+
+template <int TL, int TX, bool ONSITE, bool PEIERLS>
+__global__ void __launch_bounds__(kThreadsTri, 1)
+    kpm_step_tri_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
+                        const __grid_constant__ CUtensorMap mapA3,   // a_n 3-site box {2TL, 3, 1}
+                        const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
+                        const __grid_constant__ CUtensorMap mapP2,   // a_{n-1} 2-site box {2TL, 2, 1}
+                        const __grid_constant__ CUtensorMap mapE,    // eps~ box {TX, 1}
+                        const __grid_constant__ CUtensorMap mapE4,   // eps~ box {4, 1}
+                        const TriGeom g, const int tail) {
+    pdl_entry();
+    constexpr int CONS = 256;
+    constexpr int PRODUCER = CONS - 1;  // (no halo work: 4 TL <= 128 < 255)
+    constexpr int KSTEP = CONS / TL;  // tile sites per pass
+    constexpr int NPI = TX / KSTEP;   // interior sites per thread
+    static_assert(TX % KSTEP == 0 && TL * 16 >= 128, "tile shape");
+    constexpr int SITE = TL * 16;
+    constexpr TriLayout SL(TX, TL, ONSITE);
+    extern __shared__ __align__(128) unsigned char smem[];
+    unsigned char* ringA = smem;
+    unsigned char* ringP = ringA + kSAT * SL.a_bytes;
+    unsigned char* ringB1 = ringP + kSPT * SL.p_bytes;
+    unsigned char* ringB2 = ringB1 + 3 * SL.b1_bytes;
+    double* sacc = reinterpret_cast<double*>(ringB2 + 2 * SL.b2_bytes);  // [7][RP]
+    double2* sred = reinterpret_cast<double2*>(sacc + 7 * g.RP);           // [CONS]
+    double2* sphase = sred + CONS;                                         // [TX + 6]: x0-3 .. x0+TX+2
+    uint64_t* fullA = reinterpret_cast<uint64_t*>(sphase + TX + 6);
+    uint64_t* fullP = fullA + kSAT;
+
+    const int t = threadIdx.x;
+    const long long w_begin = g.W * blockIdx.x / gridDim.x;
+    const long long w_end = g.W * (blockIdx.x + 1) / gridDim.x;
+
+    // ---- producer state (thread CONS only; in shared memory)
+    __shared__ LoadCursor cur_smem[2];
+    __shared__ uint64_t pol_smem;
+    LoadCursor& ca = cur_smem[0];
+    LoadCursor& cp = cur_smem[1];
+    auto issueA = [&](int slot) {  // next a_n row (3-site halos) into `slot`
+        if (!ca.valid) return;
+        const int row = ca.row, c0 = ca.c0, x0 = ca.x0, xl = ca.xl, xr = ca.xr;
+        unsigned char* dst = ringA + slot * SL.a_bytes;
+        mbar_expect_tx(fullA + slot, (TX + 6) * SITE + (ONSITE ? (TX + 8) * 8 : 0));
+        tma_load(dst, &mapA3, fullA + slot, c0, xl, row);
+        tma_load(dst + 3 * SITE, &mapA, fullA + slot, c0, x0, row);
+        tma_load(dst + (TX + 3) * SITE, &mapA3, fullA + slot, c0, xr, row);
+        if (ONSITE) {
+            int xe = x0 - 4;
+            if (xe < 0) xe += g.L0;
+            tma_load_2d(dst + SL.eps_l, &mapE4, fullA + slot, xe, row);
+            tma_load_2d(dst + SL.eps_m, &mapE, fullA + slot, x0, row);
+            tma_load_2d(dst + SL.eps_r, &mapE4, fullA + slot, xr, row);
+        }
+        ca.next(g, 6);
+    };
+    auto issueP = [&](int slot) {  // next a_{n-1} row (2-site halos) into `slot`
+        if (!cp.valid) return;
+        const int row = cp.row, c0 = cp.c0, x0 = cp.x0, xl = cp.xl, xr = cp.xr;
+        unsigned char* dst = ringP + slot * SL.p_bytes;
+        mbar_expect_tx(fullP + slot, (TX + 4) * SITE);
+        const uint64_t pol = pol_smem;
+        tma_load_hint(dst, &mapP2, fullP + slot, c0, xl, row, pol);
+        tma_load_hint(dst + 2 * SITE, &mapP, fullP + slot, c0, x0, row, pol);
+        tma_load_hint(dst + (TX + 2) * SITE, &mapP2, fullP + slot, c0, xr, row, pol);
+        cp.next(g, 4);
+    };
+    if (t == PRODUCER) {
+        for (int i = 0; i < kSAT; ++i) mbar_init(fullA + i, 1);
+        for (int i = 0; i < kSPT; ++i) mbar_init(fullP + i, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        prefetch_tmap(&mapA);
+        prefetch_tmap(&mapA3);
+        prefetch_tmap(&mapP);
+        prefetch_tmap(&mapP2);
+        if (ONSITE) {
+            prefetch_tmap(&mapE);
+            prefetch_tmap(&mapE4);
+        }
+        pol_smem = policy_evict_first();
+        ca.init(g, w_begin, w_end, 6);
+        cp.init(g, w_begin, w_end, 4);
+        for (int i = 0; i < kSAT; ++i) issueA(i);
+        for (int i = 0; i < kSPT; ++i) issueP(i);
+    }
+    for (int i = t; i < 7 * g.RP; i += blockDim.x) sacc[i] = 0.0;
+    __syncthreads();
+
+    const int l = t % TL;
+    const int k0 = t / TL;
+    const int lo = l * 16;
+    double2 acc[7];
+#pragma unroll
+    for (int k = 0; k < 7; ++k) acc[k] = make_double2(0.0, 0.0);
+    auto ld = [](const unsigned char* p) { return *reinterpret_cast<const double2*>(p); };
+    auto st = [](unsigned char* p, double2 v) { *reinterpret_cast<double2*>(p) = v; };
+    auto flush = [&](int lgf) {
+#pragma unroll
+        for (int k = 0; k < 7; ++k) {
+            sred[t] = acc[k];
+            __syncthreads();
+            if (t < TL) {
+                double2 s = make_double2(0.0, 0.0);
+                for (int j = t; j < CONS; j += TL) s = add2(s, sred[j]);
+                const int v = lgf * TL + t;
+                if (PEIERLS) {
+                    sacc[k * g.RP + v] += s.x;
+                } else {
+                    sacc[k * g.RP + 2 * v] += s.x;
+                    sacc[k * g.RP + 2 * v + 1] += s.y;
+                }
+            }
+            __syncthreads();
+        }
+#pragma unroll
+        for (int k = 0; k < 7; ++k) acc[k] = make_double2(0.0, 0.0);
+    };
+    // 2 H~ x - p from the 4 neighbours (y neighbours carry the Peierls phase) and the site value
+    auto step_val = [&](double2 x, double2 xm, double2 xp, double2 ym, double2 yp, double e, double2 ph, double2 p) {
+        double2 nb = add2(xm, xp);
+        if (PEIERLS) nb = add2(nb, add2(cmulc(ph, yp), cmul(ph, ym)));
+        else nb = add2(nb, add2(ym, yp));
+        const double2 h = fma2(e, x, scale2(g.t, nb));
+        return make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));
+    };
+    // slot byte offsets of tile x index lx (level 0: [-3, TX+2]; level -1 and 1: [-2, TX+1]; level 2: [-1, TX])
+    auto oA = [&](int lx, int ll) { return (lx + 3) * SITE + ll * 16; };
+    auto oP = [&](int lx, int ll) { return (lx + 2) * SITE + ll * 16; };
+    auto oB2 = [&](int lx, int ll) { return (lx + 1) * SITE + ll * 16; };
+
+    LoadCursor cs;  // segment iterator of the consumers (same sequence)
+    cs.init(g, w_begin, w_end, 0);
+    int ia = 0, ip = 0, cur_lg = -1;
+    while (cs.valid) {
+        const int lg = cs.lg, m0 = cs.m0, H = cs.H, x0 = cs.px * TX;
+        if (cur_lg != -1 && lg != cur_lg) flush(cur_lg);
+        cur_lg = lg;
+        const long long g0 = (long long)(x0 + k0) * g.RG + (long long)lg * TL + l;
+        const long long gstep = (long long)KSTEP * g.RG;
+        const long long growstep = (long long)g.L0 * g.RG;
+        if (PEIERLS) {
+            if (t < TX + 6) sphase[t] = __ldg(g.phase + (x0 + t - 3 + 2 * g.L0) % g.L0);
+            __syncthreads();
+        }
+        const int ia_seg = ia;
+        int s0 = ia_seg % kSAT;        // ring slot of a_n row r1-1
+        int ps = ip % kSPT;
+        int r2 = (m0 - 3 + 2 * g.L1) % g.L1;  // level-2 row of iteration 0
+        int r3 = (m0 - 4 + 2 * g.L1) % g.L1;  // level-3 row
+        // per interior site: level 1 rows r1-2, r1-1 (bm, bc); level 2 rows r2-2, r2-1 (cm, cc);
+        // eps~ at rows r1-1, r1-2 (e2, e3)
+        double2 bm[NPI], bc[NPI], cm[NPI], cc[NPI];
+        double e2[NPI], e3[NPI];
+        for (int q = 0; q < H + 4; ++q) {
+            const int i0 = ia_seg + q;
+            const int s1 = s0 + 1 == kSAT ? 0 : s0 + 1;
+            const int s2 = s1 + 1 == kSAT ? 0 : s1 + 1;
+            if (q == 0) {
+                mbar_wait(fullA + s0, (uint32_t)((i0 / kSAT) & 1));
+                mbar_wait(fullA + s1, (uint32_t)(((i0 + 1) / kSAT) & 1));
+            }
+            mbar_wait(fullA + s2, (uint32_t)(((i0 + 2) / kSAT) & 1));
+            mbar_wait(fullP + ps, (uint32_t)((ip / kSPT) & 1));
+            const unsigned char* A0 = ringA + s0 * SL.a_bytes;  // a_n row r1-1
+            const unsigned char* A1 = ringA + s1 * SL.a_bytes;  // a_n row r1
+            const unsigned char* A2 = ringA + s2 * SL.a_bytes;  // a_n row r1+1
+            const unsigned char* Pq = ringP + ps * SL.p_bytes;  // a_{n-1} row r1
+            const int b1n = q % 3;
+            unsigned char* B1n = ringB1 + b1n * SL.b1_bytes;                           // level 1 row r1 (written)
+            const unsigned char* B1c = ringB1 + (b1n == 0 ? 2 : b1n - 1) * SL.b1_bytes;  // row r1-1
+            const unsigned char* B1m = ringB1 + (b1n == 2 ? 0 : b1n + 1) * SL.b1_bytes;  // row r1-2
+            unsigned char* B2n = ringB2 + (q & 1) * SL.b2_bytes;                      // level 2 row r2 (written)
+            const unsigned char* B2c = ringB2 + ((q & 1) ^ 1) * SL.b2_bytes;          // level 2 row r2-1 = r3
+            const bool do2 = q >= 2, do3 = q >= 4;
+            const bool own1 = q >= 2 && q < H + 2;  // r1 in [m0, m1)
+            const bool own2 = q >= 3 && q < H + 3;  // r2 in [m0, m1)
+            double2* outB = g.outB + r2 * growstep + g0;
+            double2* outC = g.outC + r3 * growstep + g0;
+            // halo sites of this thread (level 1 at hx1; level 2 at hx1 when hx1 is -1 or TX)
+            if (t < 4 * TL) {
+                const int hg = t / TL, hl = t % TL;  // 0: x0-1, 1: x0+TX, 2: x0-2, 3: x0+TX+1
+                const int hx = hg == 0 ? -1 : (hg == 1 ? TX : (hg == 2 ? -2 : TX + 1));
+                const double2 ph = PEIERLS ? sphase[hx + 3] : make_double2(0.0, 0.0);
+                const double e1 = ONSITE ? SL.eps(A1, hx, TX) : g.shift;
+                const double2 b = step_val(ld(A1 + oA(hx, hl)), ld(A1 + oA(hx - 1, hl)), ld(A1 + oA(hx + 1, hl)),
+                                           ld(A0 + oA(hx, hl)), ld(A2 + oA(hx, hl)), e1, ph, ld(Pq + oP(hx, hl)));
+                st(B1n + oP(hx, hl), b);
+                if (hg < 2 && do2) {
+                    const double e = ONSITE ? SL.eps(A0, hx, TX) : g.shift;
+                    const double2 c = step_val(ld(B1c + oP(hx, hl)), ld(B1c + oP(hx - 1, hl)), ld(B1c + oP(hx + 1, hl)),
+                                               ld(B1m + oP(hx, hl)), b, e, ph, ld(A0 + oA(hx, hl)));
+                    st(B2n + oB2(hx, hl), c);
+                }
+            }
+#pragma unroll
+            for (int p = 0; p < NPI; ++p) {
+                const int lx = k0 + p * KSTEP;
+                const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                // level 1 at row r1
+                const double2 x = ld(A1 + oA(lx, l));
+                const double e1 = ONSITE ? reinterpret_cast<const double*>(A1 + SL.eps_m)[lx] : g.shift;
+                const double2 b = step_val(x, ld(A1 + oA(lx - 1, l)), ld(A1 + oA(lx + 1, l)), ld(A0 + oA(lx, l)),
+                                           ld(A2 + oA(lx, l)), e1, ph, ld(Pq + oP(lx, l)));
+                st(B1n + oP(lx, l), b);
+                if (own1) {
+                    dot_acc<PEIERLS>(acc[0], x, x);
+                    dot_acc<PEIERLS>(acc[1], x, b);
+                }
+                // level 2 at row r2 = r1-1: centre bc, y-neighbours bm, b; "- a_n" at row r1-1
+                double2 c = make_double2(0.0, 0.0);
+                if (do2) {
+                    c = step_val(bc[p], ld(B1c + oP(lx - 1, l)), ld(B1c + oP(lx + 1, l)), bm[p], b,
+                                 ONSITE ? e2[p] : g.shift, ph, ld(A0 + oA(lx, l)));
+                    st(B2n + oB2(lx, l), c);
+                    if (own2) {
+                        __stcs(outB + p * gstep, c);
+                        dot_acc<PEIERLS>(acc[2], bc[p], bc[p]);
+                        dot_acc<PEIERLS>(acc[3], bc[p], c);
+                    }
+                }
+                // level 3 at row r3 = r1-2: centre cc, y-neighbours cm, c; "- a_{n+1}" at row r1-2 = bm
+                if (do3) {
+                    const double2 d = step_val(cc[p], ld(B2c + oB2(lx - 1, l)), ld(B2c + oB2(lx + 1, l)), cm[p], c,
+                                               ONSITE ? e3[p] : g.shift, ph, bm[p]);
+                    __stcs(outC + p * gstep, d);
+                    dot_acc<PEIERLS>(acc[4], cc[p], cc[p]);
+                    dot_acc<PEIERLS>(acc[5], cc[p], d);
+                    if (tail) dot_acc<PEIERLS>(acc[6], d, d);
+                }
+                // roll one row down
+                bm[p] = bc[p];
+                bc[p] = b;
+                cm[p] = cc[p];
+                cc[p] = c;
+                if (ONSITE) {
+                    e3[p] = e2[p];
+                    e2[p] = e1;
+                }
+            }
+            __syncthreads();  // row q done: a_n row r1-1 and a_{n-1} row r1 are free; B rings advance
+            if (t == PRODUCER) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                issueA(s0);
+                issueP(ps);
+            }
+            ++ip;
+            s0 = s1;
+            ps = ps + 1 == kSPT ? 0 : ps + 1;
+            r2 = r2 + 1 == g.L1 ? 0 : r2 + 1;
+            r3 = r3 + 1 == g.L1 ? 0 : r3 + 1;
+        }
+        if (t == PRODUCER) {  // the segment's last two a_n rows are free too
+            issueA((ia_seg + H + 4) % kSAT);
+            issueA((ia_seg + H + 5) % kSAT);
+        }
+        ia = ia_seg + H + 6;
+        cs.seg(g, 0);
+    }
+    if (cur_lg != -1) flush(cur_lg);
+    __syncthreads();
+    for (int k = 0; k < 7; ++k) {
+        double* rowk = g.red[k];
+        if (rowk == nullptr || (k == 6 && !tail)) continue;
+        for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + v] = sacc[k * g.RP + v];
+        for (int rr = blockIdx.x + gridDim.x; rr < g.rows_total; rr += gridDim.x)
+            for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)rr * g.RP + v] = 0.0;
+    }
+}
+
+}  // namespace kpm

@@ -498,3 +498,32 @@ def test_first_step_tile_kernel(kpm, case, first_tile):
                                 dist=(kpm.KPM_PART_ROWS, 0, 1, kpm.KPM_COMM_SELF))
     hr.set_plan_opts(no_first_tile=int(not first_tile))
     assert normwise(hr.moments(N, R, 17), oracle.moments_doubling(H, a, b, r, N)) < TOL
+
+
+@pytest.mark.parametrize("case", ["2d_R64", "2d_anderson_R16", "2d_peierls_R32", "2d_R8_four_lanes"])
+@pytest.mark.parametrize("N", [7, 8, 9, 10, 11, 12, 13, 15, 16, 40])
+def test_three_step_kernel(kpm, case, N):
+    """2D: three recursion steps per launch (kpm_tri.cuh), the step-count remainder as a leading
+    pair or single step, odd-N tail inside the last launch: the oracle's moments, per vector too,
+    and the same launch count the schedule implies.  (4-lane tiles keep the two-step kernel.)"""
+    lat, _, R = TMA_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b += 0.01 * a
+    a *= 1.02
+    r = ki.rademacher(19, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b, no_small=1, three_step=1)
+    info = h.plan_info(N, R)
+    nsteps = N // 2 - 1
+    tri = info["two_step"] == 1 and info["TL"] >= 8 and nsteps >= 3
+    assert info["ks"] == (3 if tri else 0), info
+    mu = h.moments(N, R, 19)
+    assert normwise(mu, ref) < TOL
+    assert normwise(h.moments_ex(N, R, 19, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
+    assert np.array_equal(h.moments_ex(N, R, 19, r0=r), mu)
+    assert np.array_equal(h.moments(N, R, 19), mu), "not deterministic"
+    if tri:
+        _, launches, _ = h.last_timing()
+        rem = nsteps % 3
+        assert launches == nsteps // 3 + (1 if rem else 0), (launches, nsteps)
