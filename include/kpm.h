@@ -237,9 +237,10 @@ typedef struct {
                               launches (PDL: the next kernel's prologue overlaps this one's tail) */
     int32_t no_first_tile; /* 1: first step by the generic grid-stride kernel (a_0 hashed per neighbour)
                               instead of the plane-ring tile kernel (2D/3D stencils) */
-    int32_t three_step;    /* 1: three recursion steps per launch for 2D lattices (kpm_tri.cuh: 4 D R s
-                              bytes per three steps) where the two-step kernel would run */
-    int32_t reserved[4];   /* must be 0 */
+    int32_t no_three_step; /* 1: no three-steps-per-launch kernel for 2D lattices (kpm_tri.cuh: 4 D R s
+                              bytes per three steps; tiles of >= 8 lanes): the two-step kernel */
+    int32_t no_zorder;     /* 1: 3D round-robin march in row-major pencil order instead of Z order */
+    int32_t reserved[3];   /* must be 0 */
 } kpm_plan_opts;
 
 /* Set (opts != NULL) or reset to the default (opts == NULL) the plan options of h.

@@ -458,7 +458,7 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
             p->use_tma2 = true;
             // three steps per launch: the same row tile, sites of >= 128 bytes (8+ lanes)
             const size_t smt = kpm::tri_smem_bytes(p->TX2, TL, on, p->RP);
-            p->use_tri = h->opts.three_step == 1 && TL >= 8 && TL <= 32 && TL * p->TX2 == 1024 && h->L[0] >= 8 &&
+            p->use_tri = !h->opts.no_three_step && TL >= 8 && TL <= 32 && TL * p->TX2 == 1024 && h->L[0] >= 8 &&
                          h->L[1] >= 6 && smt <= (size_t)h->smem_optin;
             p->tri_smem = smt;
         }
@@ -748,7 +748,9 @@ kpm_status launch_first_tile(kpm_handle_s* h, const Plan& p, const kpm::VecArgs&
     const int nd = h->ndim;
     g.L0 = (int)h->L[0];
     g.L1 = (int)h->L[1];
-    g.TL = std::min(nd == 3 ? 8 : 16, p.RG);
+    // lanes per tile: a power of two (it must divide the 512 threads), masked when RG is not a multiple
+    g.TL = 1;
+    while (g.TL * 2 <= std::min(nd == 3 ? 8 : 16, p.RG)) g.TL *= 2;
     g.TX = (int)std::min<int64_t>(nd == 3 ? 16 : 64, h->L[0]);
     g.TY = nd == 3 ? (int)std::min<int64_t>(16, h->L[1]) : 1;
     g.PX = (g.L0 + g.TX - 1) / g.TX;
@@ -1412,6 +1414,12 @@ struct Run {
             tg.Lm = (int)(h->ndim == 2 ? h->L[1] : h->L[2]);
             tg.W = (long long)tg.G_L * tg.PX * tg.PY * tg.Lm;
             tg.rr = p.tma_rr;
+            {
+                auto log2i = [](int v) { int b = 0; while ((1 << b) < v) ++b; return (1 << b) == v ? b : -1; };
+                const int bx = log2i(tg.PX), by = log2i(tg.PY);
+                tg.zbx = (bx >= 0 && by >= 0 && h->ndim == 3 && !h->opts.no_zorder) ? bx : -1;
+                tg.zby = tg.zbx >= 0 ? by : -1;
+            }
             tg.ghost = h->rows ? 1 : 0;
             tg.RP = p.RP;
             tg.rows_total = p.gx;
@@ -2724,12 +2732,12 @@ kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
     }
     const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
                          o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
-                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile, o->three_step};
+                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile, o->no_three_step, o->no_zorder};
     for (int32_t x : f)
         if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
     for (int32_t x : o->reserved)
         if (x != 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: reserved words must be 0");
-    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2 || o->three_step > 1)
+    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2)
         return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: value out of range");
 #ifndef KPM_EXPERIMENTAL
     if (o->experimental) return fail(KPM_ERR_UNSUPPORTED, "experimental kernels are built into libkpm_exp.so only");

@@ -49,7 +49,7 @@ class kpm_plan_opts(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "no_small", "no_tma", "no_two_step", "no_box3", "tma_lanes", "halo_warp", "ell_generic", "no_overlap",
         "no_fused_halo", "contiguous", "experimental", "exp_param", "two_step_ctas",
-        "no_pdl", "no_first_tile", "three_step")] + [("reserved", ctypes.c_int32 * 4)]
+        "no_pdl", "no_first_tile", "no_three_step", "no_zorder")] + [("reserved", ctypes.c_int32 * 3)]
 
 
 PLAN_OPTS = [f[0] for f in kpm_plan_opts._fields_ if f[0] != "reserved"]

@@ -168,9 +168,10 @@ def test_two_step_pairs_and_single_steps(kpm, case, N):
     h = make(kpm, lat, a, b, no_small=1)
     info = h.plan_info(N, R)
     assert info["two_step"] == two_step_expected(lat, info, N), info
+    h.set_plan_opts(no_small=1, no_three_step=1)  # the two-step kernel itself
     mu2 = h.moments(N, R, 5)
     for xw in (1, 2):  # with and without the halo warp
-        h.set_plan_opts(no_small=1, halo_warp=xw)
+        h.set_plan_opts(no_small=1, halo_warp=xw, no_three_step=1)
         assert normwise(h.moments(N, R, 5), ref) < TOL
     h.set_plan_opts(no_small=1, no_two_step=1)
     assert h.plan_info(N, R)["two_step"] == 0
@@ -513,7 +514,7 @@ def test_three_step_kernel(kpm, case, N):
     a *= 1.02
     r = ki.rademacher(19, R, lat["D"])
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b, no_small=1, three_step=1)
+    h = make(kpm, lat, a, b, no_small=1)  # (the default plan for 2D tiles of >= 8 lanes)
     info = h.plan_info(N, R)
     nsteps = N // 2 - 1
     tri = info["two_step"] == 1 and info["TL"] >= 8 and nsteps >= 3
