@@ -970,7 +970,9 @@ kpm_status launch_tma2(kpm_handle_s* h, const Plan& p, const BufMaps& A, const B
 template <int TL, int TX, bool ONSITE, bool PEIERLS>
 kpm_status launch_tri_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                         const CUtensorMap& E4, const kpm::TriGeom& g, int tail) {
-    auto kern = kpm::kpm_step_tri_kernel<TL, TX, ONSITE, PEIERLS>;
+    // 8 warps, 4 consecutive interior sites per thread (a 16-warp variant with 2 sites per thread and a
+    // 128-register cap spilled: c2 48.4 vs 20.2 ms per call, c4 no faster)
+    auto kern = kpm::kpm_step_tri_kernel<TL, TX, ONSITE, PEIERLS, kpm::kThreadsTri>;
     KPM_TRY(set_smem((const void*)kern, p.tri_smem, h->device));
     return launch_k(h, h->stream, kern, dim3(p.tma2_grid), dim3(kpm::kThreadsTri), p.tri_smem, A.A2, A.A3, P.A2, P.Col2, E,
                     E4, g, tail);

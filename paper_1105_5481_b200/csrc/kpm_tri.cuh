@@ -74,8 +74,8 @@ __host__ __device__ inline size_t tri_smem_bytes(int TX, int TL, bool onsite, in
            7 * (size_t)RP * 8 + (size_t)kThreadsTri * 16 + (size_t)(TX + 6) * 16 + (kSAT + kSPT) * 8;
 }
 
-template <int TL, int TX, bool ONSITE, bool PEIERLS>
-__global__ void __launch_bounds__(kThreadsTri, 1)
+template <int TL, int TX, bool ONSITE, bool PEIERLS, int NT = kThreadsTri>
+__global__ void __launch_bounds__(NT, 1)
     kpm_step_tri_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
                         const __grid_constant__ CUtensorMap mapA3,   // a_n 3-site box {2TL, 3, 1}
                         const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
@@ -84,8 +84,8 @@ __global__ void __launch_bounds__(kThreadsTri, 1)
                         const __grid_constant__ CUtensorMap mapE4,   // eps~ box {4, 1}
                         const TriGeom g, const int tail) {
     pdl_entry();
-    constexpr int CONS = 256;
-    constexpr int PRODUCER = CONS - 1;  // (no halo work: 4 TL <= 128 < 255)
+    constexpr int CONS = NT;
+    constexpr int PRODUCER = CONS - 1;  // (no halo work: 4 TL <= 128 < CONS - 1)
     constexpr int KSTEP = CONS / TL;  // tile sites per pass
     constexpr int NPI = TX / KSTEP;   // interior sites per thread
     static_assert(TX % KSTEP == 0 && TL * 16 >= 128, "tile shape");
@@ -209,8 +209,10 @@ __global__ void __launch_bounds__(kThreadsTri, 1)
         const int lg = cs.lg, m0 = cs.m0, H = cs.H, x0 = cs.px * TX;
         if (cur_lg != -1 && lg != cur_lg) flush(cur_lg);
         cur_lg = lg;
-        const long long g0 = (long long)(x0 + k0) * g.RG + (long long)lg * TL + l;
-        const long long gstep = (long long)KSTEP * g.RG;
+        // thread k0 owns the NPI CONSECUTIVE sites k0*NPI .. k0*NPI+NPI-1 of the row: x-neighbours
+        // inside that run come from its registers, only the two ends from shared memory
+        const long long g0 = (long long)(x0 + k0 * NPI) * g.RG + (long long)lg * TL + l;
+        const long long gstep = (long long)g.RG;
         const long long growstep = (long long)g.L0 * g.RG;
         if (PEIERLS) {
             if (t < TX + 6) sphase[t] = __ldg(g.phase + (x0 + t - 3 + 2 * g.L0) % g.L0);
@@ -221,10 +223,11 @@ __global__ void __launch_bounds__(kThreadsTri, 1)
         int ps = ip % kSPT;
         int r2 = (m0 - 3 + 2 * g.L1) % g.L1;  // level-2 row of iteration 0
         int r3 = (m0 - 4 + 2 * g.L1) % g.L1;  // level-3 row
-        // per interior site: level 1 rows r1-2, r1-1 (bm, bc); level 2 rows r2-2, r2-1 (cm, cc);
-        // eps~ at rows r1-1, r1-2 (e2, e3)
-        double2 bm[NPI], bc[NPI], cm[NPI], cc[NPI];
+        // per interior site: a_n rows r1-1, r1 (am, ac); level 1 rows r1-2, r1-1 (bm, bc); level 2
+        // rows r2-2, r2-1 (cm, cc); eps~ at rows r1-1, r1-2 (e2, e3)
+        double2 am[NPI], ac[NPI], bm[NPI], bc[NPI], cm[NPI], cc[NPI];
         double e2[NPI], e3[NPI];
+        const int lx0 = k0 * NPI;  // first site of this thread
         for (int q = 0; q < H + 4; ++q) {
             const int i0 = ia_seg + q;
             const int s1 = s0 + 1 == kSAT ? 0 : s0 + 1;
@@ -266,49 +269,84 @@ __global__ void __launch_bounds__(kThreadsTri, 1)
                     st(B2n + oB2(hx, hl), c);
                 }
             }
+            if (q == 0) {
 #pragma unroll
-            for (int p = 0; p < NPI; ++p) {
-                const int lx = k0 + p * KSTEP;
-                const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
-                // level 1 at row r1
-                const double2 x = ld(A1 + oA(lx, l));
-                const double e1 = ONSITE ? reinterpret_cast<const double*>(A1 + SL.eps_m)[lx] : g.shift;
-                const double2 b = step_val(x, ld(A1 + oA(lx - 1, l)), ld(A1 + oA(lx + 1, l)), ld(A0 + oA(lx, l)),
-                                           ld(A2 + oA(lx, l)), e1, ph, ld(Pq + oP(lx, l)));
-                st(B1n + oP(lx, l), b);
-                if (own1) {
-                    dot_acc<PEIERLS>(acc[0], x, x);
-                    dot_acc<PEIERLS>(acc[1], x, b);
+                for (int p = 0; p < NPI; ++p) {
+                    am[p] = ld(A0 + oA(lx0 + p, l));
+                    ac[p] = ld(A1 + oA(lx0 + p, l));
                 }
-                // level 2 at row r2 = r1-1: centre bc, y-neighbours bm, b; "- a_n" at row r1-1
-                double2 c = make_double2(0.0, 0.0);
-                if (do2) {
-                    c = step_val(bc[p], ld(B1c + oP(lx - 1, l)), ld(B1c + oP(lx + 1, l)), bm[p], b,
-                                 ONSITE ? e2[p] : g.shift, ph, ld(A0 + oA(lx, l)));
-                    st(B2n + oB2(lx, l), c);
+            }
+            // level 1 at row r1 for the run: a_n row r1+1 of the run, the run's x-end neighbours
+            double2 ap[NPI], b[NPI], c[NPI];
+            double en[NPI];  // eps~ at row r1
+#pragma unroll
+            for (int p = 0; p < NPI; ++p) c[p] = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int p = 0; p < NPI; ++p) ap[p] = ld(A2 + oA(lx0 + p, l));
+            {
+                const double2 xl = ld(A1 + oA(lx0 - 1, l)), xr = ld(A1 + oA(lx0 + NPI, l));
+#pragma unroll
+                for (int p = 0; p < NPI; ++p) {
+                    const int lx = lx0 + p;
+                    const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                    const double e1 = ONSITE ? reinterpret_cast<const double*>(A1 + SL.eps_m)[lx] : g.shift;
+                    b[p] = step_val(ac[p], p == 0 ? xl : ac[p - 1], p == NPI - 1 ? xr : ac[p + 1], am[p], ap[p], e1, ph,
+                                    ld(Pq + oP(lx, l)));
+                    if (own1) {
+                        dot_acc<PEIERLS>(acc[0], ac[p], ac[p]);
+                        dot_acc<PEIERLS>(acc[1], ac[p], b[p]);
+                    }
+                    en[p] = e1;
+                }
+                st(B1n + oP(lx0, l), b[0]);  // the run's ends: the neighbouring runs' and the halo's x-neighbours
+                st(B1n + oP(lx0 + NPI - 1, l), b[NPI - 1]);
+            }
+            // level 2 at row r2 = r1-1: centre bc, x-neighbours bc (run) / B1c (ends), y-neighbours bm, b
+            if (do2) {
+                const double2 xl = ld(B1c + oP(lx0 - 1, l)), xr = ld(B1c + oP(lx0 + NPI, l));
+#pragma unroll
+                for (int p = 0; p < NPI; ++p) {
+                    const int lx = lx0 + p;
+                    const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                    c[p] = step_val(bc[p], p == 0 ? xl : bc[p - 1], p == NPI - 1 ? xr : bc[p + 1], bm[p], b[p],
+                                    ONSITE ? e2[p] : g.shift, ph, am[p]);
                     if (own2) {
-                        __stcs(outB + p * gstep, c);
+                        __stcs(outB + p * gstep, c[p]);
                         dot_acc<PEIERLS>(acc[2], bc[p], bc[p]);
-                        dot_acc<PEIERLS>(acc[3], bc[p], c);
+                        dot_acc<PEIERLS>(acc[3], bc[p], c[p]);
                     }
                 }
-                // level 3 at row r3 = r1-2: centre cc, y-neighbours cm, c; "- a_{n+1}" at row r1-2 = bm
-                if (do3) {
-                    const double2 d = step_val(cc[p], ld(B2c + oB2(lx - 1, l)), ld(B2c + oB2(lx + 1, l)), cm[p], c,
+                st(B2n + oB2(lx0, l), c[0]);
+                st(B2n + oB2(lx0 + NPI - 1, l), c[NPI - 1]);
+            }
+            // level 3 at row r3 = r1-2: centre cc, x-neighbours cc (run) / B2c (ends), y-neighbours cm, c;
+            // "- a_{n+1}" at row r1-2 = bm
+            if (do3) {
+                const double2 xl = ld(B2c + oB2(lx0 - 1, l)), xr = ld(B2c + oB2(lx0 + NPI, l));
+#pragma unroll
+                for (int p = 0; p < NPI; ++p) {
+                    const int lx = lx0 + p;
+                    const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                    const double2 d = step_val(cc[p], p == 0 ? xl : cc[p - 1], p == NPI - 1 ? xr : cc[p + 1], cm[p], c[p],
                                                ONSITE ? e3[p] : g.shift, ph, bm[p]);
                     __stcs(outC + p * gstep, d);
                     dot_acc<PEIERLS>(acc[4], cc[p], cc[p]);
                     dot_acc<PEIERLS>(acc[5], cc[p], d);
                     if (tail) dot_acc<PEIERLS>(acc[6], d, d);
                 }
-                // roll one row down
+            }
+            // roll one row down
+#pragma unroll
+            for (int p = 0; p < NPI; ++p) {
+                am[p] = ac[p];
+                ac[p] = ap[p];
                 bm[p] = bc[p];
-                bc[p] = b;
+                bc[p] = b[p];
                 cm[p] = cc[p];
-                cc[p] = c;
-                if (ONSITE) {
+                cc[p] = c[p];
+                if (ONSITE) {  // eps~ history: rows r1-1 (e2), r1-2 (e3)
                     e3[p] = e2[p];
-                    e2[p] = e1;
+                    e2[p] = en[p];
                 }
             }
             __syncthreads();  // row q done: a_n row r1-1 and a_{n-1} row r1 are free; B rings advance
