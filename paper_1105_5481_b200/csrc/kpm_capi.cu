@@ -383,7 +383,9 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
     // 32 first -- c4 3114 vs 3166-3274 ms with 16
     // 2D: 4 lanes per site when RG is not a multiple of 8 (e.g. c2 at 8 GPUs: R = 8 real vectors per
     // GPU, an L2-resident block -- SURVEY.md 8(e) P1 strong scaling)
-    const int cands2r[4] = {16, 32, 8, 4}, cands2c[4] = {32, 16, 8, 4}, cands3[4] = {16, 32, 8, 0};
+    // 2D complex: 16 lanes (the three-step kernel: c4 2346 vs 2438 ms per call with 32; its halo is
+    // 3 sites per side, so the wider 64-site tile pays)
+    const int cands2r[4] = {16, 32, 8, 4}, cands2c[4] = {16, 32, 8, 4}, cands3[4] = {16, 32, 8, 0};
     for (int c : (h->ndim == 2 ? (is_cplx(h) ? cands2c : cands2r) : cands3))
         if (c && RG % c == 0) { TL = c; break; }
     const int tl_opt = h->opts.tma_lanes;  // pinned lanes per tile site (A/B, tests)

@@ -44,12 +44,15 @@ struct TriGeom {
 };
 
 constexpr int kThreadsTri = 256;       // 8 warps: two per SM sub-partition, up to 255 registers
-constexpr int kSAT = 4;                // a_n ring
-constexpr int kSPT = 2;                // a_{n-1} ring
+constexpr int kSAT = 6;                // a_n ring (3 rows ahead of the row in use)
+constexpr int kSPT = 3;                // a_{n-1} ring
 
 // a_n slot: [3 halo sites][TX][3 halo sites], then eps~ as three 128-byte aligned pieces
 // [4 left (x0-4 ..)][TX][4 right] (TMA boxes need 16-byte multiples); a_{n-1} slot
-// [2][TX][2]; B1 rows [2][TX][2] sites; B2 rows [1][TX][1].
+// [2][TX][2].  The level-1 and level-2 rows only ever need the ENDS of the threads' site runs and
+// the halo sites (x-neighbours inside a run stay in registers), so B1 rows hold [2 halo][2 per run]
+// [2 halo] and B2 rows [1][2 per run][1] sites: bix() maps a tile x index to its slot.
+__host__ __device__ constexpr int tri_runs(int TL) { return 256 / TL; }  // runs (threads per lane) per row
 struct TriLayout {
     int site, a_bytes, eps_l, eps_m, eps_r, p_bytes, b1_bytes, b2_bytes;
     __host__ __device__ constexpr TriLayout(int TX, int TL, bool onsite)
@@ -59,8 +62,8 @@ struct TriLayout {
           eps_m((TX + 6) * TL * 16 + 128),
           eps_r((TX + 6) * TL * 16 + 128 + (TX * 8 + 127) / 128 * 128),
           p_bytes(((TX + 4) * TL * 16 + 127) / 128 * 128),
-          b1_bytes(((TX + 4) * TL * 16 + 127) / 128 * 128),
-          b2_bytes(((TX + 2) * TL * 16 + 127) / 128 * 128) {}
+          b1_bytes(((2 * tri_runs(TL) + 4) * TL * 16 + 127) / 128 * 128),
+          b2_bytes(((2 * tri_runs(TL) + 2) * TL * 16 + 127) / 128 * 128) {}
     // eps~ at tile x index lx in [-4, TX+3]
     __device__ __forceinline__ double eps(const unsigned char* slot, int lx, int TX) const {
         return *reinterpret_cast<const double*>(
@@ -71,7 +74,7 @@ struct TriLayout {
 __host__ __device__ inline size_t tri_smem_bytes(int TX, int TL, bool onsite, int RP) {
     const TriLayout S(TX, TL, onsite);
     return (size_t)kSAT * S.a_bytes + (size_t)kSPT * S.p_bytes + 3 * (size_t)S.b1_bytes + 2 * (size_t)S.b2_bytes +
-           7 * (size_t)RP * 8 + (size_t)kThreadsTri * 16 + (size_t)(TX + 6) * 16 + (kSAT + kSPT) * 8;
+           (size_t)kThreadsTri * 16 + (size_t)(TX + 6) * 16 + (kSAT + kSPT) * 8;
 }
 
 template <int TL, int TX, bool ONSITE, bool PEIERLS, int NT = kThreadsTri>
@@ -96,8 +99,7 @@ __global__ void __launch_bounds__(NT, 1)
     unsigned char* ringP = ringA + kSAT * SL.a_bytes;
     unsigned char* ringB1 = ringP + kSPT * SL.p_bytes;
     unsigned char* ringB2 = ringB1 + 3 * SL.b1_bytes;
-    double* sacc = reinterpret_cast<double*>(ringB2 + 2 * SL.b2_bytes);  // [7][RP]
-    double2* sred = reinterpret_cast<double2*>(sacc + 7 * g.RP);           // [CONS]
+    double2* sred = reinterpret_cast<double2*>(ringB2 + 2 * SL.b2_bytes);  // [CONS]
     double2* sphase = sred + CONS;                                         // [TX + 6]: x0-3 .. x0+TX+2
     uint64_t* fullA = reinterpret_cast<uint64_t*>(sphase + TX + 6);
     uint64_t* fullP = fullA + kSAT;
@@ -157,7 +159,6 @@ __global__ void __launch_bounds__(NT, 1)
         for (int i = 0; i < kSAT; ++i) issueA(i);
         for (int i = 0; i < kSPT; ++i) issueP(i);
     }
-    for (int i = t; i < 7 * g.RP; i += blockDim.x) sacc[i] = 0.0;
     __syncthreads();
 
     const int l = t % TL;
@@ -168,20 +169,25 @@ __global__ void __launch_bounds__(NT, 1)
     for (int k = 0; k < 7; ++k) acc[k] = make_double2(0.0, 0.0);
     auto ld = [](const unsigned char* p) { return *reinterpret_cast<const double2*>(p); };
     auto st = [](unsigned char* p, double2 v) { *reinterpret_cast<double2*>(p) = v; };
+    // A CTA's rows cover its lane groups in increasing order, each in one contiguous stretch: the sum
+    // of lane group lgf is final when the CTA leaves it and goes straight to the CTA's partial row
+    // (fixed order over the CTA's threads); columns of lane groups the CTA never touched are zeroed
+    // at the end.
     auto flush = [&](int lgf) {
 #pragma unroll
         for (int k = 0; k < 7; ++k) {
             sred[t] = acc[k];
             __syncthreads();
-            if (t < TL) {
+            if (t < TL && g.red[k] != nullptr && (k < 6 || tail)) {
                 double2 s = make_double2(0.0, 0.0);
                 for (int j = t; j < CONS; j += TL) s = add2(s, sred[j]);
                 const int v = lgf * TL + t;
+                double* row = g.red[k] + (size_t)blockIdx.x * g.RP;
                 if (PEIERLS) {
-                    sacc[k * g.RP + v] += s.x;
+                    row[v] = s.x;
                 } else {
-                    sacc[k * g.RP + 2 * v] += s.x;
-                    sacc[k * g.RP + 2 * v + 1] += s.y;
+                    row[2 * v] = s.x;
+                    row[2 * v + 1] = s.y;
                 }
             }
             __syncthreads();
@@ -200,7 +206,10 @@ __global__ void __launch_bounds__(NT, 1)
     // slot byte offsets of tile x index lx (level 0: [-3, TX+2]; level -1 and 1: [-2, TX+1]; level 2: [-1, TX])
     auto oA = [&](int lx, int ll) { return (lx + 3) * SITE + ll * 16; };
     auto oP = [&](int lx, int ll) { return (lx + 2) * SITE + ll * 16; };
-    auto oB2 = [&](int lx, int ll) { return (lx + 1) * SITE + ll * 16; };
+    // compressed level-1 / level-2 rows: halo sites, then the two ends of every run
+    auto bix = [&](int lx) { return lx < 0 ? lx : (lx >= TX ? 2 * (TX / NPI) + (lx - TX) : 2 * (lx / NPI) + (lx % NPI != 0)); };
+    auto oB1 = [&](int lx, int ll) { return (bix(lx) + 2) * SITE + ll * 16; };
+    auto oB2 = [&](int lx, int ll) { return (bix(lx) + 1) * SITE + ll * 16; };
 
     LoadCursor cs;  // segment iterator of the consumers (same sequence)
     cs.init(g, w_begin, w_end, 0);
@@ -261,11 +270,11 @@ __global__ void __launch_bounds__(NT, 1)
                 const double e1 = ONSITE ? SL.eps(A1, hx, TX) : g.shift;
                 const double2 b = step_val(ld(A1 + oA(hx, hl)), ld(A1 + oA(hx - 1, hl)), ld(A1 + oA(hx + 1, hl)),
                                            ld(A0 + oA(hx, hl)), ld(A2 + oA(hx, hl)), e1, ph, ld(Pq + oP(hx, hl)));
-                st(B1n + oP(hx, hl), b);
+                st(B1n + oB1(hx, hl), b);
                 if (hg < 2 && do2) {
                     const double e = ONSITE ? SL.eps(A0, hx, TX) : g.shift;
-                    const double2 c = step_val(ld(B1c + oP(hx, hl)), ld(B1c + oP(hx - 1, hl)), ld(B1c + oP(hx + 1, hl)),
-                                               ld(B1m + oP(hx, hl)), b, e, ph, ld(A0 + oA(hx, hl)));
+                    const double2 c = step_val(ld(B1c + oB1(hx, hl)), ld(B1c + oB1(hx - 1, hl)), ld(B1c + oB1(hx + 1, hl)),
+                                               ld(B1m + oB1(hx, hl)), b, e, ph, ld(A0 + oA(hx, hl)));
                     st(B2n + oB2(hx, hl), c);
                 }
             }
@@ -298,12 +307,12 @@ __global__ void __launch_bounds__(NT, 1)
                     }
                     en[p] = e1;
                 }
-                st(B1n + oP(lx0, l), b[0]);  // the run's ends: the neighbouring runs' and the halo's x-neighbours
-                st(B1n + oP(lx0 + NPI - 1, l), b[NPI - 1]);
+                st(B1n + oB1(lx0, l), b[0]);  // the run's ends: the neighbouring runs' and the halo's x-neighbours
+                st(B1n + oB1(lx0 + NPI - 1, l), b[NPI - 1]);
             }
             // level 2 at row r2 = r1-1: centre bc, x-neighbours bc (run) / B1c (ends), y-neighbours bm, b
             if (do2) {
-                const double2 xl = ld(B1c + oP(lx0 - 1, l)), xr = ld(B1c + oP(lx0 + NPI, l));
+                const double2 xl = ld(B1c + oB1(lx0 - 1, l)), xr = ld(B1c + oB1(lx0 + NPI, l));
 #pragma unroll
                 for (int p = 0; p < NPI; ++p) {
                     const int lx = lx0 + p;
@@ -369,11 +378,17 @@ __global__ void __launch_bounds__(NT, 1)
         cs.seg(g, 0);
     }
     if (cur_lg != -1) flush(cur_lg);
-    __syncthreads();
+    // zeros in this CTA's row for the lane groups it did not process, and in rows >= gridDim.x
+    const int lg_lo = (int)(w_begin / ((long long)g.PX * g.L1));
+    const int lg_hi = w_end > w_begin ? (int)((w_end - 1) / ((long long)g.PX * g.L1)) : -1;  // inclusive
+    const int per_lg = PEIERLS ? TL : 2 * TL;  // partial-row columns of one lane group
     for (int k = 0; k < 7; ++k) {
         double* rowk = g.red[k];
         if (rowk == nullptr || (k == 6 && !tail)) continue;
-        for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)blockIdx.x * g.RP + v] = sacc[k * g.RP + v];
+        for (int v = t; v < g.RP; v += blockDim.x) {
+            const int lgv = v / per_lg;
+            if (lgv < lg_lo || lgv > lg_hi) rowk[(size_t)blockIdx.x * g.RP + v] = 0.0;
+        }
         for (int rr = blockIdx.x + gridDim.x; rr < g.rows_total; rr += gridDim.x)
             for (int v = t; v < g.RP; v += blockDim.x) rowk[(size_t)rr * g.RP + v] = 0.0;
     }
