@@ -1,8 +1,10 @@
 """Summarise a profiling pass (scripts/profile_round.sh output) into profiles/.
 
-usage: python scripts/ncu_summary.py gpurun_out/<tag> <round-name>
-writes profiles/<round>_<config>_launches.csv (kernel, duration ns), profiles/<round>_<config>_full.txt
-(key metrics of the `ncu --set full` capture) and merges profiles/traffic.json."""
+usage: python scripts/ncu_summary.py gpurun_out/<tag> <round-name> [dest]
+writes profiles/<round>_<name>_launches.csv (kernel, duration ns), profiles/<round>_<name>_full.txt
+(key metrics of the `ncu --set full` capture) and merges profiles/traffic.json.  <name> is a config
+(c2 ...) or a config variant (c2_csr, c2_R8: the config through CSR / at 8 vectors per GPU); the
+profiling script writes specs.json mapping each name to its R per GPU."""
 import collections
 import csv
 import io
@@ -35,7 +37,11 @@ def main(src, rnd, dest=None):
     os.makedirs(prof, exist_ok=True)
     tpath = os.path.join(prof, "traffic.json")
     traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
-    for c in ["c1", "c2", "c3", "c4", "c5", "pd"]:
+    specs = {}
+    sp = os.path.join(src, "specs.json")
+    if os.path.exists(sp):
+        specs = json.load(open(sp))
+    for c in (list(specs) or ["c1", "c2", "c3", "c4", "c5", "pd"]):
         ll = os.path.join(src, f"launchlist_{c}.csv")
         if os.path.exists(ll):
             rows = read_ncu_csv(ll)
@@ -69,8 +75,9 @@ def main(src, rnd, dest=None):
             t = sum(agg["gpu__time_duration.sum"]) / n
             traffic[c] = {"tma": int("tma" in (name or "")), "kernel": (name or "")[:160], "launches": n,
                           "dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes_per_launch": rd + wr,
-                          "mean_duration_ns": t, "round": rnd,
-                          "note": "mean over steady-state step launches (ncu, -s 4 -c 8)"}
+                          "mean_duration_ns": t, "round": rnd, "R_loc": specs.get(c, {}).get("R_loc"),
+                          "note": "mean over steady-state step launches (ncu dram__bytes_read.sum + "
+                                  "dram__bytes_write.sum)"}
         rep = os.path.join(src, f"full_{c}.ncu-rep")
         if os.path.exists(rep):
             out = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True,
