@@ -2,17 +2,29 @@
 //
 // Same arithmetic as kpm_step_kernel<EllOp, STEP> (Eq 18 + the doubling inner
 // products) with the row entries staged through shared memory: the CTA walks tiles
-// of TILE = TS * kEllSPW consecutive rows; while it computes tile i, cp.async copies
-// the column indices and values of tile i+gridDim.x into the other half of a
-// double buffer, so the gathers of a row never wait behind the load of their index.
+// of TILE = TS * kEllSPW consecutive rows; while it computes tile i, one thread copies
+// the column indices and values of tile i+gridDim.x into the other half of a double
+// buffer with 2 K bulk copies (cp.async.bulk, completion on an mbarrier; the [K][ld]
+// device layout makes every entry column's tile slice one aligned contiguous run), so
+// the gathers of a row never wait behind the load of their index and no other thread
+// spends instructions on the staging (ncu r02: the per-element cp.async staging with its
+// index arithmetic was ~60 of 172 warp instructions per row).
 // One warp row of threads owns the 16-byte vector lanes of a row (one matrix entry
 // serves all R vectors, BJ north_star); each thread keeps 8 gathers in flight.
 #pragma once
 #include <type_traits>
 
 #include "kpm_kernels.cuh"
+#include "kpm_tma.cuh"
 
 namespace kpm {
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 
 constexpr int kEllKMax = 16;  // rows with more entries use the generic step kernel
 constexpr int kEllSPW = 4;    // rows per thread row per tile
@@ -60,28 +72,35 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
     const double2* __restrict__ Cl = v.C + rg;  // this thread's lane of row 0
     double2* __restrict__ Pl = v.P + rg;
 
+    __shared__ uint64_t sbar[2];
+    // thread 0: the tile's K column slices and K value slices (the pad rows past D included)
     auto prefetch = [&](int tile, int buf) {
-        for (int e = tid; e < K * TILE; e += nthr) {
-            const int k = e / TILE, i = e - k * TILE;
-            const int s = tile * TILE + i;
-            if (s < D) {
-                const size_t ge = (size_t)k * D + s;
-                cp_async(scol + ((size_t)buf * K + k) * TILE + i, op.col + ge, 4);
-                cp_async(sval + (((size_t)buf * K + k) * TILE + i) * vb, reinterpret_cast<const unsigned char*>(op.val) + ge * vb,
-                         vb);
-            }
+        mbar_expect_tx(sbar + buf, (uint32_t)K * TILE * (4 + vb));
+        for (int k = 0; k < K; ++k) {
+            const size_t ge = (size_t)k * op.ld + (size_t)tile * TILE;
+            bulk_g2s(scol + ((size_t)buf * K + k) * TILE, op.col + ge, TILE * 4, sbar + buf);
+            bulk_g2s(sval + ((size_t)buf * K + k) * TILE * vb, reinterpret_cast<const unsigned char*>(op.val) + ge * vb,
+                     TILE * vb, sbar + buf);
         }
-        cp_async_commit();
     };
 
     double2 acc0 = make_double2(0.0, 0.0), acc1 = acc0, acc2 = acc0;
     int tile = blockIdx.x;
-    if (tile < ntiles) prefetch(tile, 0);
+    if (tid == 0) {
+        mbar_init(sbar, 1);
+        mbar_init(sbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (tile < ntiles) prefetch(tile, 0);
+    }
+    __syncthreads();
     for (int it = 0; tile < ntiles; tile += gridDim.x, ++it) {
         const int buf = it & 1;
-        cp_async_wait_all();
+        mbar_wait(sbar + buf, (uint32_t)((it >> 1) & 1));
         __syncthreads();  // this tile's entries are in smem; nobody reads the other buffer any more
-        if (tile + (int)gridDim.x < ntiles) prefetch(tile + gridDim.x, buf ^ 1);
+        if (tid == 0 && tile + (int)gridDim.x < ntiles) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before async writes
+            prefetch(tile + gridDim.x, buf ^ 1);
+        }
         if (!active) continue;
         const int* tc = scol + (size_t)buf * K * TILE;
         const unsigned char* tv = sval + (size_t)buf * K * TILE * vb;
@@ -119,7 +138,6 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
             }
         }
     }
-    cp_async_wait_all();
     __syncthreads();
     sred[tid] = acc0;
     sred[nthr + tid] = acc1;
