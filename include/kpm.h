@@ -348,8 +348,11 @@ kpm_status kpm_last_timing(kpm_handle h, double* steps_ms, int32_t* step_launche
  * kernel; info[6] = lanes per site; info[7] bit 0: whole (lane group, pencil) columns are
  * dealt round-robin to CTAs; bit 1: two recursion steps per launch (temporal blocking, 2D;
  * 4 vector blocks); bit 2: row partition with the halo exchange overlapped (boundary planes,
- * exchange on a comm stream, interior planes); bit 3: 3D dense-box march kernel; info[8] = two-step tile width TX2; info[9] = two-step CTAs per SM;
- * info[10] = two-step grid; info[11] = 0. */
+ * exchange on a comm stream, interior planes); bit 3: 3D dense-box march kernel; bit 4: 3D two-step
+ * (experimental); bit 5: persistent (experimental); bit 6: three steps per launch (2D, kpm_tri.cuh);
+ * info[8] = two-step tile width TX2; info[9] = two-step CTAs per SM; info[10] = two-step grid;
+ * info[11] = recursion steps per launch of the deepest kernel in the plan beyond two (3 for the
+ * three-step kernel; KS for the experimental KS-step kernel), else 0. */
 kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int64_t info[12]);
 
 /* Counters of the last kpm_moments_ex / kpm_moments_group call on this handle: stats[0] =

@@ -2724,6 +2724,7 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[10] = p.use_tma2 ? p.tma2_grid : 0;
     info[11] = p.use_tmak ? p.KSK : (p.use_tri ? 3 : 0);
     if (p.use_persist) info[7] |= 32;
+    if (p.use_tri) info[7] |= 64;
     return KPM_OK;
 }
 

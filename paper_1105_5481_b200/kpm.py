@@ -330,6 +330,7 @@ class Handle:
         d["two_step3d"] = int((info[7] >> 4) & 1)  # 3D two-step kernel (kpm_tma32.cuh)
         d["persist"] = int((info[7] >> 5) & 1)  # whole recursion in one cooperative launch (kpm_persist.cuh)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
+        d["three_step"] = int((info[7] >> 6) & 1)  # three steps per launch (kpm_tri.cuh)
         return d
 
     def last_stats(self):
