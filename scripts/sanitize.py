@@ -1,7 +1,8 @@
-"""Small parity cases for compute-sanitizer (memcheck / racecheck / synccheck): the two-step rings
-(2D, 4- and 16-lane tiles, Peierls), the 3D dense-box march, the in-place a_{n+1}-over-a_{n-1}
-single steps, the fused peer-plane stores of an in-process slab group, the ELL kernel, the
-first-step plane ring, and the finish/assemble kernels -- each checked against the oracle.
+"""Small parity cases for compute-sanitizer (memcheck / racecheck / synccheck): the three-step
+rings (2D, on-site, Peierls), the two-step rings (4- and 16-lane tiles, the halo warp), the 3D
+dense-box march, the in-place a_{n+1}-over-a_{n-1} single steps, the fused peer-plane stores of an
+in-process slab group, the ELL kernel with bulk-staged entries, the first-step plane ring, and the
+finish/assemble kernels -- each checked against the oracle.
 usage: compute-sanitizer --tool memcheck python scripts/sanitize.py"""
 import os
 import sys
@@ -27,9 +28,11 @@ def check(name, mu, ref):
 
 
 cases = [
-    ("two_step_16_lanes", lat_of(2, (128, 12), W=1.0), 14, 32, {}),
+    ("three_step_16_lanes_onsite", lat_of(2, (128, 12), W=1.0), 16, 32, {}),
+    ("three_step_peierls", lat_of(2, (128, 9), flux=1 / 8), 17, 32, {}),
+    ("two_step_16_lanes", lat_of(2, (128, 12), W=1.0), 14, 32, {"no_three_step": 1}),
     ("two_step_4_lanes", lat_of(2, (128, 10)), 14, 8, {}),
-    ("two_step_peierls_halo_warp", lat_of(2, (64, 8), flux=1 / 8), 13, 32, {}),
+    ("two_step_peierls_halo_warp", lat_of(2, (64, 8), flux=1 / 8), 13, 32, {"no_three_step": 1}),
     ("single_steps_in_place", lat_of(2, (64, 8), W=1.0), 12, 16, {"no_two_step": 1}),
     ("box3_march", lat_of(3, (16, 8, 6), W=2.0), 12, 32, {}),
     ("generic_first_and_steps", lat_of(3, (9, 7, 5), W=1.0), 11, 3, {"no_tma": 1, "no_first_tile": 1}),
