@@ -2052,10 +2052,17 @@ kpm_status kpm_create_stencil(const kpm_stencil_desc* d, double a, double b, int
         site0 = h->z0 * h->plane;
     }
     if (st == KPM_OK && d->onsite) {
-        std::vector<double> e(h->D);
-        for (int64_t i = 0; i < h->D; ++i) e[i] = (d->onsite[site0 + i] - b) / a;  // Eq (8) on the diagonal
+        // raw eps_i of this rank's sites to the device, then Eq (8) on the diagonal there:
+        // eps~_i = (eps_i - b) / a (the same correctly rounded ops as a host loop)
         cudaError_t ce = cudaMalloc(&h->d_eps, h->D * sizeof(double));
-        if (ce == cudaSuccess) ce = cudaMemcpy(h->d_eps, e.data(), h->D * sizeof(double), cudaMemcpyHostToDevice);
+        if (ce == cudaSuccess)
+            ce = cudaMemcpyAsync(h->d_eps, d->onsite + site0, h->D * sizeof(double), cudaMemcpyHostToDevice, h->stream);
+        if (ce == cudaSuccess) {
+            const int blocks = (int)std::min<long long>((h->D + 255) / 256, 16LL * h->num_sms);
+            kpm::rescale_onsite_kernel<<<blocks, 256, 0, h->stream>>>(h->d_eps, (long long)h->D, b, a);
+            ce = cudaGetLastError();
+        }
+        if (ce == cudaSuccess) ce = cudaStreamSynchronize(h->stream);
         if (ce != cudaSuccess) st = fail(KPM_ERR_CUDA, "on-site upload: %s", cudaGetErrorString(ce));
 #ifdef KPM_EXPERIMENTAL
         if (st == KPM_OK && h->ndim == 3 && !h->rows) {

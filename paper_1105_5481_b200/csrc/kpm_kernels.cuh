@@ -331,6 +331,12 @@ __global__ void load_r0_kernel(const double* __restrict__ r0, double2* __restric
     }
 }
 
+// Eq (8) on the diagonal, in place: eps~_i = (eps_i - b) / a (kpm_create_stencil).
+__global__ void rescale_onsite_kernel(double* __restrict__ e, long long n, double b, double a) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        e[i] = (e[i] - b) / a;
+}
+
 // dst[k][l] = src[idx[k]][l] over n sites of RG 16-byte lanes (row-partition ghost exchange).
 __global__ void gather_lanes_kernel(const double2* __restrict__ src, const int* __restrict__ idx, long long n, int RG,
                                     double2* __restrict__ dst) {
