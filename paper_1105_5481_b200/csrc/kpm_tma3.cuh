@@ -157,19 +157,28 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             const long long o0 = ((long long)(y0 + ly0) * (g.L0 + 2 * g.xpad) + xs + g.xpad) * g.RG + s.lg * TL + l;
             const long long prow = (long long)(KSTEP / TX) * (g.L0 + 2 * g.xpad) * g.RG;  // pass -> +rows
             const bool img_lo = xs < g.xpad, img_hi = xs >= g.L0 - g.xpad;
-            double2 zc[NPASS], zm[NPASS];
-            for (int j = 0; j < H; ++j) {
-                const long long i0 = ia_seg + j, i1 = i0 + 1, i2 = i0 + 2;
+            // z neighbours roll in registers; the plane loop is unrolled by 2 so the two roles (plane m-1,
+            // plane m) swap at compile time instead of by register moves, and the ring slots advance
+            // incrementally (no 64-bit modulo per plane)
+            double2 ZR[2][NPASS];
+            int sa0 = (int)(ia_seg % kSA), ph0 = (int)((ia_seg / kSA) & 1);  // slot / parity of load i0
+            int ps = (int)(ip % S::SP), pph = (int)((ip / S::SP) & 1);
+            auto plane = [&](const int j, const int u) {
+                double2(&zm)[NPASS] = ZR[u];
+                double2(&zc)[NPASS] = ZR[u ^ 1];
+                int sa1 = sa0 + 1, ph1 = ph0;
+                if (sa1 == kSA) { sa1 = 0; ph1 ^= 1; }
+                int sa2 = sa1 + 1, ph2 = ph1;
+                if (sa2 == kSA) { sa2 = 0; ph2 ^= 1; }
                 if (j == 0) {
-                    mbar_wait(fullA + (int)(i0 % kSA), (uint32_t)((i0 / kSA) & 1));
-                    mbar_wait(fullA + (int)(i1 % kSA), (uint32_t)((i1 / kSA) & 1));
+                    mbar_wait(fullA + sa0, (uint32_t)ph0);
+                    mbar_wait(fullA + sa1, (uint32_t)ph1);
                 }
-                mbar_wait(fullA + (int)(i2 % kSA), (uint32_t)((i2 / kSA) & 1));
-                const int ps = (int)(ip % S::SP);
-                mbar_wait(fullP + ps, (uint32_t)((ip / S::SP) & 1));
-                const unsigned char* S0 = ringA + (int)(i0 % kSA) * S::BYTES;  // plane m-1
-                const unsigned char* S1 = ringA + (int)(i1 % kSA) * S::BYTES;  // plane m
-                const unsigned char* S2 = ringA + (int)(i2 % kSA) * S::BYTES;  // plane m+1
+                mbar_wait(fullA + sa2, (uint32_t)ph2);
+                mbar_wait(fullP + ps, (uint32_t)pph);
+                const unsigned char* S0 = ringA + sa0 * S::BYTES;  // plane m-1
+                const unsigned char* S1 = ringA + sa1 * S::BYTES;  // plane m
+                const unsigned char* S2 = ringA + sa2 * S::BYTES;  // plane m+1
                 const unsigned char* Pv = ringP + ps * S::TILE;
                 const long long mo = (long long)(g.zoff + s.m0 + j + g.ghost) * zstride * g.RG;
 #pragma unroll
@@ -201,15 +210,24 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     dot_acc<false>(acc0, x, x);
                     dot_acc<false>(acc1, x, y);
                     if (tail) dot_acc<false>(acc2, y, y);
-                    zm[pass] = x;
-                    zc[pass] = zp;
+                    zm[pass] = zp;  // plane m+1 takes the slot of plane m-1: next plane's "zc"
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(emptyA + (int)(i0 % kSA));
+                    mbar_arrive(emptyA + sa0);
                     mbar_arrive(emptyP + ps);
                 }
                 ++ip;
+                sa0 = sa1;
+                ph0 = ph1;
+                if (++ps == S::SP) {
+                    ps = 0;
+                    pph ^= 1;
+                }
+            };
+            for (int j = 0; j < H; j += 2) {
+                plane(j, 0);
+                if (j + 1 < H) plane(j + 1, 1);
             }
             __syncwarp();
             if (lane == 0) {
