@@ -112,6 +112,8 @@ def kernel_name(fmt, plan):
         return "kpm_ell_step_kernel (ELL SpMM over the vector block + recursion + reductions)"
     if fmt == "dense":
         return "kpm_dense_step_kernel (DMMA fp64 GEMM H~ a_n + fused recursion and moment sums)"
+    if plan.get("four_step"):
+        return "kpm_step_quad_kernel (four recursion steps per HBM pass, TMA-fed march)"
     if plan.get("three_step"):
         return "kpm_step_tri_kernel (three recursion steps per HBM pass, TMA-fed march)"
     if plan.get("ks"):

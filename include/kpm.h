@@ -240,7 +240,9 @@ typedef struct {
     int32_t no_three_step; /* 1: no three-steps-per-launch kernel for 2D lattices (kpm_tri.cuh: 4 D R s
                               bytes per three steps; tiles of >= 8 lanes): the two-step kernel */
     int32_t no_zorder;     /* 1: 3D round-robin march in row-major pencil order instead of Z order */
-    int32_t reserved[3];   /* must be 0 */
+    int32_t no_four_step;  /* 1: no four-step launches for 2D lattices (kpm_quad.cuh, 8-lane x 64-site
+                              tiles, the default where the lanes allow it): three steps per launch */
+    int32_t reserved[2];   /* must be 0 */
 } kpm_plan_opts;
 
 /* Set (opts != NULL) or reset to the default (opts == NULL) the plan options of h.

@@ -30,6 +30,7 @@
 #include "kpm_tma2.cuh"
 #include "kpm_tma3.cuh"
 #include "kpm_tri.cuh"
+#include "kpm_quad.cuh"
 // Kernels that are parity-green but measured slower than the default plan:
 // their templates are instantiated (launched) only under KPM_EXPERIMENTAL, i.e. in libkpm_exp.so,
 // and reached through kpm_plan_opts.experimental.  The default libkpm.so contains none of them.
@@ -162,6 +163,10 @@ struct Plan {
     // three steps per launch (kpm_tri.cuh), same tile as the two-step kernel; needs 4 vector blocks
     bool use_tri = false;
     size_t tri_smem = 0;
+    // four steps per launch (kpm_quad.cuh): its own tile, TLQ lanes x TXQ sites (512 lanes)
+    bool use_quad = false;
+    int TLQ = 0, TXQ = 0, quad_grid = 0;
+    size_t quad_smem = 0;
     // two steps per launch for 3D lattices (kpm_tma32.cuh); needs 4 vector blocks
     bool use_tma32 = false;
     int TX32 = 0, TY32 = 0, TL32 = 0, tma32_grid = 0, tma32_rr = 0;
@@ -464,6 +469,18 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
             p->use_tri = !h->opts.no_three_step && TL >= 8 && TL <= 32 && TL * p->TX2 == 1024 && h->L[0] >= 8 &&
                          h->L[1] >= 6 && smt <= (size_t)h->smem_optin;
             p->tri_smem = smt;
+            // four steps per launch: 8-lane x 64-site tiles (2 sites per thread run)
+            const int tlq = 8, txq = 64;
+            const size_t smq = kpm::quad_smem_bytes(txq, tlq, on);
+            p->use_quad = !h->opts.no_four_step && RG % tlq == 0 && h->L[0] % txq == 0 && h->L[1] >= 8 &&
+                          smq <= (size_t)h->smem_optin;
+            if (p->use_quad) {
+                p->TLQ = tlq;
+                p->TXQ = txq;
+                p->quad_smem = smq;
+                const long long WQ = (long long)(RG / tlq) * (h->L[0] / txq) * Lm2;
+                p->quad_grid = (int)std::min<long long>(WQ, (long long)h->num_sms);
+            }
         }
     }
     // KS-step kernel: 2D lattices, row tiles of TXK * TLK = 512 lanes (kpm_tmak.cuh)
@@ -533,7 +550,7 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->use_tmak) p->gx = std::max(p->gx, p->tmak_grid);
     if (p->use_tma32) p->gx = std::max(p->gx, p->tma32_grid);
     p->nslots = N;
-    if (h->rows) p->use_tma2 = p->use_tri = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
+    if (h->rows) p->use_tma2 = p->use_tri = p->use_quad = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
     p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL && !(flags & KPM_DIRECT) &&
                  !h->opts.no_overlap;
     if (p->overlap) p->gx = 3 * p->tma_grid;
@@ -568,6 +585,8 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->off_R = off;
     if ((flags & KPM_DIRECT) && with_r0) off = align_up(off + p->lane_bytes);
     if (p->use_tri && (p->M - 1 < 3 || !p->use_tma2)) p->use_tri = false;
+    if (p->use_quad && (p->M - 1 < 4 || !p->use_tma2)) p->use_quad = false;
+    if (p->use_quad) p->gx = std::max(p->gx, p->quad_grid);
     if (p->use_tma2 && p->M - 1 < 2) p->use_tma2 = false;
     if (p->use_tma32 && p->M - 1 < 2) p->use_tma32 = false;
     if (p->use_tma2 || p->use_tmak || p->use_tma32) {  // out-of-place multi-step launches: two spare blocks
@@ -877,6 +896,7 @@ struct BufMaps {
     CUtensorMap A, Col, Row, P, Col2;  // main, 1-site column, row, (=main), 2-site column (2D)
     CUtensorMap A2;                    // main box of the two-step kernel (width TX2)
     CUtensorMap A3;                    // 3-site box of the three-step kernel
+    CUtensorMap AQ, AQ4, AQ3;          // four-step kernel (TLQ lanes): main box TXQ, 4-site and 3-site boxes
     CUtensorMap AK, AKH, AKH1;         // KS-step kernel: main (TXK), KS-site and (KS-1)-site boxes, TLK lanes
     CUtensorMap Box3, Row3;            // 3D dense-box kernel: (TX+2) x TY box, (TX+2)-site row
     CUtensorMap A32, A32r, P32, P32r;  // 3D two-step kernel: (TX+4) x TY, (TX+4) x 2, (TX+2) x TY, (TX+2) x 1
@@ -890,6 +910,11 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     if (h->ndim == 2) KPM_TRY(make_vec_map(h, p, base, 2, 1, 1, &bm->Col2));
     if (p.use_tma2) KPM_TRY(make_vec_map(h, p, base, p.TX2, 1, 1, &bm->A2));
     if (p.use_tri) KPM_TRY(make_vec_map(h, p, base, 3, 1, 1, &bm->A3));
+    if (p.use_quad) {
+        KPM_TRY(make_vec_map(h, p, base, p.TXQ, 1, 1, &bm->AQ, p.TLQ));
+        KPM_TRY(make_vec_map(h, p, base, 4, 1, 1, &bm->AQ4, p.TLQ));
+        KPM_TRY(make_vec_map(h, p, base, 3, 1, 1, &bm->AQ3, p.TLQ));
+    }
     if (p.use_tma3) {
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, p.TY, 1, &bm->Box3));
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, 1, 1, &bm->Row3));
@@ -991,6 +1016,23 @@ kpm_status launch_tri_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const 
     }
     if (on) return launch_tri_t<TL, TX, true, false>(h, p, A, P, E, E4, g, tail);
     return launch_tri_t<TL, TX, false, false>(h, p, A, P, E, E4, g, tail);
+}
+
+template <bool ONSITE, bool PEIERLS>
+kpm_status launch_quad_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                         const CUtensorMap& E4, const kpm::QuadGeom& g, int tail) {
+    auto kern = kpm::kpm_step_quad_kernel<8, 64, ONSITE, PEIERLS>;
+    KPM_TRY(set_smem((const void*)kern, p.quad_smem, h->device));
+    return launch_k(h, h->stream, kern, dim3(p.quad_grid), dim3(kpm::kThreadsQuad), p.quad_smem, A.AQ, A.AQ4, P.AQ, P.AQ3,
+                    E, E4, g, tail);
+}
+
+kpm_status launch_quad(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
+                       const CUtensorMap& E4, const kpm::QuadGeom& g, int tail) {
+    if (p.TLQ != 8 || p.TXQ != 64) return fail(KPM_ERR_UNSUPPORTED, "no four-step kernel for TL=%d TX=%d", p.TLQ, p.TXQ);
+    const bool on = h->d_eps != nullptr;
+    if (is_cplx(h)) return on ? launch_quad_t<true, true>(h, p, A, P, E, E4, g, tail) : launch_quad_t<false, true>(h, p, A, P, E, E4, g, tail);
+    return on ? launch_quad_t<true, false>(h, p, A, P, E, E4, g, tail) : launch_quad_t<false, false>(h, p, A, P, E, E4, g, tail);
 }
 
 // instantiated tile shapes of the three-step kernel (TX * TL = 1024 lanes per row tile)
@@ -1237,7 +1279,9 @@ struct Run {
     kpm::TmaGeom tg{};
     kpm::Tma2Geom tg2{};
     kpm::TriGeom tgt{};
-    CUtensorMap mapE4;               // eps~: 4-site box (three-step kernel)
+    kpm::QuadGeom tgq{};
+    CUtensorMap mapE4;               // eps~: 4-site box (three- and four-step kernels)
+    CUtensorMap mapEQ;               // eps~: TXQ box (four-step kernel)
     kpm::TmaKGeom tgk{};
     kpm::Tma32Geom tg32{};
     CUtensorMap mapE32, mapE32r;     // eps~ frame: (TX+4) x TY box, (TX+4) x 1 box (3D two-step kernel)
@@ -1381,6 +1425,7 @@ struct Run {
         memset(&mapE, 0, sizeof mapE);
         memset(&mapE2, 0, sizeof mapE2);
         memset(&mapE4, 0, sizeof mapE4);
+        memset(&mapEQ, 0, sizeof mapEQ);
         memset(&mapEf, 0, sizeof mapEf);
         memset(&mapEK, 0, sizeof mapEK);
         memset(&mapEKH, 0, sizeof mapEKH);
@@ -1396,7 +1441,8 @@ struct Run {
                     KPM_TRY(make_eps_map_w(h, p, 2, &mapE2));
                     KPM_TRY(make_eps_map_w(h, p, p.TX2, &mapEf));
                 }
-                if (p.use_tri) KPM_TRY(make_eps_map_w(h, p, 4, &mapE4));
+                if (p.use_tri || p.use_quad) KPM_TRY(make_eps_map_w(h, p, 4, &mapE4));
+                if (p.use_quad) KPM_TRY(make_eps_map_w(h, p, p.TXQ, &mapEQ));
                 if (p.use_tma32) {
                     KPM_TRY(make_epsf_map(h, p.TX32 + 4, p.TY32, &mapE32));
                     KPM_TRY(make_epsf_map(h, p.TX32 + 4, 1, &mapE32r));
@@ -1463,6 +1509,19 @@ struct Run {
             tgt.t = tg.t;
             tgt.shift = tg.shift;
             tgt.phase = tg.phase;
+            tgq.L0 = tg2.L0;
+            tgq.L1 = tg2.L1;
+            tgq.TX = p.TXQ;
+            tgq.TL = p.TLQ;
+            tgq.RG = tg2.RG;
+            tgq.G_L = p.TLQ ? p.RG / p.TLQ : 0;
+            tgq.PX = p.TXQ ? (int)(h->L[0] / p.TXQ) : 0;
+            tgq.W = (long long)tgq.G_L * tgq.PX * tg2.L1;
+            tgq.RP = tg2.RP;
+            tgq.rows_total = p.gx;
+            tgq.t = tg.t;
+            tgq.shift = tg.shift;
+            tgq.phase = tg.phase;
             tgk.L0 = tg.L0;
             tgk.L1 = tg.L1;
             tgk.TX = p.TXK;
@@ -1692,10 +1751,32 @@ struct Run {
             n += 2;
             return KPM_OK;
         }
+        // four-step launches (kpm_quad.cuh): the remainder of the step count goes first (a three-step
+        // launch, a pair or a single step), then every launch advances four steps
+        const int left = nsteps - n + 1;
+        if (!direct && p.use_quad && left >= 4 && left % 4 == 0) {
+            // steps n .. n+3: slots 2n .. 2n+7 (+ odd-N tail 2n+8)
+            const bool tail = (N & 1) && n + 3 == nsteps;
+            for (int k = 0; k < 8; ++k) tgq.red[k] = part + (size_t)(2 * n + k) * slot;
+            tgq.red[8] = tail ? part + (size_t)(2 * n + 8) * slot : nullptr;
+            tgq.outB = spare0;
+            tgq.outC = spare1;
+            KPM_TRY(launch_quad(h, p, maps_of(base_of(cur)), maps_of(base_of(prev)), mapEQ, mapE4, tgq, tail));
+            double2* oc = cur;
+            double2* op = prev;
+            cur = spare1;
+            prev = spare0;
+            spare0 = oc;
+            spare1 = op;
+            h->steps_bytes += 4.0 * (3.0 * vbytes + ebytes);  // four steps
+            h->design_bytes += 4.0 * vbytes + ebytes;         // a_n, a_{n-1} read, a_{n+3}, a_{n+4} written once
+            h->step_launches++;
+            n += 4;
+            return KPM_OK;
+        }
         // three-step launches (kpm_tri.cuh): the remainder of the step count goes first as one pair
         // or one single step, then every launch advances three steps
-        const int left = nsteps - n + 1;
-        if (!direct && p.use_tri && left >= 3 && left % 3 == 0) {
+        if (!direct && p.use_tri && left >= 3 && (p.use_quad ? left % 4 == 3 : left % 3 == 0)) {
             // steps n, n+1, n+2: slots 2n .. 2n+5 (+ odd-N tail 2n+6)
             const bool tail = (N & 1) && n + 2 == nsteps;
             for (int k = 0; k < 6; ++k) tgt.red[k] = part + (size_t)(2 * n + k) * slot;
@@ -1716,7 +1797,7 @@ struct Run {
             return KPM_OK;
         }
         const bool pair = !direct && p.use_tma2 && n + 1 <= nsteps &&
-                          (p.use_tri ? left % 3 == 2 : !(n == 1 && (nsteps & 1)));
+                          (p.use_quad ? left % 4 == 2 : (p.use_tri ? left % 3 == 2 : !(n == 1 && (nsteps & 1))));
         if (pair) {
             // steps n and n+1: slots 2n .. 2n+3 (+ odd-N tail 2n+4)
             const bool tail = (N & 1) && n + 1 == nsteps;
@@ -2729,9 +2810,10 @@ kpm_status kpm_plan_info(kpm_handle h, int32_t N, int64_t R, uint32_t flags, int
     info[8] = p.use_tma2 ? p.TX2 : (p.use_tma32 ? p.TX32 * 100 + p.TY32 : 0);
     info[9] = p.use_tma2 ? p.tma2_minb : 0;
     info[10] = p.use_tma2 ? p.tma2_grid : 0;
-    info[11] = p.use_tmak ? p.KSK : (p.use_tri ? 3 : 0);
+    info[11] = p.use_tmak ? p.KSK : (p.use_quad ? 4 : (p.use_tri ? 3 : 0));
     if (p.use_persist) info[7] |= 32;
     if (p.use_tri) info[7] |= 64;
+    if (p.use_quad) info[7] |= 128;
     return KPM_OK;
 }
 
@@ -2756,12 +2838,12 @@ kpm_status kpm_set_plan_opts(kpm_handle h, const kpm_plan_opts* o) {
     }
     const int32_t f[] = {o->no_small, o->no_tma,        o->no_two_step, o->no_box3,   o->tma_lanes,
                          o->halo_warp, o->ell_generic,  o->no_overlap,  o->no_fused_halo, o->contiguous,
-                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile, o->no_three_step, o->no_zorder};
+                         o->experimental, o->exp_param, o->two_step_ctas, o->no_pdl, o->no_first_tile, o->no_three_step, o->no_zorder, o->no_four_step};
     for (int32_t x : f)
         if (x < 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: negative field");
     for (int32_t x : o->reserved)
         if (x != 0) return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: reserved words must be 0");
-    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2)
+    if (o->halo_warp > 2 || o->experimental > 3 || o->two_step_ctas > 2 || o->no_four_step > 1)
         return fail(KPM_ERR_INVALID_ARG, "kpm_plan_opts: value out of range");
 #ifndef KPM_EXPERIMENTAL
     if (o->experimental) return fail(KPM_ERR_UNSUPPORTED, "experimental kernels are built into libkpm_exp.so only");

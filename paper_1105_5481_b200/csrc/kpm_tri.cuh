@@ -30,6 +30,24 @@
 
 namespace kpm {
 
+// 2 H~ x - p at one site of a 2D lattice (Eq 18), with the factor 2 folded into the coefficients:
+// x-neighbours xm, xp with t2 = 2t; y-neighbours ym, yp with the Peierls phases in tph2 = 2t e^{i phi}
+// (Landau gauge: conj(e^{i phi}) yp + e^{i phi} ym, expanded: 8 real operations instead of 12);
+// e2 = 2 eps~ (or -2b/a).  Accumulated onto -p: 7 operations per component (real lattice: 5).
+template <bool PEIERLS>
+__device__ __forceinline__ double2 hop_step(double2 x, double2 xm, double2 xp, double2 ym, double2 yp, double e2,
+                                           double t2, double2 tph2, double2 p) {
+    double hx, hy;
+    if (PEIERLS) {
+        hx = fma(e2, x.x, fma(t2, xm.x + xp.x, fma(tph2.x, ym.x + yp.x, fma(tph2.y, yp.y - ym.y, -p.x))));
+        hy = fma(e2, x.y, fma(t2, xm.y + xp.y, fma(tph2.x, ym.y + yp.y, fma(tph2.y, ym.x - yp.x, -p.y))));
+    } else {
+        hx = fma(e2, x.x, fma(t2, (xm.x + xp.x) + (ym.x + yp.x), -p.x));
+        hy = fma(e2, x.y, fma(t2, (xm.y + xp.y) + (ym.y + yp.y), -p.y));
+    }
+    return make_double2(hx, hy);
+}
+
 struct TriGeom {
     int L0, L1;          // lattice extents
     int TX, TL, RG, G_L, PX;
@@ -44,8 +62,8 @@ struct TriGeom {
 };
 
 constexpr int kThreadsTri = 256;       // 8 warps: two per SM sub-partition, up to 255 registers
-constexpr int kSAT = 6;                // a_n ring (3 rows ahead of the row in use)
-constexpr int kSPT = 3;                // a_{n-1} ring
+constexpr int kSAT = 5;                // a_n ring (2 rows ahead of the rows in use)
+constexpr int kSPT = 4;                // a_{n-1} ring (3 ahead: ncu showed 30% of warp samples waiting on a 3-deep ring)
 
 // a_n slot: [3 halo sites][TX][3 halo sites], then eps~ as three 128-byte aligned pieces
 // [4 left (x0-4 ..)][TX][4 right] (TMA boxes need 16-byte multiples); a_{n-1} slot
@@ -197,11 +215,7 @@ __global__ void __launch_bounds__(NT, 1)
     };
     // 2 H~ x - p from the 4 neighbours (y neighbours carry the Peierls phase) and the site value
     auto step_val = [&](double2 x, double2 xm, double2 xp, double2 ym, double2 yp, double e, double2 ph, double2 p) {
-        double2 nb = add2(xm, xp);
-        if (PEIERLS) nb = add2(nb, add2(cmulc(ph, yp), cmul(ph, ym)));
-        else nb = add2(nb, add2(ym, yp));
-        const double2 h = fma2(e, x, scale2(g.t, nb));
-        return make_double2(fma(2.0, h.x, -p.x), fma(2.0, h.y, -p.y));
+        return hop_step<PEIERLS>(x, xm, xp, ym, yp, 2.0 * e, 2.0 * g.t, ph, p);
     };
     // slot byte offsets of tile x index lx (level 0: [-3, TX+2]; level -1 and 1: [-2, TX+1]; level 2: [-1, TX])
     auto oA = [&](int lx, int ll) { return (lx + 3) * SITE + ll * 16; };
@@ -224,7 +238,7 @@ __global__ void __launch_bounds__(NT, 1)
         const long long gstep = (long long)g.RG;
         const long long growstep = (long long)g.L0 * g.RG;
         if (PEIERLS) {
-            if (t < TX + 6) sphase[t] = __ldg(g.phase + (x0 + t - 3 + 2 * g.L0) % g.L0);
+            if (t < TX + 6) sphase[t] = scale2(2.0 * g.t, __ldg(g.phase + (x0 + t - 3 + 2 * g.L0) % g.L0));
             __syncthreads();
         }
         const int ia_seg = ia;
@@ -242,11 +256,17 @@ __global__ void __launch_bounds__(NT, 1)
         double2 XA[3][NPI], XB[3][NPI], XC[3][NPI];
         double XE[3][NPI];
         const int lx0 = k0 * NPI;  // first site of this thread
-        auto row = [&](const int q, const int u) {  // iteration q of the segment, u = q % 3
+        double2 PH[NPI];  // 2t e^{i phi} of the run's sites (Landau gauge: a function of x only)
+#pragma unroll
+        for (int p = 0; p < NPI; ++p) PH[p] = PEIERLS ? sphase[lx0 + p + 3] : make_double2(0.0, 0.0);
+        // S (steady): all three levels computed and owned (q in [4, H+2)) -- compile-time, so the
+        // levels of a row form one basic block the scheduler can interleave
+        auto row = [&](const int q, const int u, auto steady) {  // iteration q of the segment, u = q % 3
+            constexpr bool S = decltype(steady)::value;
             const int i0 = ia_seg + q;
             const int s1 = s0 + 1 == kSAT ? 0 : s0 + 1;
             const int s2 = s1 + 1 == kSAT ? 0 : s1 + 1;
-            if (q == 0) {
+            if (!S && q == 0) {
                 mbar_wait(fullA + s0, (uint32_t)((i0 / kSAT) & 1));
                 mbar_wait(fullA + s1, (uint32_t)(((i0 + 1) / kSAT) & 1));
             }
@@ -261,9 +281,9 @@ __global__ void __launch_bounds__(NT, 1)
             const unsigned char* B1m = ringB1 + ((u + 1) % 3) * SL.b1_bytes;          // row r1-2
             unsigned char* B2n = ringB2 + (q & 1) * SL.b2_bytes;                      // level 2 row r2 (written)
             const unsigned char* B2c = ringB2 + ((q & 1) ^ 1) * SL.b2_bytes;          // level 2 row r2-1 = r3
-            const bool do2 = q >= 2, do3 = q >= 4;
-            const bool own1 = q >= 2 && q < H + 2;  // r1 in [m0, m1)
-            const bool own2 = q >= 3 && q < H + 3;  // r2 in [m0, m1)
+            const bool do2 = S || q >= 2, do3 = S || q >= 4;
+            const bool own1 = S || (q >= 2 && q < H + 2);  // r1 in [m0, m1)
+            const bool own2 = S || (q >= 3 && q < H + 3);  // r2 in [m0, m1)
             double2* outB = g.outB + r2 * growstep + g0;
             double2* outC = g.outC + r3 * growstep + g0;
             double2(&am)[NPI] = XA[u];
@@ -294,7 +314,7 @@ __global__ void __launch_bounds__(NT, 1)
                     st(B2n + oB2(hx, hl), hc);
                 }
             }
-            if (q == 0) {
+            if (!S && q == 0) {
 #pragma unroll
                 for (int p = 0; p < NPI; ++p) {
                     am[p] = ld(A0 + oA(lx0 + p, l));
@@ -309,7 +329,7 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
                 for (int p = 0; p < NPI; ++p) {
                     const int lx = lx0 + p;
-                    const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                    const double2 ph = PH[p];
                     const double e1 = ONSITE ? reinterpret_cast<const double*>(A1 + SL.eps_m)[lx] : g.shift;
                     b[p] = step_val(ac[p], p == 0 ? xl : ac[p - 1], p == NPI - 1 ? xr : ac[p + 1], am[p], ap[p], e1, ph,
                                     ld(Pq + oP(lx, l)));
@@ -327,8 +347,7 @@ __global__ void __launch_bounds__(NT, 1)
                 const double2 xl = ld(B1c + oB1(lx0 - 1, l)), xr = ld(B1c + oB1(lx0 + NPI, l));
 #pragma unroll
                 for (int p = 0; p < NPI; ++p) {
-                    const int lx = lx0 + p;
-                    const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                    const double2 ph = PH[p];
                     c[p] = step_val(bc[p], p == 0 ? xl : bc[p - 1], p == NPI - 1 ? xr : bc[p + 1], bm[p], b[p],
                                     ONSITE ? e2[p] : g.shift, ph, am[p]);
                     if (own2) {
@@ -346,14 +365,13 @@ __global__ void __launch_bounds__(NT, 1)
                 const double2 xl = ld(B2c + oB2(lx0 - 1, l)), xr = ld(B2c + oB2(lx0 + NPI, l));
 #pragma unroll
                 for (int p = 0; p < NPI; ++p) {
-                    const int lx = lx0 + p;
-                    const double2 ph = PEIERLS ? sphase[lx + 3] : make_double2(0.0, 0.0);
+                    const double2 ph = PH[p];
                     const double2 d = step_val(cc[p], p == 0 ? xl : cc[p - 1], p == NPI - 1 ? xr : cc[p + 1], cm[p], c[p],
                                                ONSITE ? e3[p] : g.shift, ph, bm[p]);
                     __stcs(outC + p * gstep, d);
                     dot_acc<PEIERLS>(acc[4], cc[p], cc[p]);
                     dot_acc<PEIERLS>(acc[5], cc[p], d);
-                    if (tail) dot_acc<PEIERLS>(acc[6], d, d);
+                    dot_acc<PEIERLS>(acc[6], d, d);  // (kept only with the tail; no branch in the row)
                 }
             }
             __syncthreads();  // row q done: a_n row r1-1 and a_{n-1} row r1 are free; B rings advance
@@ -369,9 +387,15 @@ __global__ void __launch_bounds__(NT, 1)
             r3 = r3 + 1 == g.L1 ? 0 : r3 + 1;
         };
         for (int q0 = 0; q0 < H + 4; q0 += 3) {
-            row(q0, 0);
-            if (q0 + 1 < H + 4) row(q0 + 1, 1);
-            if (q0 + 2 < H + 4) row(q0 + 2, 2);
+            if (q0 >= 4 && q0 + 2 < H + 2) {
+                row(q0, 0, std::true_type{});
+                row(q0 + 1, 1, std::true_type{});
+                row(q0 + 2, 2, std::true_type{});
+            } else {
+                row(q0, 0, std::false_type{});
+                if (q0 + 1 < H + 4) row(q0 + 1, 1, std::false_type{});
+                if (q0 + 2 < H + 4) row(q0 + 2, 2, std::false_type{});
+            }
         }
         if (t == PRODUCER) {  // the segment's last two a_n rows are free too
             issueA((ia_seg + H + 4) % kSAT);

@@ -49,7 +49,7 @@ class kpm_plan_opts(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int32) for n in (
         "no_small", "no_tma", "no_two_step", "no_box3", "tma_lanes", "halo_warp", "ell_generic", "no_overlap",
         "no_fused_halo", "contiguous", "experimental", "exp_param", "two_step_ctas",
-        "no_pdl", "no_first_tile", "no_three_step", "no_zorder")] + [("reserved", ctypes.c_int32 * 3)]
+        "no_pdl", "no_first_tile", "no_three_step", "no_zorder", "no_four_step")] + [("reserved", ctypes.c_int32 * 2)]
 
 
 PLAN_OPTS = [f[0] for f in kpm_plan_opts._fields_ if f[0] != "reserved"]
@@ -331,6 +331,7 @@ class Handle:
         d["persist"] = int((info[7] >> 5) & 1)  # whole recursion in one cooperative launch (kpm_persist.cuh)
         d["ks"] = int(info[11])  # steps per launch of the deep temporal-blocking kernel (0 = not used)
         d["three_step"] = int((info[7] >> 6) & 1)  # three steps per launch (kpm_tri.cuh)
+        d["four_step"] = int((info[7] >> 7) & 1)  # four steps per launch (kpm_quad.cuh)
         return d
 
     def last_stats(self):

@@ -17,7 +17,7 @@ R = {"c2": 64, "c3": 128, "c4": 256, "c5": 32, "pd": 1792, "c2_csr": 64, "c3_csr
 json.dump({n: {"R_loc": R[n]} for n in sys.argv[2:]}, open(sys.argv[1] + "/specs.json", "w"))
 PY
 B="python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e"
-K="kpm_step_tri|kpm_step2_tma|kpm_step3_tma|kpm_step_tma|kpm_ell_step|kpm_dense_step"
+K="kpm_step_quad|kpm_step_tri|kpm_step2_tma|kpm_step3_tma|kpm_step_tma|kpm_ell_step|kpm_dense_step"
 for c in $NAMES; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1200 --csv \
     --log-file $OUT/launchlist_$c.csv $B ${ARGS[$c]} > /dev/null 2>&1

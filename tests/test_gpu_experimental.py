@@ -84,7 +84,7 @@ def test_multi_step_kernel_matches_oracle(kpm, case, N, ks):
     a *= 1.03
     r = ki.rademacher(13, R, lat["D"])
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b, no_small=1, experimental=kpm.EXP_KSTEP, exp_param=ks, no_three_step=1)
+    h = make(kpm, lat, a, b, no_small=1, experimental=kpm.EXP_KSTEP, exp_param=ks, no_three_step=1, no_four_step=1)
     info = h.plan_info(N, R)
     assert info["ks"] == ks, info
     mu = h.moments(N, R, 13)
@@ -96,7 +96,7 @@ def test_multi_step_kernel_matches_oracle(kpm, case, N, ks):
     M = N // 2
     rem = (M - 1) % ks
     assert launches == (M - 1) // ks + (rem // 2 + rem % 2 if info["two_step"] else rem), (launches, info)
-    h.set_plan_opts(no_small=1, no_three_step=1)
+    h.set_plan_opts(no_small=1, no_three_step=1, no_four_step=1)
     assert h.plan_info(N, R)["ks"] == 0
     assert normwise(h.moments(N, R, 13), ref) < TOL
 

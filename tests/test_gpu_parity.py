@@ -168,10 +168,10 @@ def test_two_step_pairs_and_single_steps(kpm, case, N):
     h = make(kpm, lat, a, b, no_small=1)
     info = h.plan_info(N, R)
     assert info["two_step"] == two_step_expected(lat, info, N), info
-    h.set_plan_opts(no_small=1, no_three_step=1)  # the two-step kernel itself
+    h.set_plan_opts(no_small=1, no_three_step=1, no_four_step=1)  # the two-step kernel itself
     mu2 = h.moments(N, R, 5)
     for xw in (1, 2):  # with and without the halo warp
-        h.set_plan_opts(no_small=1, halo_warp=xw, no_three_step=1)
+        h.set_plan_opts(no_small=1, halo_warp=xw, no_three_step=1, no_four_step=1)
         assert normwise(h.moments(N, R, 5), ref) < TOL
     h.set_plan_opts(no_small=1, no_two_step=1)
     assert h.plan_info(N, R)["two_step"] == 0
@@ -501,6 +501,41 @@ def test_first_step_tile_kernel(kpm, case, first_tile):
     assert normwise(hr.moments(N, R, 17), oracle.moments_doubling(H, a, b, r, N)) < TOL
 
 
+QUAD_CASES = {
+    "2d_R64": TMA_CASES["2d_R64"],
+    "2d_anderson_R16": TMA_CASES["2d_anderson_R16"],
+    "2d_peierls_R32": TMA_CASES["2d_peierls_R32"],
+    # 2 lane groups x 3 pencils, 20 rows over the grid: ragged segments, on-site + Peierls
+    "2d_peierls_anderson_R16": (lat_of(2, (192, 20), flux=1 / 8, W=1.0), 30, 16),
+}
+
+
+@pytest.mark.parametrize("case", list(QUAD_CASES))
+@pytest.mark.parametrize("N", [9, 10, 11, 12, 13, 14, 15, 16, 17, 40, 41])
+def test_four_step_kernel(kpm, case, N):
+    """2D: four recursion steps per launch (kpm_quad.cuh, the default for 2D tiles of >= 8 lanes), the step-count
+    remainder first (a three-step launch, a pair or a single step), odd-N tail inside the last
+    launch: the oracle's moments, per vector too, bitwise equal to the run from the same a_0."""
+    lat, _, R = QUAD_CASES[case]
+    H = oracle.lattice_csr(lat)
+    a, b = oracle.gershgorin(H)
+    b += 0.01 * a
+    a *= 1.02
+    r = ki.rademacher(23, R, lat["D"])
+    ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
+    h = make(kpm, lat, a, b, no_small=1)
+    info = h.plan_info(N, R)
+    nsteps = N // 2 - 1
+    assert info["four_step"] == (1 if nsteps >= 4 else 0) and info["ks"] == (4 if nsteps >= 4 else 3), info
+    mu = h.moments(N, R, 23)
+    assert normwise(mu, ref) < TOL
+    assert normwise(h.moments_ex(N, R, 23, flags=kpm.KPM_PER_VECTOR), ref_pv) < TOL
+    assert np.array_equal(h.moments_ex(N, R, 23, r0=r), mu)
+    assert np.array_equal(h.moments(N, R, 23), mu), "not deterministic"
+    _, launches, _ = h.last_timing()
+    assert launches == nsteps // 4 + (1 if nsteps % 4 else 0), (launches, nsteps)
+
+
 @pytest.mark.parametrize("case", ["2d_R64", "2d_anderson_R16", "2d_peierls_R32", "2d_R8_four_lanes"])
 @pytest.mark.parametrize("N", [7, 8, 9, 10, 11, 12, 13, 15, 16, 40])
 def test_three_step_kernel(kpm, case, N):
@@ -514,7 +549,7 @@ def test_three_step_kernel(kpm, case, N):
     a *= 1.02
     r = ki.rademacher(19, R, lat["D"])
     ref, ref_pv = oracle.moments_doubling(H, a, b, r, N, per_vector=True)
-    h = make(kpm, lat, a, b, no_small=1)  # (the default plan for 2D tiles of >= 8 lanes)
+    h = make(kpm, lat, a, b, no_small=1, no_four_step=1)  # (the plan for 2D tiles of >= 8 lanes without kpm_quad.cuh)
     info = h.plan_info(N, R)
     nsteps = N // 2 - 1
     tri = info["two_step"] == 1 and info["TL"] >= 8 and nsteps >= 3
