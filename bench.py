@@ -303,6 +303,10 @@ def main():
     ap.add_argument("--partition", default="vectors", choices=["vectors", "rows"],
                     help="vectors: SURVEY 8(e) P1; rows: slabs of the slowest dimension with halo exchange "
                          "every step (P2, BASELINE.json configs[4])")
+    ap.add_argument("--halo", default="ipc", choices=["ipc", "nccl"],
+                    help="row partition: ipc = KPM_COMM_IPC, the recursion kernels store boundary planes straight "
+                         "into the neighbours' ghost planes (CUDA IPC / NVLink peer memory, fused halo); nccl = "
+                         "KPM_COMM_NCCL send/recv of the planes overlapped with the interior")
     ap.add_argument("--plan", default="", help="kpm_plan_opts for A/B runs, e.g. 'no_two_step=1,tma_lanes=8'")
     args = ap.parse_args()
 
@@ -347,9 +351,15 @@ def main():
     if rows or args.format != "stencil":
         args.no_e2e = True  # (e2e below re-creates a stencil handle)
     if rows:
-        if world == 1:
-            dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % free_port(), rank=0, world_size=1)
-        part = (kpm.KPM_PART_ROWS, rank, world, kpm.KPM_COMM_NCCL, kpm.nccl_id_for_group())
+        if args.halo == "ipc":
+            name = [kpm.kpm_ipc_unique_name() if rank == 0 else None]
+            if world > 1:
+                dist.broadcast_object_list(name, src=0)
+            part = (kpm.KPM_PART_ROWS, rank, world, kpm.KPM_COMM_IPC, name[0])
+        else:
+            if world == 1:
+                dist.init_process_group("gloo", init_method="tcp://127.0.0.1:%d" % free_port(), rank=0, world_size=1)
+            part = (kpm.KPM_PART_ROWS, rank, world, kpm.KPM_COMM_NCCL, kpm.nccl_id_for_group())
         R_loc = R_total
     elif world > 1:
         part = ((kpm.KPM_PART_VECTORS, rank, world, kpm.KPM_COMM_NCCL, kpm.nccl_id_for_group()) if lib_comm
@@ -516,8 +526,11 @@ def main():
                 "vs_baseline": None, "dtype": "c128" if lat["flux"] else "f64",
                 "data": "synthetic (seeded Rademacher vectors generated on the GPU, lattice H of the config)",
                 "config": config_obj(args, cfg, lat, world, R_total, R_loc, args.format, l2_resident),
-                "collective": ("library NCCL all-reduce of the moment sums (KPM_COMM_NCCL)" if (lib_comm or rows)
-                               else ("gloo all-reduce of raw sums (ranks share GPUs)" if world > 1 else None)),
+                "collective": (("KPM_COMM_IPC: fused peer-plane halo stores in the recursion kernels, interprocess "
+                                "event ordering, rank-order sum of the moment sums over mapped workspaces")
+                               if rows and args.halo == "ipc" else
+                               ("library NCCL all-reduce of the moment sums (KPM_COMM_NCCL)" if (lib_comm or rows)
+                                else ("gloo all-reduce of raw sums (ranks share GPUs)" if world > 1 else None))),
                 "devices": min(world, ndev),
                 # the whole job's algorithmic bytes over the step time
                 "hbm_gbs_alg": alg_bytes / args.steps * world / (ms_per_step / 1000.0) / 1e9,
@@ -525,6 +538,7 @@ def main():
                 # the products actually performed are floor(N/2) per vector
                 "physical_updates_per_s": D * (N // 2) * R_total / (ms_per_step / 1000.0),
                 "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+                "halo_stats": h.last_stats() if rows else None,
                 "clocks": clk.summary(), "mu_check": {"mu0": float(mu_host[0]),
                                                         "max_abs_mu": float(np.abs(mu_host).max())}}
         print(json.dumps(line), file=_OUT, flush=True)

@@ -57,9 +57,12 @@ enum {
     KPM_ERR_UNSUPPORTED = 4, /* valid request this build does not implement */
     KPM_ERR_SPECTRUM = 5,    /* |mu_n| > mu_0 (1 + 1e-8) or non-finite: [b-a, b+a] does not
                                 enclose the spectrum (Eq 8 requires it).  Output still written. */
-    KPM_ERR_NCCL = 6         /* an NCCL call of the handle failed, or ncclCommGetAsyncError reported an
+    KPM_ERR_NCCL = 6,        /* an NCCL call of the handle failed, or ncclCommGetAsyncError reported an
                                 asynchronous error (a peer died, a network fault).  The communicator
                                 has been aborted; the handle is unusable except for kpm_destroy. */
+    KPM_ERR_COMM = 7         /* KPM_COMM_IPC: a peer rank failed, or made no progress for 600 s, or the
+                                ranks' calls disagree (N, R); the shared segment or a CUDA IPC mapping
+                                could not be set up.  The handle is unusable except for kpm_destroy. */
 };
 
 /* Element type of H and of the vector block. */
@@ -118,7 +121,18 @@ enum {
                            the recursion (Eq 16 is a sum over the ranks' vectors; PAPER.md:120-128,
                            Fig 3 step (3) PAPER.md:179), so kpm_moments returns mu on every rank.
                            KPM_PART_ROWS: NCCL send/recv of halo planes + the same all-reduce. */
-    KPM_COMM_LOCAL = 2  /* all ranks' handles in this process, driven by kpm_moments_group */
+    KPM_COMM_LOCAL = 2, /* all ranks' handles in this process, driven by kpm_moments_group */
+    KPM_COMM_IPC = 3    /* ranks are processes on ONE node (one per GPU, or several sharing a GPU), no
+                           NCCL: the handle opens the POSIX shared-memory segment `ipc_name` (made
+                           by kpm_ipc_unique_name on one rank and passed to all) and maps the other
+                           ranks' workspaces with CUDA IPC (NVLink peer memory across GPUs).
+                           KPM_PART_ROWS (stencils): the recursion kernels store their boundary
+                           planes straight into the neighbours' ghost planes (fused halo, SURVEY.md
+                           8(f) NEXT-4) and each launch waits on the device for the neighbours'
+                           previous launch (interprocess CUDA events); both partitions end with
+                           every rank summing all ranks' S[N] in rank order (Eq 16), so kpm_moments
+                           returns identical mu on every rank.  Calls are collective.  Errors:
+                           KPM_ERR_COMM. */
 };
 typedef struct {
     int32_t partition; /* KPM_PART_VECTORS: rank owns global vectors
@@ -145,10 +159,16 @@ typedef struct {
                                 sums are combined inside the row group (rank/world, comm); across the
                                 vworld groups the caller sums the raw sums (KPM_RAW_SUMS, allowed for
                                 row partitions) and calls kpm_assemble with the global R. */
+    const char* ipc_name;    /* KPM_COMM_IPC: the shared-memory segment name ("/...", from
+                                kpm_ipc_unique_name), the same on every rank; copied, not kept.
+                                Rank 0 removes the name once every rank has mapped the segment. */
 } kpm_dist;
 
 /* 128-byte NCCL unique id for KPM_COMM_NCCL (call on rank 0, broadcast to the others). */
 kpm_status kpm_nccl_unique_id(void* out128);
+/* A fresh shared-memory segment name for KPM_COMM_IPC ("/kpm-<pid>-<random>", NUL-terminated,
+ * at most 63 characters): call on one rank and pass the same string to every rank's kpm_dist. */
+kpm_status kpm_ipc_unique_name(char out64[64]);
 
 /* Slab of the row partition: planes [begin, begin + count) of an extent Lm.  Host only. */
 kpm_status kpm_slab_range(int64_t Lm, int32_t rank, int32_t world, int64_t* begin, int64_t* count);

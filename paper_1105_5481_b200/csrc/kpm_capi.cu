@@ -70,6 +70,8 @@ kpm_status fail(kpm_status st, const char* fmt, ...) {
         if (s_ != KPM_OK) return s_;         \
     } while (0)
 
+struct IpcComm;  // kpm_ipc.cuh (KPM_COMM_IPC)
+
 enum Kind { KIND_STENCIL = 0, KIND_ELL = 1, KIND_DENSE = 2 };
 constexpr int kThreads = 512;     // threads per CTA of the step kernels
 constexpr size_t kAlign = 256;
@@ -118,6 +120,7 @@ struct kpm_handle_s {
     int32_t* d_send = nullptr;       // [n_send] local rows the other ranks need, peer by peer, ascending
     std::vector<int64_t> roff, rcnt, soff, scnt;  // per peer: ghost / send list offsets and counts
     ncclComm_t nccl = nullptr;
+    IpcComm* ipc = nullptr;  // KPM_COMM_IPC: shared segment, launch events, mapped peer workspaces
     // workspace
     char* ws = nullptr;
     size_t ws_bytes = 0;
@@ -241,6 +244,10 @@ kpm_status nccl_poll(kpm_handle_s* h) {
     if (ae != ncclSuccess && ae != ncclInProgress) return nccl_fail(h, ae, "asynchronous NCCL error");
     return KPM_OK;
 }
+
+}  // namespace
+#include "kpm_ipc.cuh"
+namespace {
 
 // Wait for the handle's stream; with a communicator, poll its error state while waiting.
 kpm_status sync_stream(kpm_handle_s* h) {
@@ -551,7 +558,8 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     if (p->use_tma32) p->gx = std::max(p->gx, p->tma32_grid);
     p->nslots = N;
     if (h->rows) p->use_tma2 = p->use_tri = p->use_quad = p->use_tmak = p->use_tma32 = false;  // multi-step kernels need deep halos; not with slabs
-    p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL && !(flags & KPM_DIRECT) &&
+    p->overlap = h->rows && p->use_tma && h->nloc >= 3 && h->dist.comm != KPM_COMM_LOCAL &&
+                 h->dist.comm != KPM_COMM_IPC && !(flags & KPM_DIRECT) &&
                  !h->opts.no_overlap;
     if (p->overlap) p->gx = 3 * p->tma_grid;
     if (p->use_tmak && p->M - 1 < p->KSK) p->use_tmak = false;
@@ -609,11 +617,22 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
 kpm_status ensure_workspace(kpm_handle_s* h, size_t bytes) {
     if (h->ws_bytes >= bytes) return KPM_OK;
     if (!h->ws_own) return fail(KPM_ERR_OOM, "caller workspace has %zu bytes, need %zu", h->ws_bytes, bytes);
-    if (h->ws) cudaFreeAsync(h->ws, h->stream);
-    h->ws = nullptr;
-    h->ws_bytes = 0;
     void* p = nullptr;
-    cudaError_t e = cudaMallocAsync(&p, bytes, h->stream);
+    cudaError_t e;
+    if (h->ipc) {  // CUDA IPC handles need a plain allocation (not the stream-ordered pool)
+        if (h->ws) {
+            cudaStreamSynchronize(h->stream);
+            cudaFree(h->ws);
+        }
+        h->ws = nullptr;
+        h->ws_bytes = 0;
+        e = cudaMalloc(&p, bytes);
+    } else {
+        if (h->ws) cudaFreeAsync(h->ws, h->stream);
+        h->ws = nullptr;
+        h->ws_bytes = 0;
+        e = cudaMallocAsync(&p, bytes, h->stream);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(KPM_ERR_OOM, "cudaMallocAsync(%zu) failed: %s", bytes, cudaGetErrorString(e));
@@ -1187,8 +1206,11 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
         if (dist->world < 1 || dist->rank < 0 || dist->rank >= dist->world)
             return fail(KPM_ERR_INVALID_ARG, "bad rank %d / world %d", dist->rank, dist->world);
         if (dist->partition != KPM_PART_NONE) {
-            if (dist->comm != KPM_COMM_SELF && dist->comm != KPM_COMM_NCCL && dist->comm != KPM_COMM_LOCAL)
+            if (dist->comm != KPM_COMM_SELF && dist->comm != KPM_COMM_NCCL && dist->comm != KPM_COMM_LOCAL &&
+                dist->comm != KPM_COMM_IPC)
                 return fail(KPM_ERR_INVALID_ARG, "bad comm %d", dist->comm);
+            if (dist->comm == KPM_COMM_IPC && !dist->ipc_name)
+                return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_IPC needs ipc_name");
             if (dist->comm == KPM_COMM_NCCL && !dist->nccl_id)
                 return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_NCCL needs nccl_id");
         }
@@ -1223,6 +1245,15 @@ kpm_status new_handle(int32_t device, const kpm_dist* dist, kpm_handle_s** out) 
         return fail(KPM_ERR_CUDA, "stream/event creation failed: %s", cudaGetErrorString(e));
     }
     h->own_stream = true;
+    if (dist && dist->partition != KPM_PART_NONE && dist->comm == KPM_COMM_IPC) {
+        const kpm_status st = ipc_open(h, dist->ipc_name);
+        if (st != KPM_OK) {
+            const std::string msg = g_err;
+            kpm_destroy(h);
+            return fail(st, "%s", msg.c_str());
+        }
+    }
+    h->dist.ipc_name = nullptr;  // not kept
     *out = h;
     return KPM_OK;
 }
@@ -1694,7 +1725,8 @@ struct Run {
     bool more() const { return n <= nsteps; }
     // the vector partition's all-reduce of S runs inside the library (KPM_COMM_NCCL)
     bool vector_collective() const {
-        return !h->rows && h->dist.partition == KPM_PART_VECTORS && h->dist.comm == KPM_COMM_NCCL && h->nccl &&
+        return !h->rows && h->dist.partition == KPM_PART_VECTORS &&
+               ((h->dist.comm == KPM_COMM_NCCL && h->nccl) || h->dist.comm == KPM_COMM_IPC) &&
                !(flags & (KPM_RAW_SUMS | KPM_PER_VECTOR));
     }
     double2* fresh() const { return cur; }
@@ -2038,8 +2070,10 @@ const char* kpm_version(void) { return "kpm-b200 0.1 (sm_100a)"; }
 void kpm_destroy(kpm_handle h) {
     if (!h) return;
     cudaSetDevice(h->device);
-    if (h->ws_own && h->ws) cudaFreeAsync(h->ws, h->stream);
+    if (h->ws_own && h->ws && !h->ipc) cudaFreeAsync(h->ws, h->stream);
     if (h->stream) cudaStreamSynchronize(h->stream);
+    if (h->ws_own && h->ws && h->ipc) cudaFree(h->ws);
+    ipc_close(h);
     cudaFree(h->d_eps);
     cudaFree(h->d_epsf);
     cudaFree(h->d_phase);
@@ -2504,13 +2538,107 @@ kpm_status kpm_set_workspace(kpm_handle h, void* dev_ptr, size_t bytes) {
     return KPM_OK;
 }
 
+// KPM_COMM_IPC (kpm_ipc.cuh): one kpm_moments_ex call of a rank.  Row partition: the first
+// step's ghost planes are pulled from the neighbours' mapped blocks (peer copies), then every
+// recursion launch stores its boundary planes into the neighbours' ghost planes (fused halo) and
+// the next launch waits on the device for both neighbours' launch; if any rank's plan is not a
+// TMA march (or opts.no_fused_halo), ghost planes are pulled by peer copies after every launch.
+// Both partitions end with the rank-order sum of S (and Sv for rows) over all ranks.
+kpm_status moments_ipc(kpm_handle_s* h, int32_t N, int64_t R, uint64_t seed, const void* r0, uint32_t flags,
+                       void* out) {
+    IpcComm& I = *h->ipc;
+    if (h->rows && h->kind != KIND_STENCIL) return fail(KPM_ERR_UNSUPPORTED, "KPM_COMM_IPC row partitions: stencils only");
+    Run run;
+    kpm_status st = run.begin(h, N, R, seed, r0, flags);  // plan, workspace, first step (launch 0)
+    if (st != KPM_OK) {
+        I.seg->r[I.rank].failed.store(1);
+        h->dead = true;
+        return st;
+    }
+    auto body = [&]() -> kpm_status {
+        const bool fused_ok = h->rows && run.p.use_tma && !run.p.overlap && !h->opts.no_fused_halo;
+        KPM_TRY(ipc_publish(h, run.p, reinterpret_cast<char*>(run.P), reinterpret_cast<char*>(run.C),
+                            reinterpret_cast<char*>(run.S), reinterpret_cast<char*>(run.Sv), run.nsteps, fused_ok));
+        KPM_TRY(ipc_attach(h));
+        bool fused = fused_ok;
+        for (int q = 0; q < I.world; ++q) {
+            const IpcRank& r = I.seg->r[q];
+            if (r.N != N || r.steps != run.nsteps || (h->rows && r.R_loc != run.p.R_loc))
+                return ipc_fail(h, "KPM_COMM_IPC: %s", "ranks called with different N / R");
+            fused = fused && r.fused_ok;
+        }
+        if (!h->rows) {
+            while (run.more()) KPM_TRY(run.launch_next());
+            return KPM_OK;
+        }
+        int nb[2];
+        const int nn = ipc_neighbours(I, nb);
+        const int lo = nn ? nb[0] : I.rank, hi = nn ? nb[nn - 1] : I.rank;
+        const IpcRank& rl = I.seg->r[lo];
+        const size_t pb = run.plane_bytes();
+        // a block of rank q (its P or C, as `mine` is this rank's P or C) in this process's address space
+        auto blk = [&](int q, const double2* mine) -> char* {
+            const IpcRank& r = I.seg->r[q];
+            return I.peers[q].ws + (mine == run.P ? r.off_P : r.off_C);
+        };
+        auto pull = [&](double2* X) -> kpm_status {  // ghost planes of X from the neighbours' same block
+            const char* lo_last = blk(lo, X) + (rl.nloc - 1) * (int64_t)pb;
+            const char* hi_first = blk(hi, X);
+            KPM_CUDA(cudaMemcpyAsync(run.ghost_lo(X), lo_last, pb, cudaMemcpyDefault, h->stream));
+            KPM_CUDA(cudaMemcpyAsync(run.ghost_hi(X), hi_first, pb, cudaMemcpyDefault, h->stream));
+            h->halo_copies += 2;
+            return KPM_OK;
+        };
+        KPM_TRY(ipc_record(h));  // launch 0: the first step
+        KPM_TRY(ipc_wait_neighbours(h));
+        KPM_TRY(pull(run.fresh()));
+        while (run.more()) {
+            if (fused) {
+                // the neighbours' ghost planes of the block this launch overwrites (a_{n-1} -> a_{n+1})
+                run.tg.peer_lo = reinterpret_cast<double2*>(blk(lo, run.prev) + rl.nloc * (int64_t)pb);
+                run.tg.peer_hi = reinterpret_cast<double2*>(blk(hi, run.prev) - (int64_t)pb);
+            }
+            KPM_TRY(run.launch_next());
+            if (fused) h->fused_halo_launches++;
+            KPM_TRY(ipc_record(h));
+            KPM_TRY(ipc_wait_neighbours(h));
+            if (!fused) KPM_TRY(pull(run.fresh()));
+        }
+        run.tg.peer_lo = run.tg.peer_hi = nullptr;
+        return KPM_OK;
+    };
+    st = body();
+    if (st == KPM_OK) st = run.collect();
+    if (st == KPM_OK) st = sync_stream(h);
+    // sums over the ranks (Eq 16): all final -> every rank adds all ranks' sums in rank order ->
+    // all reads done -> each rank overwrites its own
+    const bool sum_S = h->rows || run.vector_collective();
+    const bool sum_Sv = h->rows;
+    std::vector<double> S, Sv;
+    if (st == KPM_OK) st = ipc_barrier(h);
+    if (st == KPM_OK && sum_S) st = ipc_sum(h, [](const IpcRank& r) { return r.off_S; }, (size_t)N, S);
+    if (st == KPM_OK && sum_Sv) st = ipc_sum(h, [](const IpcRank& r) { return r.off_Sv; }, (size_t)N * run.p.R_loc, Sv);
+    if (st == KPM_OK) st = ipc_barrier(h);
+    if (st != KPM_OK) {
+        I.seg->r[I.rank].failed.store(1);
+        h->dead = true;
+        return st;
+    }
+    if (sum_S) KPM_CUDA(cudaMemcpyAsync(run.S, S.data(), S.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    if (sum_Sv) KPM_CUDA(cudaMemcpyAsync(run.Sv, Sv.data(), Sv.size() * sizeof(double), cudaMemcpyHostToDevice, h->stream));
+    return run.output(out);
+}
+
 kpm_status kpm_moments_ex(kpm_handle h, int32_t N, int64_t R, uint64_t seed, const void* r0, uint32_t flags,
                           void* out) {
     if (!h) return fail(KPM_ERR_INVALID_ARG, "NULL handle");
     if (!out) return fail(KPM_ERR_INVALID_ARG, "NULL output");
-    if (h->dead) return fail(KPM_ERR_NCCL, "the handle's communicator was aborted by an earlier NCCL failure");
+    if (h->dead)
+        return h->ipc ? fail(KPM_ERR_COMM, "the handle's KPM_COMM_IPC partition failed in an earlier call")
+                      : fail(KPM_ERR_NCCL, "the handle's communicator was aborted by an earlier NCCL failure");
     if (h->rows && h->dist.comm == KPM_COMM_LOCAL)
         return fail(KPM_ERR_INVALID_ARG, "KPM_COMM_LOCAL slab handles run through kpm_moments_group");
+    if (h->ipc) return moments_ipc(h, N, R, seed, r0, flags, out);
     Run run;
     if (h->rows) run.exchange_hook = exchange_single;
     KPM_TRY(run.begin(h, N, R, seed, r0, flags));
@@ -2636,6 +2764,14 @@ kpm_status kpm_nccl_unique_id(void* out128) {
     ncclResult_t e = ncclGetUniqueId(&id);
     if (e != ncclSuccess) return fail(KPM_ERR_NCCL, "ncclGetUniqueId: %s", ncclGetErrorString(e));
     memcpy(out128, &id, sizeof id);
+    return KPM_OK;
+}
+
+kpm_status kpm_ipc_unique_name(char out64[64]) {
+    if (!out64) return fail(KPM_ERR_INVALID_ARG, "NULL output");
+    std::random_device rd;
+    const unsigned long long r = ((unsigned long long)rd() << 32) ^ rd();
+    snprintf(out64, 64, "/kpm-%d-%016llx", (int)getpid(), r);
     return KPM_OK;
 }
 

@@ -23,19 +23,20 @@ if not os.path.exists(LIB_PATH):
     raise ImportError(f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
                       "g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
 
-KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM_ERR_SPECTRUM, KPM_ERR_NCCL = range(7)
+(KPM_OK, KPM_ERR_INVALID_ARG, KPM_ERR_OOM, KPM_ERR_CUDA, KPM_ERR_UNSUPPORTED, KPM_ERR_SPECTRUM, KPM_ERR_NCCL,
+ KPM_ERR_COMM) = range(8)
 KPM_REAL64, KPM_COMPLEX128 = 0, 1
 KPM_KERNEL_JACKSON, KPM_KERNEL_NONE, KPM_KERNEL_LORENTZ, KPM_KERNEL_FEJER = 0, 1, 2, 3
 KPM_LORENTZ_DEFAULT_LAMBDA = 4.0
 KPM_PER_VECTOR, KPM_DIRECT, KPM_DEVICE_OUT, KPM_RAW_SUMS, KPM_DEVICE_IN, KPM_LOCAL = 1, 2, 4, 8, 16, 32
 KPM_PART_NONE, KPM_PART_VECTORS, KPM_PART_ROWS = 0, 1, 2
-KPM_COMM_SELF, KPM_COMM_NCCL, KPM_COMM_LOCAL = 0, 1, 2
+KPM_COMM_SELF, KPM_COMM_NCCL, KPM_COMM_LOCAL, KPM_COMM_IPC = 0, 1, 2, 3
 
 EXPORTS = ["kpm_create_stencil", "kpm_create_csr", "kpm_create_ell", "kpm_gershgorin_stencil",
            "kpm_gershgorin_csr", "kpm_set_stream", "kpm_workspace_size", "kpm_set_workspace",
            "kpm_moments", "kpm_moments_ex", "kpm_assemble", "kpm_dos", "kpm_last_timing",
            "kpm_step_bytes", "kpm_plan_info", "kpm_vector_range", "kpm_slab_range", "kpm_nccl_unique_id",
-           "kpm_moments_group", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moment_stats", "kpm_moments_local", "kpm_create_dense",
+           "kpm_moments_group", "kpm_ipc_unique_name", "kpm_dos_ex", "kpm_green", "kpm_damping", "kpm_moment_stats", "kpm_moments_local", "kpm_create_dense",
            "kpm_gershgorin_dense", "kpm_csr_partition", "kpm_last_stats", "kpm_set_plan_opts",
            "kpm_step_traffic", "kpm_destroy", "kpm_last_error", "kpm_version"]
 
@@ -59,7 +60,7 @@ EXP_3D_TWO_STEP, EXP_KSTEP, EXP_PERSIST = 1, 2, 3  # kpm_plan_opts.experimental
 class kpm_dist(ctypes.Structure):
     _fields_ = [("partition", ctypes.c_int32), ("rank", ctypes.c_int32), ("world", ctypes.c_int32),
                 ("comm", ctypes.c_int32), ("nccl_id", ctypes.c_void_p), ("vrank", ctypes.c_int32),
-                ("vworld", ctypes.c_int32)]
+                ("vworld", ctypes.c_int32), ("ipc_name", ctypes.c_char_p)]
 
 
 _P, _i32, _i64, _u32, _u64, _f64, _sz = (ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32,
@@ -92,6 +93,7 @@ _SIG = {
     "kpm_plan_info": [_P, _i32, _i64, _u32, _P],
     "kpm_slab_range": [_i64, _i32, _i32, _P, _P],
     "kpm_nccl_unique_id": [_P],
+    "kpm_ipc_unique_name": [_P],
     "kpm_moments_group": [_P, _i32, _i32, _i64, _u64, _P],
     "kpm_set_plan_opts": [_P, ctypes.POINTER(kpm_plan_opts)],
     "kpm_step_traffic": [_P, _P],
@@ -170,10 +172,14 @@ def _dist(dist):
     part, rank, world = dist[:3]
     comm = dist[3] if len(dist) > 3 else KPM_COMM_SELF
     nid = dist[4] if len(dist) > 4 else None
-    keep = ctypes.create_string_buffer(bytes(nid), 128) if nid is not None else None
     vrank, vworld = (int(dist[5]), int(dist[6])) if len(dist) > 6 else (0, 0)
+    if comm == KPM_COMM_IPC:  # dist[4]: the shared-segment name (kpm_ipc_unique_name)
+        name = nid.encode() if isinstance(nid, str) else bytes(nid)
+        st = kpm_dist(int(part), int(rank), int(world), int(comm), None, vrank, vworld, name)
+        return ctypes.byref(st), (st, name)
+    keep = ctypes.create_string_buffer(bytes(nid), 128) if nid is not None else None
     st = kpm_dist(int(part), int(rank), int(world), int(comm), ctypes.cast(keep, ctypes.c_void_p) if keep else None,
-                  vrank, vworld)
+                  vrank, vworld, None)
     return ctypes.byref(st), (st, keep)
 
 
@@ -458,6 +464,13 @@ def kpm_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(_lib.kpm_nccl_unique_id(buf))
     return buf.raw
+
+
+def kpm_ipc_unique_name() -> str:
+    """A fresh shared-segment name for KPM_COMM_IPC (make it on one rank, pass it to all)."""
+    buf = ctypes.create_string_buffer(64)
+    _check(_lib.kpm_ipc_unique_name(buf))
+    return buf.value.decode()
 
 
 def kpm_moments_group(handles, N, R, seed):

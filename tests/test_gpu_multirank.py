@@ -148,6 +148,19 @@ def test_bench_two_ranks_on_one_gpu():
     assert line["gpu_launches"] > 0 and line["roofline"]["achieved"] > 0
 
 
+def test_bench_rows_two_ranks_ipc_halo():
+    """bench.py --gpus 2 --partition rows: two processes (sharing the one GPU here), slabs of c3 with
+    the KPM_COMM_IPC fused halo -- every recursion launch stores into the peer's ghost planes."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--config", "c3", "--partition",
+                        "rows", "--steps", "1", "--warmup", "1", "--no-cpu-baseline"], capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"] == "rows2", line
+    assert line["halo_stats"]["fused_halo"] == 2048 // 2 - 1 and line["halo_stats"]["halo_copies"] == 2
+    assert line["mu_check"]["mu0"] == 1.0 and line["mu_check"]["max_abs_mu"] <= 1.0
+
+
 def test_plan_opts_validation(kpm):
     lat, N, R = CASES["2d_small_R5"]
     h = kpm.kpm_create_stencil(lat["ndim"], lat["L"], lat["t"], 4.0, 0.0)
