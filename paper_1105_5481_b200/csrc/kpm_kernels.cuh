@@ -60,6 +60,54 @@ __device__ __forceinline__ void dot_acc(double2& acc, double2 a, double2 b) {
     }
 }
 
+// ------------------------------------------------------------ CTA reductions
+// Fixed-order CTA sum of a per-thread double2 over the threads that share a vector lane
+// (lane = t % TL, TL a power of two; t = the linear thread index, threads t >= NT contribute
+// nothing).  TL < 32: a shuffle tree inside each warp (offsets 16, 8, .., TL: thread t % 32 < TL
+// ends up with its warp's partial of lane t % TL), then the NT / 32 warp partials in warp order;
+// TL >= 32: the NT / TL partials of a lane in thread order.  The order depends only on (TL, NT),
+// so repeated launches give identical bits.  Threads t < TL receive their lane's CTA total.  All
+// threads of the block must call it (it holds two __syncthreads); scratch: >= NT double2 of shared
+// memory.  (The former loop -- one thread per lane adding the NT / TL values serially -- cost up to
+// 64 dependent shared-memory round trips per sum: ~1/4 of a launch for 4-lane tiles.)
+template <int TL, int NT>
+__device__ __forceinline__ double2 cta_lane_sum(double2 v, int t, double2* scratch) {
+    static_assert(TL >= 1 && (TL & (TL - 1)) == 0 && NT % 32 == 0, "lanes a power of two, whole warps");
+    double2 s = make_double2(0.0, 0.0);
+    if (TL < 32) {
+#pragma unroll
+        for (int off = 16; off >= TL; off >>= 1) {
+            v.x += __shfl_down_sync(0xffffffffu, v.x, off);
+            v.y += __shfl_down_sync(0xffffffffu, v.y, off);
+        }
+        if (t < NT && (t & 31) < TL) scratch[(t >> 5) * TL + (t & 31)] = v;
+        __syncthreads();
+        if (t < TL)
+#pragma unroll
+            for (int w = 0; w < NT / 32; ++w) s = add2(s, scratch[w * TL + t]);
+    } else {
+        if (t < NT) scratch[t] = v;
+        __syncthreads();
+        if (t < TL)
+#pragma unroll
+            for (int j = 0; j < NT / TL; ++j) s = add2(s, scratch[j * TL + t]);
+    }
+    __syncthreads();
+    return s;
+}
+// The same with the lane count known only at run time (a power of two <= 32, NT a multiple of 32).
+template <int NT>
+__device__ __forceinline__ double2 cta_lane_sum_rt(double2 v, int t, int TL, double2* scratch) {
+    switch (TL) {
+        case 1: return cta_lane_sum<1, NT>(v, t, scratch);
+        case 2: return cta_lane_sum<2, NT>(v, t, scratch);
+        case 4: return cta_lane_sum<4, NT>(v, t, scratch);
+        case 8: return cta_lane_sum<8, NT>(v, t, scratch);
+        case 16: return cta_lane_sum<16, NT>(v, t, scratch);
+        default: return cta_lane_sum<32, NT>(v, t, scratch);
+    }
+}
+
 // ------------------------------------------------------------ operators H~
 struct StencilGeom {
     int L0, L1, L2;          // extents (sites = L0*L1*L2; the slowest used extent is local under KPM_PART_ROWS)
@@ -279,20 +327,15 @@ __device__ __forceinline__ void step_body(const OP& op, const VecArgs& v, const 
         }
     }
     // CTA-level finish of the per-vector partial sums, fixed order over the TS site rows.
+    // (blocks of 512 threads = TR lanes x TS site rows, TR a power of two <= 32; cta_lane_sum)
     extern __shared__ double2 sred[];
     const int tid = threadIdx.y * TR + threadIdx.x;
-    const int nthr = TR * TS;
-    sred[tid] = acc0;
-    sred[nthr + tid] = acc1;
-    sred[2 * nthr + tid] = acc2;
-    __syncthreads();
-    if (threadIdx.y == 0 && active) {
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            double* rowk = k == 0 ? v.red0 : (k == 1 ? v.red1 : (tail ? v.red2 : nullptr));
-            if (rowk == nullptr) continue;
-            double2 s = make_double2(0.0, 0.0);
-            for (int ty = 0; ty < TS; ++ty) s = add2(s, sred[k * nthr + ty * TR + threadIdx.x]);
+    for (int k = 0; k < 3; ++k) {
+        double* rowk = k == 0 ? v.red0 : (k == 1 ? v.red1 : (tail ? v.red2 : nullptr));
+        if (rowk == nullptr) continue;  // (uniform over the CTA)
+        const double2 s = cta_lane_sum_rt<512>(k == 0 ? acc0 : (k == 1 ? acc1 : acc2), tid, TR, sred);
+        if (threadIdx.y == 0 && active) {
             double* row = rowk + (size_t)blockIdx.x * v.RP;
             if (CPLX) {
                 row[rg] = s.x;

@@ -168,11 +168,8 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
     auto flush = [&](int lgf) {
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-            if (t < CONS) sred[t] = acc[k];
-            __syncthreads();
+            const double2 s = cta_lane_sum<TL, CONS>(acc[k], t, sred);  // (fixed-order shuffle tree)
             if (t < TL && g.red[k] != nullptr && (k < 8 || tail)) {
-                double2 s = make_double2(0.0, 0.0);
-                for (int j = t; j < CONS; j += TL) s = add2(s, sred[j]);
                 const int v = lgf * TL + t;
                 double* row = g.red[k] + (size_t)blockIdx.x * g.RP;
                 if (PEIERLS) {
@@ -182,7 +179,6 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
                     row[2 * v + 1] = s.y;
                 }
             }
-            __syncthreads();
         }
 #pragma unroll
         for (int k = 0; k < 9; ++k) acc[k] = make_double2(0.0, 0.0);

@@ -236,11 +236,17 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
     auto flush = [&](int lgf) {
 #pragma unroll
         for (int k = 0; k < 5; ++k) {
-            if (t < CONS) sred[t] = acc[k];
-            __syncthreads();
+            double2 s = make_double2(0.0, 0.0);
+            if (TL <= 4) {  // few lanes: 64+ values per lane -- shuffle tree (cta_lane_sum)
+                s = cta_lane_sum<TL, CONS>(acc[k], t, sred);
+            } else {
+                if (t < CONS) sred[t] = acc[k];
+                __syncthreads();
+                if (t < TL)
+                    for (int j = t; j < CONS; j += TL) s = add2(s, sred[j]);
+                __syncthreads();
+            }
             if (t < TL) {
-                double2 s = make_double2(0.0, 0.0);
-                for (int j = t; j < CONS; j += TL) s = add2(s, sred[j]);
                 const int v = lgf * TL + t;
                 if (PEIERLS) {
                     sacc[k * g.RP + v] += s.x;
@@ -249,7 +255,6 @@ __global__ void __launch_bounds__(Threads2<XW>::N, MINB)
                     sacc[k * g.RP + 2 * v + 1] += s.y;
                 }
             }
-            __syncthreads();
         }
 #pragma unroll
         for (int k = 0; k < 5; ++k) acc[k] = make_double2(0.0, 0.0);
