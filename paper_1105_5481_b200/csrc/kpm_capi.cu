@@ -476,8 +476,9 @@ void plan_tma(const kpm_handle_s* h, uint32_t flags, Plan* p) {
             p->use_tri = !h->opts.no_three_step && TL >= 8 && TL <= 32 && TL * p->TX2 == 1024 && h->L[0] >= 8 &&
                          h->L[1] >= 6 && smt <= (size_t)h->smem_optin;
             p->tri_smem = smt;
-            // four steps per launch: 8-lane x 64-site tiles (2 sites per thread run)
-            const int tlq = 8, txq = 64;
+            // four steps per launch: 8-lane x 64-site tiles (2 sites per thread run); 4-lane x 128-site
+            // tiles when the lanes are not a multiple of 8 (small R per GPU)
+            const int tlq = RG % 8 == 0 ? 8 : 4, txq = tlq == 8 ? 64 : 128;
             const size_t smq = kpm::quad_smem_bytes(txq, tlq, on);
             p->use_quad = !h->opts.no_four_step && RG % tlq == 0 && h->L[0] % txq == 0 && h->L[1] >= 8 &&
                           smq <= (size_t)h->smem_optin;
@@ -932,7 +933,7 @@ kpm_status make_buf_maps(const kpm_handle_s* h, const Plan& p, void* base, BufMa
     if (p.use_quad) {
         KPM_TRY(make_vec_map(h, p, base, p.TXQ, 1, 1, &bm->AQ, p.TLQ));
         KPM_TRY(make_vec_map(h, p, base, 4, 1, 1, &bm->AQ4, p.TLQ));
-        KPM_TRY(make_vec_map(h, p, base, 3, 1, 1, &bm->AQ3, p.TLQ));
+        KPM_TRY(make_vec_map(h, p, base, kpm::quad_php(p.TLQ), 1, 1, &bm->AQ3, p.TLQ));
     }
     if (p.use_tma3) {
         KPM_TRY(make_vec_map(h, p, base, p.TX + 2, p.TY, 1, &bm->Box3));
@@ -1037,10 +1038,10 @@ kpm_status launch_tri_s(kpm_handle_s* h, const Plan& p, const BufMaps& A, const 
     return launch_tri_t<TL, TX, false, false>(h, p, A, P, E, E4, g, tail);
 }
 
-template <bool ONSITE, bool PEIERLS>
+template <int TL, int TX, bool ONSITE, bool PEIERLS>
 kpm_status launch_quad_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                          const CUtensorMap& E4, const kpm::QuadGeom& g, int tail) {
-    auto kern = kpm::kpm_step_quad_kernel<8, 64, ONSITE, PEIERLS>;
+    auto kern = kpm::kpm_step_quad_kernel<TL, TX, ONSITE, PEIERLS>;
     KPM_TRY(set_smem((const void*)kern, p.quad_smem, h->device));
     return launch_k(h, h->stream, kern, dim3(p.quad_grid), dim3(kpm::kThreadsQuad), p.quad_smem, A.AQ, A.AQ4, P.AQ, P.AQ3,
                     E, E4, g, tail);
@@ -1048,10 +1049,16 @@ kpm_status launch_quad_t(kpm_handle_s* h, const Plan& p, const BufMaps& A, const
 
 kpm_status launch_quad(kpm_handle_s* h, const Plan& p, const BufMaps& A, const BufMaps& P, const CUtensorMap& E,
                        const CUtensorMap& E4, const kpm::QuadGeom& g, int tail) {
-    if (p.TLQ != 8 || p.TXQ != 64) return fail(KPM_ERR_UNSUPPORTED, "no four-step kernel for TL=%d TX=%d", p.TLQ, p.TXQ);
     const bool on = h->d_eps != nullptr;
-    if (is_cplx(h)) return on ? launch_quad_t<true, true>(h, p, A, P, E, E4, g, tail) : launch_quad_t<false, true>(h, p, A, P, E, E4, g, tail);
-    return on ? launch_quad_t<true, false>(h, p, A, P, E, E4, g, tail) : launch_quad_t<false, false>(h, p, A, P, E, E4, g, tail);
+    if (p.TLQ == 8 && p.TXQ == 64) {
+        if (is_cplx(h)) return on ? launch_quad_t<8, 64, true, true>(h, p, A, P, E, E4, g, tail) : launch_quad_t<8, 64, false, true>(h, p, A, P, E, E4, g, tail);
+        return on ? launch_quad_t<8, 64, true, false>(h, p, A, P, E, E4, g, tail) : launch_quad_t<8, 64, false, false>(h, p, A, P, E, E4, g, tail);
+    }
+    if (p.TLQ == 4 && p.TXQ == 128) {  // 4-lane tiles (e.g. 8 real / 4 complex vectors per GPU)
+        if (is_cplx(h)) return on ? launch_quad_t<4, 128, true, true>(h, p, A, P, E, E4, g, tail) : launch_quad_t<4, 128, false, true>(h, p, A, P, E, E4, g, tail);
+        return on ? launch_quad_t<4, 128, true, false>(h, p, A, P, E, E4, g, tail) : launch_quad_t<4, 128, false, false>(h, p, A, P, E, E4, g, tail);
+    }
+    return fail(KPM_ERR_UNSUPPORTED, "no four-step kernel for TL=%d TX=%d", p.TLQ, p.TXQ);
 }
 
 // instantiated tile shapes of the three-step kernel (TX * TL = 1024 lanes per row tile)

@@ -42,10 +42,19 @@ struct QuadGeom {
 };
 
 constexpr int kThreadsQuad = 256;       // 8 warps: two per SM sub-partition, up to 255 registers
-constexpr int kSAQ = 10;                // a_n ring: rows r1-2 .. r1+1 in use (eps of level 3's halo) + 6 ahead
-constexpr int kSPQ = 6;                 // a_{n-1} ring (5 ahead)
+#ifndef KPM_SAQ
+#define KPM_SAQ 10
+#endif
+#ifndef KPM_SPQ
+#define KPM_SPQ 6
+#endif
+constexpr int kSAQ = KPM_SAQ;           // a_n ring: rows r1-2 .. r1+1 in use (eps of level 3's halo) + 6 ahead
+constexpr int kSPQ = KPM_SPQ;           // a_{n-1} ring (5 ahead)
 
 __host__ __device__ constexpr int quad_runs(int TL) { return 256 / TL; }  // runs per row
+// a_{n-1} halo sites per side: 3, or 4 when 3 sites are not a multiple of 128 bytes (4-lane tiles:
+// every TMA destination of a slot stays 128-byte aligned)
+__host__ __device__ constexpr int quad_php(int TL) { return (3 * TL * 16) % 128 == 0 ? 3 : 4; }
 // a_n slot: [4 halo][TX][4 halo] sites, then eps~ pieces [4 left][TX][4 right] (128-byte aligned);
 // a_{n-1} slot [3][TX][3]; level rings keep the halo sites and the two ends of every run:
 // level 1 [3 halo][2 per run][3 halo], level 2 [2][..][2], level 3 [1][..][1].
@@ -57,7 +66,7 @@ struct QuadLayout {
           eps_l((TX + 8) * TL * 16),
           eps_m((TX + 8) * TL * 16 + 128),
           eps_r((TX + 8) * TL * 16 + 128 + (TX * 8 + 127) / 128 * 128),
-          p_bytes(((TX + 6) * TL * 16 + 127) / 128 * 128),
+          p_bytes(((TX + 2 * quad_php(TL)) * TL * 16 + 127) / 128 * 128),
           b1_bytes(((2 * quad_runs(TL) + 6) * TL * 16 + 127) / 128 * 128),
           b2_bytes(((2 * quad_runs(TL) + 4) * TL * 16 + 127) / 128 * 128),
           b3_bytes(((2 * quad_runs(TL) + 2) * TL * 16 + 127) / 128 * 128) {}
@@ -79,7 +88,7 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
     kpm_step_quad_kernel(const __grid_constant__ CUtensorMap mapA,    // a_n main box {2TL, TX, 1}
                          const __grid_constant__ CUtensorMap mapA4,   // a_n 4-site box {2TL, 4, 1}
                          const __grid_constant__ CUtensorMap mapP,    // a_{n-1} main box
-                         const __grid_constant__ CUtensorMap mapP3,   // a_{n-1} 3-site box {2TL, 3, 1}
+                         const __grid_constant__ CUtensorMap mapP3,   // a_{n-1} halo box {2TL, PHP, 1}
                          const __grid_constant__ CUtensorMap mapE,    // eps~ box {TX, 1}
                          const __grid_constant__ CUtensorMap mapE4,   // eps~ box {4, 1}
                          const QuadGeom g, const int tail) {
@@ -88,7 +97,8 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
     constexpr int PRODUCER = CONS - 1;  // (chains: warps 0 and 1)
     constexpr int KSTEP = CONS / TL;  // runs per row
     constexpr int NPI = TX / KSTEP;   // sites per run
-    static_assert(TX % KSTEP == 0 && NPI >= 1 && TL * 16 >= 128 && 4 * TL <= 32, "tile shape");
+    static_assert(TX % KSTEP == 0 && NPI >= 1 && TL * 16 >= 64 && 4 * TL <= 32, "tile shape");
+    constexpr int PHP = quad_php(TL);  // a_{n-1} halo sites per side in a slot (3 needed)
     constexpr int SITE = TL * 16;
     constexpr QuadLayout SL(TX, TL, ONSITE);
     extern __shared__ __align__(128) unsigned char smem[];
@@ -129,12 +139,12 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
         if (!cp.valid) return;
         const int row = cp.row, c0 = cp.c0, x0 = cp.x0, xl = cp.xl, xr = cp.xr;
         unsigned char* dst = ringP + slot * SL.p_bytes;
-        mbar_expect_tx(fullP + slot, (TX + 6) * SITE);
+        mbar_expect_tx(fullP + slot, (TX + 2 * PHP) * SITE);
         const uint64_t pol = pol_smem;
         tma_load_hint(dst, &mapP3, fullP + slot, c0, xl, row, pol);
-        tma_load_hint(dst + 3 * SITE, &mapP, fullP + slot, c0, x0, row, pol);
-        tma_load_hint(dst + (TX + 3) * SITE, &mapP3, fullP + slot, c0, xr, row, pol);
-        cp.next(g, 6);
+        tma_load_hint(dst + PHP * SITE, &mapP, fullP + slot, c0, x0, row, pol);
+        tma_load_hint(dst + (TX + PHP) * SITE, &mapP3, fullP + slot, c0, xr, row, pol);
+        cp.next(g, 6, PHP);
     };
     if (t == PRODUCER) {
         for (int i = 0; i < kSAQ; ++i) mbar_init(fullA + i, 1);
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
         }
         pol_smem = policy_evict_first();
         ca.init(g, w_begin, w_end, 8);
-        cp.init(g, w_begin, w_end, 6);
+        cp.init(g, w_begin, w_end, 6, PHP);
         for (int i = 0; i < kSAQ; ++i) issueA(i);
         for (int i = 0; i < kSPQ; ++i) issueP(i);
     }
@@ -189,7 +199,7 @@ __global__ void __launch_bounds__(kThreadsQuad, 1)
     // slot offsets of tile x index lx: level 0 [-4, TX+3], level -1 [-3, TX+2]; level rings keep the
     // halo and the run ends: bix maps an interior run end to its packed index
     auto oA = [&](int lx, int ll) { return (lx + 4) * SITE + ll * 16; };
-    auto oP = [&](int lx, int ll) { return (lx + 3) * SITE + ll * 16; };
+    auto oP = [&](int lx, int ll) { return (lx + PHP) * SITE + ll * 16; };
     auto bix = [&](int lx) { return lx < 0 ? lx : (lx >= TX ? 2 * KSTEP + (lx - TX) : 2 * (lx / NPI) + (lx % NPI != 0)); };
     auto oB1 = [&](int lx, int ll) { return (bix(lx) + 3) * SITE + ll * 16; };
     auto oB2 = [&](int lx, int ll) { return (bix(lx) + 2) * SITE + ll * 16; };
