@@ -543,6 +543,10 @@ kpm_status make_plan(const kpm_handle_s* h, int32_t N, int64_t R, uint32_t flags
     p->gy = (p->RG + tr - 1) / tr;
     const long long site_ctas = (h->D + p->TS - 1) / p->TS;
     p->gx = (int)std::min<long long>(site_ctas, 2LL * h->num_sms);
+    // the staged ELL kernel (one 512-thread CTA per SM: 128 registers) walks its tiles grid-stride:
+    // one wave of CTAs over the (gx, gy) grid instead of 2 gy waves
+    if (h->kind == KIND_ELL && h->K > 0 && h->K <= kpm::kEllKMax && !h->opts.ell_generic)
+        p->gx = (int)std::max<long long>(1, std::min<long long>(site_ctas, h->num_sms / std::max(1, p->gy)));
     plan_tma(h, flags, p);
     if (p->use_tma) p->gx = p->tma_grid;
     if (h->kind == KIND_DENSE) p->gx = (int)(h->Dp / kpm::kDBM);  // partial rows = M tiles
