@@ -73,3 +73,35 @@ def test_invalid_arguments_are_rejected():
     with pytest.raises(kpm.KPMError) as e:
         kpm.kpm_create_stencil(2, (8, 8), -1.0, a=-1.0, b=0.0)       # a <= 0
     assert e.value.status == kpm.KPM_ERR_INVALID_ARG
+
+
+def test_ipc_unique_name_and_dist_layout():
+    """KPM_COMM_IPC plumbing that needs no GPU: fresh shared-segment names ("/kpm-<pid>-<hex>",
+    < 64 bytes, distinct per call) and the ctypes kpm_dist carrying the name at the end."""
+    import ctypes
+    from paper_1105_5481_b200 import kpm
+    names = {kpm.kpm_ipc_unique_name() for _ in range(8)}
+    assert len(names) == 8
+    for n in names:
+        assert re.fullmatch(r"/kpm-%d-[0-9a-f]{16}" % os.getpid(), n) and len(n) < 64
+    ref, keep = kpm._dist((kpm.KPM_PART_ROWS, 1, 3, kpm.KPM_COMM_IPC, "/kpm-x"))
+    st = keep[0]
+    assert (st.partition, st.rank, st.world, st.comm) == (kpm.KPM_PART_ROWS, 1, 3, kpm.KPM_COMM_IPC)
+    assert st.ipc_name == b"/kpm-x" and st.nccl_id is None
+    assert kpm_dist_fields_match_header()
+
+
+def kpm_dist_fields_match_header():
+    """the binding's kpm_dist field order equals the header's struct members"""
+    from paper_1105_5481_b200 import kpm
+    src = re.sub(r"/\*.*?\*/", "", open(os.path.join(ROOT, "include", "kpm.h")).read(), flags=re.S)
+    body = re.search(r"typedef struct \{([^}]*)\} kpm_dist;", src).group(1)
+    names = []
+    for decl in body.split(";"):
+        decl = decl.strip()
+        if not decl:
+            continue
+        head, *rest = decl.split(",")
+        names.append(re.findall(r"(\w+)\s*$", head)[0])
+        names += [r.strip().lstrip("*") for r in rest]
+    return names == [f[0] for f in kpm.kpm_dist._fields_]
