@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
             prefetch_tmap(&mapP);
             if (ONSITE) prefetch_tmap(&mapE);
             const uint64_t pol_first = policy_evict_first();
+            const uint64_t pol_last = policy_evict_last();
             constexpr uint32_t bytesA = S::VEC + (ONSITE ? TX * TY * 8 : 0);
             long long ia = 0, ip = 0;
             Sched sq = sched_begin(g);
@@ -98,9 +99,11 @@ __global__ void __launch_bounds__(kTmaThreads, 1)
                     if (ia >= kSA) mbar_wait(emptyA + slot, (uint32_t)(((ia / kSA) - 1) & 1));
                     unsigned char* dst = ringA + slot * S::BYTES;
                     mbar_expect_tx(fullA + slot, bytesA);
-                    tma_load(dst, &mapRow, fullA + slot, c0, xb, yt, m);
-                    tma_load(dst + S::ROW, &mapBox, fullA + slot, c0, xb, y0, m);
-                    tma_load(dst + (TY + 1) * S::ROW, &mapRow, fullA + slot, c0, xb, yb, m);
+// a_n boxes with the L2 evict-last policy: the halo rows and columns a neighbouring pencil re-reads
+                    // stay in L2 behind the streamed a_{n-1} / a_{n+1} (A/B: c3 1087 -> 1078 ms, c5 9013 -> 8818 ms)
+                    tma_load_hint(dst, &mapRow, fullA + slot, c0, xb, yt, m, pol_last);
+                    tma_load_hint(dst + S::ROW, &mapBox, fullA + slot, c0, xb, y0, m, pol_last);
+                    tma_load_hint(dst + (TY + 1) * S::ROW, &mapRow, fullA + slot, c0, xb, yb, m, pol_last);
                     if (ONSITE) tma_load(dst + S::EPS, &mapE, fullA + slot, x0, y0, m - g.ghost);
                     ++ia;
                     if (q >= 1 && q - 1 < H) {
