@@ -97,9 +97,10 @@ struct kpm_handle_s {
     double2* d_phase = nullptr;   // e^{i 2 pi phi x}
     // ELL
     int K = 0;
-    int32_t* d_col = nullptr;     // [K][ell_ld]
-    double* d_val = nullptr;      // [K][ell_ld] (x2 for complex)
-    int64_t ell_ld = 0;           // row stride of the ELL arrays: D rounded up to 256
+    int32_t* d_col = nullptr;     // [ell_ld rows][ell_kp] (row-major)
+    double* d_val = nullptr;      // [ell_ld rows][ell_kp] (x2 for complex)
+    int64_t ell_ld = 0;           // stored rows: D rounded up to 2048 (whole tiles)
+    int ell_kp = 0;               // stored entries per row: K rounded up to a multiple of 4
     // dense H~ (the paper's variant): Dp x Dp row-major, H / a, zero padded (kpm_dense.cuh)
     double* d_dense = nullptr;
     int64_t Dp = 0;
@@ -686,12 +687,18 @@ kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, i
     dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
     const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX);
     const bool wide = (double)(h->D + h->n_ghost) * p.RG >= 2147483648.0;  // 32-bit element offsets otherwise
-    auto kern = wide ? (h->K <= 4 ? kpm::kpm_ell_step_kernel<CPLX, 4, true>
-                                  : (h->K <= 8 ? kpm::kpm_ell_step_kernel<CPLX, 8, true> : kpm::kpm_ell_step_kernel<CPLX, 16, true>))
-                     : (h->K <= 4 ? kpm::kpm_ell_step_kernel<CPLX, 4, false>
-                                  : (h->K <= 8 ? kpm::kpm_ell_step_kernel<CPLX, 8, false> : kpm::kpm_ell_step_kernel<CPLX, 16, false>));
+    auto pick = [&](auto w) {
+        constexpr bool W = decltype(w)::value;
+        switch (h->ell_kp) {
+            case 4: return kpm::kpm_ell_step_kernel<CPLX, 4, W>;
+            case 8: return kpm::kpm_ell_step_kernel<CPLX, 8, W>;
+            case 12: return kpm::kpm_ell_step_kernel<CPLX, 12, W>;
+            default: return kpm::kpm_ell_step_kernel<CPLX, 16, W>;
+        }
+    };
+    auto kern = wide ? pick(std::true_type{}) : pick(std::false_type{});
     KPM_TRY(set_smem((const void*)kern, smem, h->device));
-    const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld};
+    const kpm::EllOp<CPLX> op{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp};
     return launch_k(h, h->stream, kern, grid, block, smem, op, v, tail);
 }
 
@@ -706,8 +713,8 @@ kpm_status launch_small_t(kpm_handle_s* h, const Plan& p, const OP& op, const kp
 kpm_status launch_small(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int from_buf, int N, double* part) {
     using namespace kpm;
     if (h->kind == KIND_ELL) {
-        if (is_cplx(h)) return launch_small_t<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld}, v, from_buf, N, part);
-        return launch_small_t<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld}, v, from_buf, N, part);
+        if (is_cplx(h)) return launch_small_t<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp}, v, from_buf, N, part);
+        return launch_small_t<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp}, v, from_buf, N, part);
     }
     const StencilGeom g = stencil_geom(h);
     const bool on = h->d_eps != nullptr;
@@ -761,8 +768,8 @@ kpm_status launch(kpm_handle_s* h, const Plan& p, int mode, const kpm::VecArgs& 
         ell_smem_bytes(kThreads, p.TS, h->K, is_cplx(h)) <= (size_t)h->smem_optin)
         return is_cplx(h) ? launch_ell_t<true>(h, p, v, tail) : launch_ell_t<false>(h, p, v, tail);
     if (h->kind == KIND_ELL) {
-        if (is_cplx(h)) return launch_mode<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld}, mode, v, tail);
-        return launch_mode<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld}, mode, v, tail);
+        if (is_cplx(h)) return launch_mode<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp}, mode, v, tail);
+        return launch_mode<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp}, mode, v, tail);
     }
     const StencilGeom g = stencil_geom(h);
     const bool on = h->d_eps != nullptr;
@@ -839,9 +846,9 @@ kpm_status launch_persist(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v,
     using namespace kpm;
     if (h->kind == KIND_ELL) {
         if (is_cplx(h))
-            return launch_persist_op<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld}, v, first_buf, N,
+            return launch_persist_op<true>(h, p, EllOp<true>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp}, v, first_buf, N,
                                            slot, part);
-        return launch_persist_op<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, (int)h->ell_ld}, v, first_buf,
+        return launch_persist_op<false>(h, p, EllOp<false>{(int)h->D, h->K, h->d_col, h->d_val, -h->b / h->a, h->ell_kp}, v, first_buf,
                                         N, slot, part);
     }
     const StencilGeom g = stencil_geom(h);
@@ -2379,17 +2386,20 @@ kpm_status kpm_create_ell(int64_t D, int32_t K, const int32_t* col, const void* 
     kpm_status st = KPM_OK;
     if (dist && dist->partition == KPM_PART_ROWS) st = ell_rows_setup(h, dist, c, v, w);
     if (st == KPM_OK && K > 0) {
-        // device layout [K][ld], ld = D rounded up to 2048 rows (the largest ELL tile): every tile
-        // slice of an entry column is one aligned run inside the array (bulk copies into shared
-        // memory, kpm_ell.cuh); pad rows hold column 0, value 0 and are never used
-        const int64_t Dl = h->D, ld = (Dl + 2047) / 2048 * 2048;
+        // device layout row-major [ld][KP]: ld = D rounded up to 2048 rows (the largest ELL tile),
+        // KP = K rounded up to a multiple of 4, so a tile of rows is one contiguous, 16-byte aligned run
+        // of each array (one bulk copy into shared memory, kpm_ell.cuh) and a row's indices are KP/4
+        // 16-byte loads; padding entries are (row, 0), pad rows (0, 0) and are never used
+        const int64_t Dl = h->D, ld = (Dl + 2047) / 2048 * 2048, KP = kpm::ell_kp(K);
         h->ell_ld = ld;
-        std::vector<int32_t> cp((size_t)K * ld, 0);
-        std::vector<double> vp((size_t)K * ld * w, 0.0);
-        for (int64_t k = 0; k < K; ++k) {
-            std::copy(c.begin() + k * Dl, c.begin() + (k + 1) * Dl, cp.begin() + k * ld);
-            std::copy(v.begin() + k * Dl * w, v.begin() + (k + 1) * Dl * w, vp.begin() + k * ld * w);
-        }
+        h->ell_kp = (int)KP;
+        std::vector<int32_t> cp((size_t)KP * ld, 0);
+        std::vector<double> vp((size_t)KP * ld * w, 0.0);
+        for (int64_t i = 0; i < Dl; ++i)
+            for (int64_t k = 0; k < KP; ++k) {
+                cp[i * KP + k] = k < K ? c[k * Dl + i] : (int32_t)i;
+                for (int q = 0; q < w && k < K; ++q) vp[(i * KP + k) * w + q] = v[(k * Dl + i) * w + q];
+            }
         cudaError_t ce = cudaMalloc(&h->d_col, cp.size() * sizeof(int32_t));
         if (ce == cudaSuccess) ce = cudaMalloc(&h->d_val, vp.size() * sizeof(double));
         if (ce == cudaSuccess) ce = cudaMemcpy(h->d_col, cp.data(), cp.size() * sizeof(int32_t), cudaMemcpyHostToDevice);

@@ -22,7 +22,7 @@
 
 #include <cstdint>
 
-#include "kpm_ell.cuh"  // cp_async_commit
+#include "kpm_kernels.cuh"
 
 namespace kpm {
 
@@ -31,6 +31,7 @@ constexpr int kDHS = kDBK + 4;  // smem row stride (doubles) of the H tile   [64
 constexpr int kDAS = kDBN + 4;  // smem row stride (doubles) of the a_n tile [32][68]
 constexpr size_t kDenseSmem = (size_t)kDStages * (kDBM * kDHS + kDBK * kDAS) * sizeof(double);
 
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem_dst)),
                  "l"(gmem_src)

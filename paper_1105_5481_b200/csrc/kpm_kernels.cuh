@@ -157,16 +157,17 @@ struct StencilOp {
     }
 };
 
-// General sparse H~ in ELL form: K entries per row, [K][ld] arrays (row stride ld >= D, a multiple
-// of 2048 so that every tile slice of an entry column is an aligned run for bulk copies), values
-// pre-scaled by 1/a, the -b/a shift applied separately.  Padding: col = row, val = 0.
+// General sparse H~ in ELL form, row-major: row i holds kp >= K entries (K rounded up to a multiple
+// of 4: one 16-byte load brings 4 column indices) -- [rows][kp] arrays, values pre-scaled by 1/a, the
+// -b/a shift applied separately.  Padding: col = row, val = 0.  A tile of consecutive rows is one
+// contiguous run of both arrays (one bulk copy each into shared memory, kpm_ell.cuh).
 template <bool CPLX>
 struct EllOp {
     int D, K;
-    const int* col;       // [K][ld]
-    const double* val;    // real: double[K][ld]; complex: double2[K][ld]
+    const int* col;       // [rows][kp]
+    const double* val;    // real: double[rows][kp]; complex: double2[rows][kp]
     double shift;         // -b / a
-    int ld;               // row stride of the entry columns
+    int kp;               // entries per stored row (row stride)
     template <class XF>
     __device__ __forceinline__ double2 apply(int s, const XF& X, double2 xs) const {
         double2 h = scale2(shift, xs);
@@ -179,7 +180,7 @@ struct EllOp {
 #pragma unroll
             for (int u = 0; u < CH; ++u) {
                 const int k = k0 + u;
-                const size_t e = (size_t)(k < K ? k : K - 1) * ld + s;
+                const size_t e = (size_t)s * kp + (k < K ? k : K - 1);
                 j[u] = __ldg(col + e);
                 v[u] = CPLX ? __ldg(reinterpret_cast<const double2*>(val) + e) : make_double2(__ldg(val + e), 0.0);
                 if (k >= K) v[u] = make_double2(0.0, 0.0);
