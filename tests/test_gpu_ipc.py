@@ -93,6 +93,8 @@ ROWS = {
     "2d_odd_N": dict(ndim=2, L=[64, 40], W=0.0, flux=0.0, N=31, R=32, seed=3),
     # complex128 Peierls lattice (flux 1/8), slabs along y
     "2d_peierls": dict(ndim=2, L=[64, 24], W=1.0, flux=0.125, N=28, R=16, seed=4),
+    # uneven slabs (10 planes over 3 ranks: 3, 3, 4), 16-lane box tiles
+    "3d_uneven_slabs": dict(ndim=3, L=[16, 8, 10], W=2.0, flux=0.0, N=19, R=32, seed=8),
 }
 
 
