@@ -319,7 +319,9 @@ kpm_status init_comm(kpm_handle_s* h, const kpm_dist* dist) {
 std::mutex g_attr_mu;
 std::map<std::pair<const void*, int>, size_t> g_attr;
 kpm_status set_smem(const void* kern, size_t smem, int device) {
-    if (smem <= 48 * 1024) return KPM_OK;
+    // (raised for any request above 32 KB: the 48 KB default covers dynamic AND static shared memory,
+    // so a dynamic request of exactly 48 KB plus a kernel's static barriers failed to launch)
+    if (smem <= 32 * 1024) return KPM_OK;
     std::lock_guard<std::mutex> lk(g_attr_mu);
     size_t& done = g_attr[{kern, device}];
     if (done >= smem) return KPM_OK;
@@ -685,13 +687,14 @@ kpm::StencilGeom stencil_geom(const kpm_handle_s* h) {
 template <bool CPLX>
 kpm_status launch_ell_t(kpm_handle_s* h, const Plan& p, const kpm::VecArgs& v, int tail) {
     dim3 block(p.TR, p.TS), grid(p.gx, p.gy);
-    const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX);
+    const bool spw8 = h->ell_kp == 8 && kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX, kpm::kEllSPW8) <= (size_t)h->smem_optin;
+    const size_t smem = kpm::ell_smem_bytes(kThreads, p.TS, h->K, CPLX, spw8 ? kpm::kEllSPW8 : kpm::kEllSPW);
     const bool wide = (double)(h->D + h->n_ghost) * p.RG >= 2147483648.0;  // 32-bit element offsets otherwise
     auto pick = [&](auto w) {
         constexpr bool W = decltype(w)::value;
         switch (h->ell_kp) {
             case 4: return kpm::kpm_ell_step_kernel<CPLX, 4, W>;
-            case 8: return kpm::kpm_ell_step_kernel<CPLX, 8, W>;
+            case 8: return spw8 ? kpm::kpm_ell_step_kernel<CPLX, 8, W, kpm::kEllSPW8> : kpm::kpm_ell_step_kernel<CPLX, 8, W>;
             case 12: return kpm::kpm_ell_step_kernel<CPLX, 12, W>;
             default: return kpm::kpm_ell_step_kernel<CPLX, 16, W>;
         }

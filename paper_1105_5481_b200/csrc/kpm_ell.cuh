@@ -37,23 +37,24 @@ __device__ __forceinline__ double2 ldg_hint(const double2* p, uint64_t pol) {
 }
 
 constexpr int kEllKMax = 16;  // rows with more entries use the generic step kernel
-constexpr int kEllSPW = 4;    // rows per thread row per tile
+constexpr int kEllSPW = 4;    // rows per thread row per tile (KP = 8: kEllSPW8, when it fits)
+constexpr int kEllSPW8 = 16;  // (c3 via CSR: 1683 -> 1556 ms per call -- a quarter of the tile barriers)
 
 __host__ __device__ inline int ell_kp(int K) { return (K + 3) / 4 * 4; }  // stored entries per row
 
-__host__ __device__ inline size_t ell_smem_bytes(int nthr, int TS, int K, bool cplx) {
-    const size_t tile = (size_t)TS * kEllSPW, KP = (size_t)ell_kp(K);
+__host__ __device__ inline size_t ell_smem_bytes(int nthr, int TS, int K, bool cplx, int spw = kEllSPW) {
+    const size_t tile = (size_t)TS * spw, KP = (size_t)ell_kp(K);
     return 3 * (size_t)nthr * 16 + (2 * KP * tile * 4 + 15) / 16 * 16 + 2 * KP * tile * (cplx ? 16 : 8);
 }
 
 // KP: stored entries per row (4, 8, 12 or 16).  U rows per thread are processed together -- all
 // their gathers issued before any is consumed -- so a thread keeps U (KP + 2) 16-byte loads in
 // flight.  One 512-thread CTA per SM (128 registers hold the loads in flight).
-template <bool CPLX, int KP, bool WIDE>
+template <bool CPLX, int KP, bool WIDE, int SPW = kEllSPW>
 __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> op, const VecArgs v, const int tail) {
     pdl_entry();
     constexpr int U = KP <= 4 ? 4 : (KP <= 8 ? 2 : 1);  // U (KP + 2) double2 in flight: 24, 20, 14-18
-    static_assert(kEllSPW % U == 0 && KP % 4 == 0, "rows per thread, 16-byte index groups");
+    static_assert(SPW % U == 0 && KP % 4 == 0, "rows per thread, 16-byte index groups");
     // element offsets j * RG + rg in 32 bits unless the extended block has 2^31 lanes or more (WIDE)
     using off_t = typename std::conditional<WIDE, long long, unsigned>::type;
     const int TR = blockDim.x, TS = blockDim.y;
@@ -62,7 +63,7 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
     const bool active = rg < v.RG;
     const int D = op.D;
     const off_t RG = (off_t)v.RG;
-    const int TILE = TS * kEllSPW;
+    const int TILE = TS * SPW;
     extern __shared__ double2 sred[];                                     // [3][nthr]
     int* scol = reinterpret_cast<int*>(sred + 3 * nthr);                 // [2][TILE][KP]
     const size_t vofs = ((size_t)2 * KP * TILE * 4 + 15) / 16 * 16;
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(512, 1) kpm_ell_step_kernel(const EllOp<CPLX> 
         const int nrow = min(TILE, D - tile * TILE);
         const off_t row0 = (off_t)tile * TILE;
 #pragma unroll 1
-        for (int u0 = 0; u0 < kEllSPW; u0 += U) {
+        for (int u0 = 0; u0 < SPW; u0 += U) {
             int ii[U];
             double2 x[U], p[U], xj[U][KP];
 #pragma unroll
