@@ -571,3 +571,37 @@ def test_three_step_kernel(kpm, case, N):
         _, launches, _ = h.last_timing()
         rem = nsteps % 3
         assert launches == nsteps // 3 + (1 if rem else 0), (launches, nsteps)
+
+
+def random_sparse_k(D, K, seed, cplx):
+    """Random Hermitian H with at most K stored entries per row (ELL width K): a random symmetric
+    bond pattern of degree <= K - 1 plus the diagonal."""
+    rng = np.random.default_rng(seed)
+    A = np.zeros((D, D), dtype=np.complex128 if cplx else np.float64)
+    deg = np.zeros(D, dtype=int)
+    for i in rng.permutation(D):
+        for j in rng.choice(D, size=K, replace=False):
+            if i != j and deg[i] < K - 1 and deg[j] < K - 1 and A[i, j] == 0:
+                v = rng.normal() + (1j * rng.normal() if cplx else 0.0)
+                A[i, j], A[j, i] = v, np.conj(v)
+                deg[i] += 1
+                deg[j] += 1
+    A[np.diag_indices(D)] = rng.normal(size=D)
+    return oracle.csr_from_dense(A)
+
+
+@pytest.mark.parametrize("K", [3, 5, 9, 14, 16])
+@pytest.mark.parametrize("cplx", [False, True])
+@pytest.mark.parametrize("R", [7, 64])
+def test_ell_kernel_entry_widths(kpm, K, cplx, R):
+    """The staged ELL kernel for every stored width KP = 4, 8 (256-row tiles), 12, 16 (K rounded up to
+    a multiple of 4, padding entries (row, 0)), real and complex, ragged last tile, 1-2 lane groups."""
+    H = random_sparse_k(1300, K, 11 + K, cplx)
+    a, b = oracle.gershgorin(H)
+    N = 22
+    ref = oracle.moments_doubling(H, a, b, ki.rademacher(6, R, H.D), N)
+    val = H.val_re + 1j * H.val_im if H.is_complex else H.val_re
+    h = kpm.kpm_create_csr(H.D, H.rowptr, H.col, val, a, b)
+    h.set_plan_opts(no_small=1)
+    assert normwise(h.moments(N, R, 6), ref) < TOL
+    assert np.array_equal(h.moments(N, R, 6), h.moments(N, R, 6)), "not deterministic"
